@@ -1,0 +1,365 @@
+"""Pins for the fp64 oracle (oracle/): each test ties an oracle function to something other than
+itself -- a closed form, an identity of the mathematics, a textbook special case, a brute-force
+evaluation of the paper's defining integral, or a hand-derived golden fixture.  The comment on each
+test names the plausible oracle mistake it would catch.  CPU only (-m "not gpu")."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ref
+from synth import make_dataset, radial_grid
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _load_gold(name):
+    return np.loadtxt(os.path.join(GOLD, name), comments="#")
+
+
+def _rand_rings(rng, n, R, Q):
+    return rng.standard_normal((n, R, Q)) + 1j * rng.standard_normal((n, R, Q))
+
+
+def _all_pairs(na, nb):
+    ia, ib = np.meshgrid(np.arange(na), np.arange(nb), indexing="ij")
+    return ia.ravel(), ib.ravel()
+
+
+def _rand_orth(rng, R):
+    q, _ = np.linalg.qr(rng.standard_normal((R, R)))
+    return q
+
+
+# ------------------------------------------------------------------ radial quadrature (harness)
+def test_gauss_jacobi_golden_R2():
+    """Hand-derived 2-point Gauss-Jacobi(0,1) rule. Catches a wrong (alpha,beta)
+    or a wrong k/w mapping in the generator."""
+    g = _load_gold("gauss_jacobi_R2.txt")
+    k, w = radial_grid(2)
+    np.testing.assert_allclose(k, g[:, 3], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(w, g[:, 4], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("R", [3, 16, 64, 128])
+def test_radial_quadrature_exactness(R):
+    """sum_r w_r p(k_r) = int_0^K p(k) k dk for deg p <= 2R-1; sum w = K^2/2."""
+    k, w = radial_grid(R)
+    K = R - 1
+    assert abs(w.sum() - K * K / 2) <= 1e-12 * K * K
+    for n in [1, 2, R, 2 * R - 1]:
+        # int_0^K (k/K)^n k dk / K^2 = 1 / (n + 2)
+        approx = (w * (k / K) ** n).sum() / (K * K)
+        assert abs(approx - 1.0 / (n + 2)) <= 1e-11 / (n + 2)
+
+
+# ------------------------------------------------------------------ O1 / O2 / P8
+def test_P5_single_ring_closed_form():
+    """P5: one-ring content gives X_k = 2 pi w_r e^{-i p gamma_k} (golden).  Catches a missing dpsi,
+    a conj on the wrong operand (would flip the phase sign) or a wrong shift direction."""
+    g = _load_gold("single_ring_landscape.txt")
+    R, Q, p = 3, 8, 2
+    w = np.array([0.5, 1.25, 2.0])
+    psi = 2 * np.pi * np.arange(Q) / Q
+    a = np.zeros((1, R, Q), complex)
+    a[0, 1] = np.exp(1j * p * psi)
+    X = ref.landscape_full(a, a, w, [0], [0])[0]
+    np.testing.assert_allclose(X.real, g[:, 1], atol=1e-13)
+    np.testing.assert_allclose(X.imag, g[:, 2], atol=1e-13)
+
+
+def test_P2_on_grid_rotation_peaks_at_k0():
+    """P2: image = template rotated by +gamma_k0 (a[r,j] = b[r,(j-k0)]) peaks at
+    k0 with X = ||b||_w^2 exactly (Cauchy-Schwarz).  Catches a reversed shift (peak at Q-k0)."""
+    rng = np.random.default_rng(1)
+    R, Q = 5, 32
+    k, w = radial_grid(R)
+    b = _rand_rings(rng, 1, R, Q)
+    for k0 in [0, 1, 7, 31]:
+        a = np.roll(b, k0, axis=-1)                 # a[j] = b[j - k0]
+        X = ref.landscape_full(a, b, w, [0], [0])[0]
+        assert ref.argmax_first(X.real) == k0
+        nb = (w[:, None] * (2 * np.pi / Q) * np.abs(b[0]) ** 2).sum()
+        assert abs(X[k0] - nb) <= 1e-13 * nb
+
+
+def test_P2_analytic_rotation_generator():
+    """P2 via the analytic generator: a noiseless image whose planted angle is on-grid equals the
+    template cyclically shifted (A2), and its landscape peaks at that index."""
+    d = make_dataset("tiny", complex128=True, noise=False)
+    Q = d.Q
+    m = 3
+    t = int(d.t_true[m])
+    k0 = int(round(float(d.gamma[m]) / (2 * np.pi / Q))) % Q
+    # re-evaluate that image exactly on-grid by using the planted template with a cyclic shift
+    b = d.templates[t].numpy()
+    a_shift = np.roll(b, k0, axis=-1)[None]
+    X = ref.landscape_full(a_shift, b[None], d.w.numpy(), [0], [0])[0]
+    assert ref.argmax_first(X.real) == k0
+    # the off-grid analytic image peaks within one sample of its planted angle
+    Xo = ref.landscape_full(d.images.numpy()[m:m + 1], b[None], d.w.numpy(), [0], [0])[0]
+    kk = ref.argmax_first(Xo.real)
+    g = float(d.gamma[m]) / (2 * np.pi / Q)
+    assert min(abs(kk - g), Q - abs(kk - g)) <= 1.0
+
+
+def test_P8_fourier_bessel_form_equals_direct_sum():
+    """P8: Eq. image_innerproduct_0 with the direct DFT and ahat = DFT/Q (G1)
+    equals O1.  Catches a 2 pi / dpsi normalization slip or the inverse-FFT sign (G3)."""
+    rng = np.random.default_rng(2)
+    for (R, Q) in [(4, 16), (7, 24), (3, 64)]:
+        k, w = radial_grid(R)
+        A = _rand_rings(rng, 3, R, Q)
+        B = _rand_rings(rng, 2, R, Q)
+        ia, ib = _all_pairs(3, 2)
+        X1 = ref.landscape_full(A, B, w, ia, ib)
+        X8 = ref.landscape_fb(A, B, w, ia, ib)
+        assert np.abs(X1 - X8).max() <= 1e-13 * np.abs(X1).max()
+
+
+def test_P1_full_rank_equals_uncompressed():
+    """P1: H = R with ANY orthogonal U reproduces O1.  Catches eta_r = sqrt(w dpsi)
+    (would scale by dpsi, G2) or a missing sqrt(w)."""
+    rng = np.random.default_rng(3)
+    R, Q = 9, 32
+    k, w = radial_grid(R)
+    A = _rand_rings(rng, 2, R, Q)
+    B = _rand_rings(rng, 3, R, Q)
+    U = _rand_orth(rng, R)
+    ia, ib = _all_pairs(2, 3)
+    X1 = ref.landscape_full(A, B, w, ia, ib)
+    X2 = ref.landscape_rank(A, B, w, U, ia, ib)
+    assert np.abs(X1 - X2).max() <= 1e-13 * np.abs(X1).max()
+
+
+def test_P3_parseval_over_q():
+    """P3: sum_k |X_k|^2 = 4 pi^2 Q sum_q |S_q|^2 with S_q = sum_r w_r conj(ahat) bhat (direct DFT),
+    and ring Plancherel sum_j |a_j|^2 dpsi = 2 pi sum_q |ahat_q|^2."""
+    rng = np.random.default_rng(4)
+    R, Q = 6, 40
+    k, w = radial_grid(R)
+    A = _rand_rings(rng, 1, R, Q)
+    B = _rand_rings(rng, 1, R, Q)
+    X = ref.landscape_full(A, B, w, [0], [0])[0]
+    j = np.arange(Q)
+    F = np.exp(-2j * np.pi * np.outer(j, j) / Q)
+    ah = A[0] @ F.T / Q
+    bh = B[0] @ F.T / Q
+    S = (w[:, None] * np.conj(ah) * bh).sum(0)
+    lhs = (np.abs(X) ** 2).sum()
+    rhs = 4 * np.pi ** 2 * Q * (np.abs(S) ** 2).sum()
+    assert abs(lhs - rhs) <= 1e-12 * rhs
+    ring = (np.abs(A[0]) ** 2).sum(1) * (2 * np.pi / Q)
+    assert np.allclose(ring, 2 * np.pi * (np.abs(ah) ** 2).sum(1), rtol=1e-13)
+
+
+def test_P4_mean_over_gamma():
+    """P4: (1/Q) sum_k X_k = 2 pi sum_r w_r conj(abar_r) bbar_r (ring means)."""
+    rng = np.random.default_rng(5)
+    R, Q = 4, 16
+    k, w = radial_grid(R)
+    A = _rand_rings(rng, 1, R, Q)
+    B = _rand_rings(rng, 1, R, Q)
+    X = ref.landscape_full(A, B, w, [0], [0])[0]
+    rhs = 2 * np.pi * (w * np.conj(A[0].mean(1)) * B[0].mean(1)).sum()
+    assert abs(X.mean() - rhs) <= 1e-13 * abs(X).max()
+
+
+def test_P6_conjugate_symmetry():
+    """P6: X(gamma; A, B) = conj X(-gamma; B, A).  Catches conj applied to the shifted operand."""
+    rng = np.random.default_rng(6)
+    R, Q = 5, 16
+    k, w = radial_grid(R)
+    A = _rand_rings(rng, 1, R, Q)
+    B = _rand_rings(rng, 1, R, Q)
+    Xab = ref.landscape_full(A, B, w, [0], [0])[0]
+    Xba = ref.landscape_full(B, A, w, [0], [0])[0]
+    minus = (-np.arange(Q)) % Q
+    assert np.abs(Xab - np.conj(Xba[minus])).max() <= 1e-13 * np.abs(Xab).max()
+
+
+def test_P11_hermitian_data_gives_real_landscape():
+    """P11: noiseless templates are Fourier transforms of real functions, so X is real
+    (PAPER.md:410-411 conjugacy); Im X <= 1e-13 max|X|."""
+    d = make_dataset("tiny", complex128=True, noise=False)
+    B = d.templates.numpy()
+    ia, ib = _all_pairs(B.shape[0], B.shape[0])
+    X = ref.landscape_full(B, B, d.w.numpy(), ia, ib)
+    assert np.abs(X.imag).max() <= 1e-13 * np.abs(X).max()
+
+
+def test_P10_whole_tiny_config_brute_force():
+    """P10: whole Tiny config: O1, O2 at H = R (oracle basis) and P8 agree on all 64 pairs."""
+    d = make_dataset("tiny")
+    A, B, w = d.images.numpy(), d.templates.numpy(), d.w.numpy()
+    ia, ib = _all_pairs(8, 8)
+    X1 = ref.landscape_full(A, B, w, ia, ib)
+    U, lam = ref.basis(ref.kernel_C(B, w), d.R)
+    X2 = ref.landscape_rank(A, B, w, U, ia, ib)
+    X8 = ref.landscape_fb(A, B, w, ia, ib)
+    s = np.abs(X1).max()
+    assert np.abs(X1 - X2).max() <= 1e-12 * s
+    assert np.abs(X1 - X8).max() <= 1e-12 * s
+
+
+def test_rank_landscape_depends_only_on_projector():
+    """O2 depends on U only through P = U U^T: rotating the basis inside its span changes nothing."""
+    rng = np.random.default_rng(7)
+    R, Q, H = 8, 16, 3
+    k, w = radial_grid(R)
+    A = _rand_rings(rng, 2, R, Q)
+    B = _rand_rings(rng, 2, R, Q)
+    U = _rand_orth(rng, R)[:, :H]
+    Rh = _rand_orth(rng, H)
+    ia, ib = _all_pairs(2, 2)
+    X = ref.landscape_rank(A, B, w, U, ia, ib)
+    Y = ref.landscape_rank(A, B, w, U @ Rh, ia, ib)
+    assert np.abs(X - Y).max() <= 1e-13 * np.abs(X).max()
+
+
+# ------------------------------------------------------------------ O3 kernel / basis
+def test_kernel_golden_single_frequency_rings():
+    """O3 on single-frequency rings (golden): catches including q = 0 (ring 2 would be nonzero),
+    using w instead of sqrt(w) sqrt(w') off the diagonal, or a 1/Q^2 normalization slip."""
+    g = _load_gold("two_ring_kernel.txt")
+    R, Q = 3, 16
+    w = np.array([1.0, 2.0, 3.0])
+    c = np.array([1 + 1j, 2.0, 0.5j])
+    p = np.array([3, 3, 0])
+    psi = 2 * np.pi * np.arange(Q) / Q
+    b = (c[:, None] * np.exp(1j * p[:, None] * psi[None, :]))[None]
+    np.testing.assert_allclose(ref.kernel_C(b, w), g, atol=1e-14)
+
+
+def test_kernel_equals_brute_force_rotation_average():
+    """Eq. Image_single_kern brute force: average over on-grid gamma, gamma' of
+    sum_q [R_g b - R_g' b]^dagger [R_g b' - R_g' b'] dpsi, weights sqrt(w_r w_r'), equals C up to
+    one positive constant.  Catches a kernel that forgets the q = 0 exclusion (:665)."""
+    rng = np.random.default_rng(8)
+    R, Q, T = 4, 12, 3
+    k, w = radial_grid(R)
+    Bt = _rand_rings(rng, T, R, Q) + 3.0            # strong ring means (q = 0 content)
+    brute = np.zeros((R, R))
+    for t in range(T):
+        x = np.sqrt(w)[:, None] * Bt[t]
+        for g in range(Q):
+            for gp in range(Q):
+                d = np.roll(x, g, axis=1) - np.roll(x, gp, axis=1)
+                brute += (np.conj(d) @ d.T).real
+    brute /= T
+    C = ref.kernel_C(Bt, w)
+    scale = brute.trace() / C.trace()
+    assert scale > 0
+    assert np.abs(brute - scale * C).max() <= 1e-10 * np.abs(brute).max()
+
+
+def test_P9_kernel_symmetric_psd_rotation_invariant():
+    """P9: C symmetric PSD; invariant under rotating any template (phase cancellation, SPEC-style
+    invariant); trace = sum of eigenvalues."""
+    d = make_dataset("tiny", complex128=True, noise=False)
+    B, w = d.templates.numpy(), d.w.numpy()
+    C = ref.kernel_C(B, w)
+    assert np.abs(C - C.T).max() == 0.0
+    U, lam = ref.basis(C, d.R)
+    assert lam.min() >= -1e-12 * lam.max()
+    assert abs(lam.sum() - np.trace(C)) <= 1e-12 * abs(np.trace(C))
+    Br = B.copy()
+    Br[2] = np.roll(Br[2], 5, axis=-1)
+    Br[5] = np.roll(Br[5], 17, axis=-1)
+    assert np.abs(ref.kernel_C(Br, w) - C).max() <= 1e-13 * np.abs(C).max()
+    res = np.linalg.norm(C @ U - U * lam[None, :])
+    assert res <= 1e-12 * lam[0]
+
+
+def test_P7_truncation_bounded_by_eigenvalues():
+    """P7 (i) Eckart-Young: sum_t ||(I-P_H) B'_t||^2 over q != 0 = T sum_{h>H} lambda_h;
+    (ii) per pair max_k |dX_k - dX^(q=0)| <= 2 pi ||(I-P)A'||_F ||(I-P)B'||_F (q != 0 norms).
+    Catches a kernel with the wrong weights or with q = 0 included."""
+    d = make_dataset("tiny")
+    A, B, w = d.images.numpy(), d.templates.numpy(), d.w.numpy()
+    T, R, Q = B.shape
+    C = ref.kernel_C(B, w)
+    for H in [1, 2, 4, 8]:
+        U, lam = ref.basis(C, H)
+        P = ref.projector(U)
+        Bp = np.sqrt(w)[None, :, None] * ref.fb_coefficients(B)
+        resid = np.einsum("rs,tsq->trq", np.eye(R) - P, Bp)[:, :, 1:]
+        lhs = (np.abs(resid) ** 2).sum()
+        rhs = T * lam[H:].sum()
+        assert abs(lhs - rhs) <= 1e-10 * max(rhs, 1e-300) + 1e-12 * lam[0]
+        ia, ib = _all_pairs(A.shape[0], T)
+        Xf = ref.landscape_full(A, B, w, ia, ib)
+        Xh = ref.landscape_rank(A, B, w, U, ia, ib)
+        Ap = np.sqrt(w)[None, :, None] * ref.fb_coefficients(A)
+        ra = np.einsum("rs,tsq->trq", np.eye(R) - P, Ap)
+        rb = np.einsum("rs,tsq->trq", np.eye(R) - P, Bp)
+        dq0 = 2 * np.pi * (np.conj(ra[ia, :, 0]) * rb[ib, :, 0]).sum(1)
+        lhs2 = np.abs((Xf - Xh) - dq0[:, None]).max(1)
+        na = np.sqrt((np.abs(ra[:, :, 1:]) ** 2).sum((1, 2)))
+        nb = np.sqrt((np.abs(rb[:, :, 1:]) ** 2).sum((1, 2)))
+        bound = 2 * np.pi * na[ia] * nb[ib]
+        assert np.all(lhs2 <= bound * (1 + 1e-9) + 1e-12 * np.abs(Xf).max())
+
+
+# ------------------------------------------------------------------ O4 / O5
+def test_O4_reductions_tie_breaks():
+    x = np.array([[1.0, 3.0, 3.0, 2.0], [5.0, 5.0, 5.0, 5.0]])
+    assert list(ref.argmax_first(x)) == [1, 0]
+    assert list(ref.top2_gap(np.array([[1.0, 4.0, 2.5]]))) == [1.5]
+    Xre = np.array([[1.0, 7.0], [7.0, 0.0]])            # tie between (t0,k1) and (t1,k0)
+    assert ref.per_image_winner(Xre) == (7.0, 0, 1)
+    assert bool(ref.near_tie_ok(np.array([1.0, 2.0, 1.999]), np.array(2), 0.01))
+    assert not bool(ref.near_tie_ok(np.array([1.0, 2.0, 1.9]), np.array(2), 0.01))
+
+
+def test_O5_metrics_identities():
+    """Frobenius / correlation / backward-error f identities."""
+    rng = np.random.default_rng(9)
+    full = rng.standard_normal((5, 16))
+    assert ref.rel_frobenius(full, full) == 0.0
+    assert abs(ref.rel_frobenius(np.zeros_like(full), full) - 1.0) < 1e-15
+    assert abs(ref.rel_frobenius(2 * full, full) - 1.0) < 1e-15
+    assert abs(ref.correlation(full, full) - 1.0) < 1e-14
+    assert abs(ref.correlation(-full, full) + 1.0) < 1e-14
+    assert abs(ref.correlation(3 * full + 7, full) - 1.0) < 1e-14
+    assert np.all(ref.backward_fraction(full, full) == 1.0)
+    # literal counting loop
+    appr = rng.standard_normal((5, 16))
+    f = ref.backward_fraction(appr, full)
+    for p in range(5):
+        ke = int(np.argmax(appr[p]))
+        assert f[p] == sum(1 for k in range(16) if full[p, k] <= full[p, ke]) / 16
+
+
+# ------------------------------------------------------------------ generator (harness)
+def test_noise_variance_calibration():
+    """Per-node noise variance = sigma_hat^2 / (w_r dpsi) within 2% (G11)."""
+    d0 = make_dataset("small", M=32, T=4, noise=False, complex128=True)
+    d1 = make_dataset("small", M=32, T=4, noise=True, complex128=True)
+    nz = (d1.images - d0.images).numpy()
+    Q = d1.Q
+    var = (np.abs(nz) ** 2).mean(axis=(0, 2))                 # per ring
+    expect = d1.sigma_hat2 / (d1.w.numpy() * 2 * np.pi / Q)
+    np.testing.assert_allclose(var, expect, rtol=0.06)       # 4096 samples per ring
+    pooled = (np.abs(nz) ** 2 / expect[None, :, None]).mean()
+    assert abs(pooled - 1.0) < 0.02                           # 131072 samples
+    # SNR definition G11: Pbar / E||noise||_w^2 = SNR
+    assert abs(d1.meta["pbar"] / (d1.sigma_hat2 * d1.R * Q) - 0.5) < 1e-12
+
+
+def test_generator_rotation_is_cyclic_shift():
+    """A2: evaluating the analytic slice at psi - 2 pi k0/Q equals the cyclic
+    shift of the unrotated samples (to fp64 rounding)."""
+    import torch
+    from synth.generator import _slice_rows, molecule_centres, view_frames
+    k, w = radial_grid(8)
+    kt = torch.tensor(k)
+    c = torch.tensor(molecule_centres(0, 5))
+    e1, e2 = view_frames(0, 2, "random")
+    p1 = torch.tensor(e1) @ c.T
+    p2 = torch.tensor(e2) @ c.T
+    Q, k0 = 32, 5
+    b0 = _slice_rows(p1, p2, torch.zeros(2, dtype=torch.float64), kt, Q).numpy()
+    b1 = _slice_rows(p1, p2, torch.full((2,), 2 * np.pi * k0 / Q, dtype=torch.float64), kt, Q).numpy()
+    assert np.abs(b1 - np.roll(b0, k0, axis=-1)).max() <= 1e-12 * np.abs(b0).max()
