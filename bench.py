@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""bench.py -- many-to-many radial-SVD rotational alignment on B200 (arXiv 2202.07235 hot path).
+
+One "step" = one pass of the whole hot path over one batch of
+synthetic input resident in HBM:
+  a0 kernel-matrix partials on the rank's template shard -> all-gather (G > 1) -> reduce -> host
+     eigen-solver -> U;
+  a1 compress all images and the rank's template shard;
+  a2-a4 contraction + length-Q FFT + per-image argmax (packed keys, t_offset = shard start);
+  G > 1: all-gather of the per-image keys (NCCL over NVLink) + combine kernel.
+value = M * T pairs / step time (whole job, max over ranks, CUDA events).  Templates are sharded
+over the ranks (total work fixed: "strong" scaling).  Default workload: the Large config
+(BASELINE.json configs[3]: R=128, Q=512, H=24, M=16384, T=8192), the configuration the north star's
+scaling target is stated on; DESIGN.md explains the choice.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config large] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from synth import CONFIGS, make_dataset, sample_pairs  # noqa: E402
+
+METRIC = "image–template pairs/s (full landscape over Q angles) at rank H; % roofline"
+UNIT = "pairs/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="large", choices=list(CONFIGS))
+    p.add_argument("--H", type=int, default=None)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            ident = str(self.dev)
+            try:
+                uuid = str(torch.cuda.get_device_properties(self.dev).uuid)
+                ident = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+            except Exception:
+                pass
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", ident, f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ helpers
+def flops_per_pair(H: int, Q: int):
+    """SURVEY.md §8(d) algorithmic FLOPs per pair: contraction 8HQ + FFT 5 Q log2 Q."""
+    return 8 * H * Q, 5 * Q * math.log2(Q)
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ oracle (cpu baseline / reference arm)
+def oracle_pairs_per_s(A, B, w, U, m, t, seconds: float):
+    """Time the fp64 oracle (O2 direct sum, as it stands) on sampled pairs; grow the sample until
+    it takes ~`seconds`.  Returns (pairs/s, pairs timed, threads, seconds)."""
+    from oracle import ref
+    threads = os.cpu_count() or 1
+    n = 4
+    while True:
+        n = min(n, len(m))
+        t0 = time.perf_counter()
+        X = ref.landscape_rank(A, B, w, U, m[:n], t[:n], nthreads=threads)
+        _ = ref.argmax_first(X.real)
+        dt = time.perf_counter() - t0
+        if dt >= seconds * 0.5 or n >= len(m):
+            return n / dt, n, threads, dt
+        n = int(min(len(m), max(2 * n, n * seconds / max(dt, 1e-3))))
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    from paper_2202_07235_b200 import api
+    from paper_2202_07235_b200 import dist as pdist
+
+    world, rank, local = dist_setup()
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[args.config]
+    H = args.H or cfg["H"][0]
+    Q, R = cfg["Q"], cfg["R"]
+    chunk = api.kernel_chunk()
+    T = cfg["T"]
+    t0, t1 = pdist.shard_range(T, world, rank, chunk)
+    tg0 = time.perf_counter()
+    ds = make_dataset(args.config, device=dev, t_range=(t0, t1))
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - tg0
+    images, tmpl = ds.images, ds.templates
+    M = images.shape[0]
+    T_loc = tmpl.shape[0]
+    w_dev = ds.w.contiguous()
+    ib = torch.empty(api.block_bytes(M, Q, H) // 4, dtype=torch.float32, device=dev)
+    tb = torch.empty(max(api.block_bytes(T_loc, Q, H), 16) // 4, dtype=torch.float32, device=dev)
+    work = torch.empty(api.align_workspace_bytes(M, T_loc, Q, H) // 4, dtype=torch.float32, device=dev)
+    keys = torch.zeros(M, dtype=torch.int64, device=dev)
+    U_dev = torch.zeros((R, H), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    ev = {}
+
+    def mark(name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        ev[name] = e
+
+    def step(imgs, tmps, record=False):
+        if record:
+            mark("start")
+        U, lam = pdist.basis_from_shards(tmps, T, w_dev, H)         # a0 (syncs for the host solve)
+        U_dev.copy_(torch.from_numpy(U), non_blocking=False)
+        if record:
+            mark("basis")
+        api.compress(imgs, w_dev, U_dev, api.SIDE_IMAGE, out=ib)      # a1
+        if T_loc:
+            api.compress(tmps, w_dev, U_dev, api.SIDE_TEMPLATE, out=tb)
+        if record:
+            mark("compress")
+        api.winners_reset(keys)                                       # a2-a4
+        if T_loc:
+            api.align_argmax(ib, M, tb, T_loc, Q, H, api.PER_IMAGE, work, best_key=keys, t_offset=t0)
+        if record:
+            mark("align")
+        out = pdist.combine_keys(keys, Q)                             # all-gather + combine
+        if record:
+            mark("combine")
+        return out, U
+
+    for _ in range(args.warmup):
+        step(images, tmpl)
+    torch.cuda.synchronize()
+    barrier(world)
+
+    clocks = Clocks(local)
+    clocks.start()
+    phase = {k: 0.0 for k in ["basis", "compress", "align", "combine"]}
+    api.timing_read()
+    api.timing_enable(True)
+    n0 = api.launch_count()
+    barrier(world)
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    last_U = None
+    for _ in range(args.steps):
+        out, last_U = step(images, tmpl, record=True)
+    end.record(stream)
+    torch.cuda.synchronize()
+    elapsed_ms = start.elapsed_time(end)
+    barrier(world)
+    launches = api.launch_count() - n0
+    api.timing_enable(False)
+    ktime = api.timing_read()
+    clk = clocks.stop()
+    # per-phase of the last step
+    names = ["start", "basis", "compress", "align", "combine"]
+    for a, b in zip(names[:-1], names[1:]):
+        phase[b] = ev[a].elapsed_time(ev[b])
+    ms_step = max_over_ranks(elapsed_ms / args.steps, world)
+    launches_all = int(sum_over_ranks(launches, world))
+    pairs = M * T
+    value = pairs / (ms_step / 1e3)
+
+    # dominant kernel roofline: the contraction (FP32 SIMT, ALU bound)
+    pk, pk_kind = peaks()
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = sm_count * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12      # TFLOP/s
+    f_contr, f_fft = flops_per_pair(H, Q)
+    c_ms, c_n = ktime["contract"]
+    f_ms, f_n = ktime["fft_reduce"]
+    contr_flops = args.steps * M * T_loc * f_contr
+    achieved = contr_flops / (c_ms / 1e3) / 1e12 if c_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(args.config, {}).get("contract_kernel_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roof = {"bound": "alu", "kernel": "contract_kernel (Step 2 contraction, FP32 SIMT)",
+            "achieved": round(achieved, 3) if achieved else None, "peak": round(fp32_peak, 2),
+            "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4) if achieved else None,
+            "traffic": traffic,
+            "peak_note": f"{sm_count} SMs x 128 FP32 lanes x 2 flop x {pk.get('sm_max_mhz', 1965.0):.0f} MHz "
+                         f"(sm_max_mhz from MEASURED_PEAKS.json, {pk_kind})",
+            "avg_launch_ms": round(c_ms / max(c_n, 1), 4), "launches": c_n,
+            "algorithmic_flops_per_pair": f_contr}
+    t_roof = pairs * (f_contr + f_fft) / (fp32_peak * 1e12) / world
+    step_roof = {"t_roof_ms": round(t_roof * 1e3, 3), "frac": round(t_roof * 1e3 / ms_step, 4),
+                 "definition": "M*T*(8HQ + 5Q log2 Q) / (G * FP32 peak) vs measured step (SURVEY.md 8(d))",
+                 "kernel_ms_per_step": {"contract": round(c_ms / args.steps, 3),
+                                        "fft_reduce": round(f_ms / args.steps, 3),
+                                        "compress": round(ktime["compress"][0] / args.steps, 3),
+                                        "kernel_partials": round(ktime["kernel_partials"][0] / args.steps, 3)}}
+
+    # e2e: host (pinned) rings -> device -> step -> winners back, through the public API
+    e2e = None
+    if not args.no_e2e:
+        try:
+            h_img = torch.empty(images.shape, dtype=images.dtype, pin_memory=True)
+            h_tmp = torch.empty(tmpl.shape, dtype=tmpl.dtype, pin_memory=True)
+            h_img.copy_(images)
+            h_tmp.copy_(tmpl)
+            d_img = torch.empty_like(images)
+            d_tmp = torch.empty_like(tmpl)
+            h_out = [torch.empty(M, dtype=x, pin_memory=True) for x in (torch.float32, torch.int32, torch.int32)]
+            torch.cuda.synchronize()
+            barrier(world)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.e2e_steps):
+                d_img.copy_(h_img, non_blocking=True)
+                d_tmp.copy_(h_tmp, non_blocking=True)
+                (kk, val, tt, k), _ = step(d_img, d_tmp)
+                for h, d in zip(h_out, (val, tt, k)):
+                    h.copy_(d, non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, world)
+            h2d = int(sum_over_ranks(h_img.numel() * 8 + h_tmp.numel() * 8, world))
+            d2h = int(sum_over_ranks(M * 12, world))
+            e2e = {"value": pairs / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": round(e2e_ms, 3),
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+                   "path": "pinned host rings -> cudaMemcpyAsync -> basis/compress/align/combine -> "
+                           "winners (val,t,k) to pinned host"}
+            del h_img, h_tmp, d_img, d_tmp
+        except Exception as exc:  # host memory etc.
+            e2e = {"value": None, "unit": UNIT, "error": str(exc)[:200]}
+
+    # cpu baseline: the oracle as it stands, rank 0 at N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        m, t = sample_pairs(args.config, M, T, 2048, 0)
+        rows_m, inv_m = np.unique(m, return_inverse=True)
+        rows_t, inv_t = np.unique(t, return_inverse=True)
+        A = images[torch.as_tensor(rows_m, device=dev)].cpu().numpy()
+        B = tmpl[torch.as_tensor(rows_t, device=dev)].cpu().numpy()
+        rate, n, thr, secs = oracle_pairs_per_s(A, B, ds.w.cpu().numpy(), last_U, inv_m, inv_t, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "oracle",
+               "sample": f"{n} seeded random (m,t) pairs of the {args.config} workload, O2 rank-{H} fp64 direct "
+                         f"sum (oracle/direct.c, OpenMP) + argmax, library U; {secs:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.config, "M": M, "T": T, "R": R, "Q": Q, "H": H, "mode": "per_image",
+                       "parallelism": f"template-sharded x{world} (NCCL all-gather of winners)",
+                       "l2": "inputs larger than L2 (rings %.1f GB per step)" % ((images.numel() + T * R * Q) * 8 / 1e9),
+                       "seed": 220207235},
+            "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": launches_all, "phases_ms_last_step": {k: round(v, 3) for k, v in phase.items()},
+            "gen_seconds": round(gen_s, 1),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import ref
+    cfg = CONFIGS[args.config]
+    H = args.H or cfg["H"][0]
+    Q, R, T = cfg["Q"], cfg["R"], cfg["T"]
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    # inputs: the same seeded workload (harness generator); oracle basis from a template sample
+    ds = make_dataset(args.config, device=dev)
+    M = ds.images.shape[0]
+    w = ds.w.cpu().numpy()
+    nb = min(T, 512)
+    tb = ds.templates[:nb].cpu().numpy()
+    U, lam = ref.basis(ref.kernel_C(tb, w), H)
+    m, t = sample_pairs(args.config, M, T, 4096, 0)
+    rows_m, inv_m = np.unique(m, return_inverse=True)
+    rows_t, inv_t = np.unique(t, return_inverse=True)
+    A = ds.images[torch.as_tensor(rows_m, device=dev)].cpu().numpy()
+    B = ds.templates[torch.as_tensor(rows_t, device=dev)].cpu().numpy()
+    del ds
+    # size one step to ~cpu_seconds/2 of oracle work
+    rate, n, thr, secs = oracle_pairs_per_s(A, B, w, U, inv_m, inv_t, max(2.0, args.cpu_seconds / 2))
+    n_step = max(1, int(rate * max(2.0, args.cpu_seconds / 2)))
+    n_step = min(n_step, len(inv_m))
+
+    def one_step():
+        X = ref.landscape_rank(A, B, w, U, inv_m[:n_step], inv_t[:n_step], nthreads=thr)
+        return ref.argmax_first(X.real)
+
+    for _ in range(args.warmup):
+        one_step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one_step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = n_step / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": args.config, "M": M, "T": T, "R": R, "Q": Q, "H": H, "mode": "per_pair argmax sample",
+                   "seed": 220207235},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
+                         "sample": f"{n_step} seeded random (m,t) pairs per step; O2 rank-{H} fp64 direct sum + "
+                                   f"argmax, oracle basis (eigh of C from {nb} templates)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

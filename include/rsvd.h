@@ -1,0 +1,170 @@
+/* rsvd.h -- C ABI of the B200 radial-SVD rotational-alignment library (librsvd.so).
+ *
+ * Method: A. Rangan, "Radial-recombination for rigid rotational alignment of images and volumes"
+ * (arXiv 2202.07235).  Citations "PAPER.md:L" refer to lines of that paper's LaTeX source.
+ *
+ * The library computes, for every (image m, template t) pair of polar-Fourier images sampled on a
+ * shared grid of R rings (radial nodes k_r, weights w_r) x Q equispaced angles psi_j = 2 pi j / Q,
+ * the rank-H landscape of inner products over the rotation angles gamma_k = 2 pi k / Q,
+ *
+ *   Re X(gamma_k) = Re[ 2 pi sum_q e^{-2 pi i q k / Q} sum_{h<H} conj(A_q[m,h]) B_q[t,h] ]
+ *                                                       (Eq. image_innerproduct_pm)
+ *
+ * with A_q[m,h] = sum_r U[r,h] sqrt(w_r) ahat_m[r,q] and ahat = (1/Q) DFT over psi (PAPER.md:240-244,
+ * principal image rings PAPER.md:580-585; readings G1/G2), and its per-pair or per-image
+ * maximum over gamma (the maximum-likelihood alignment).  At H = R and any
+ * orthogonal U this equals sum_r w_r dpsi sum_j Re(conj(a[r,j]) b[r,(j-k) mod Q]).
+ *
+ * Conventions (all entry points):
+ *  - Device pointers are CUDA device memory owned by the caller; host pointers are marked (host).
+ *  - Complex data is interleaved float32 (re, im) = 8-byte elements; complex buffers must be 16-byte
+ *    aligned.  Rings are [n][R][Q] row-major, angle fastest.
+ *  - Every call returns rsvd_status; no C++ exception crosses the ABI.  Arguments are validated
+ *    before any launch; on a non-OK return no work was enqueued and rsvd_last_error() (thread-local)
+ *    holds a message.  Launch failures return RSVD_ERR_CUDA; asynchronous device faults surface on
+ *    a later call or stream synchronisation.
+ *  - All device work is enqueued on `stream` (NULL = legacy default stream).  Only
+ *    rsvd_build_basis synchronises (it returns host outputs).  Calls are reentrant across streams.
+ *  - The align path allocates no memory: the caller passes a workspace.  rsvd_build_basis allocates
+ *    scratch with cudaMallocAsync on `stream` and frees it before returning.
+ *  - Supported sizes: Q a power of two in [32, 1024]; 1 <= H <= R <= 256.  Sizes of 0 rows/templates
+ *    are valid empty problems (no work, RSVD_OK).  Negative sizes, NULL or misaligned pointers and
+ *    non-finite or non-positive weights are RSVD_ERR_ARG; unsupported Q/R/H are RSVD_ERR_UNSUPPORTED.
+ */
+#ifndef RSVD_H
+#define RSVD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *rsvd_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    RSVD_OK = 0,
+    RSVD_ERR_ARG = 1,          /* bad size, NULL / misaligned pointer, non-finite weight   */
+    RSVD_ERR_UNSUPPORTED = 2,  /* Q not a power of two in [32,1024], R > 256, H > R, ...  */
+    RSVD_ERR_CUDA = 3,         /* a CUDA runtime call or launch failed                     */
+    RSVD_ERR_NUMERIC = 4       /* non-finite kernel matrix or eigen-solver non-convergence */
+} rsvd_status;
+
+typedef enum { RSVD_SIDE_IMAGE = 0, RSVD_SIDE_TEMPLATE = 1 } rsvd_side;
+typedef enum { RSVD_PER_PAIR = 0, RSVD_PER_IMAGE = 1 } rsvd_reduce;
+
+/* Thread-local message describing the last non-OK status returned on this thread. */
+const char *rsvd_last_error(void);
+/* ABI version of this header (bumped when a signature or the block layout changes). */
+int32_t rsvd_abi_version(void);
+
+/* ------------------------------------------------------------------ sizes */
+/* Bytes of one compressed block buffer holding `rows` images or templates at (Q, H).
+ * The block layout is opaque; read it back only through rsvd_blocks_unpack. */
+int64_t rsvd_block_bytes(int64_t rows, int32_t Q, int32_t H);
+/* Templates per fixed chunk of the kernel-matrix partial sums (rsvd_kernel_partials). */
+int64_t rsvd_kernel_chunk(void);
+/* Bytes of the partial-sum buffer for T templates with R rings: ceil(T/chunk) * R * R doubles. */
+int64_t rsvd_kernel_partials_bytes(int64_t T, int32_t R);
+/* Recommended align workspace bytes for an M x T problem (chunk of the per-pair spectra, sized to
+ * stay resident in L2).  Any size >= rsvd_align_min_workspace_bytes(Q) works. */
+int64_t rsvd_align_workspace_bytes(int64_t M, int64_t T, int32_t Q, int32_t H);
+int64_t rsvd_align_min_workspace_bytes(int32_t Q);
+
+/* ------------------------------------------------------------------ row a0: basis (precompute)
+ * Kernel matrix (Eq. Image_simple_kern PAPER.md:661-665 averaged over targets, Eq.
+ * image_cost_and_kern :704-708, constants dropped, real part; G6):
+ *   C[r][r'] = (1/(T Q)) sqrt(w_r w_r') sum_t Re sum_j W_t[r,j] conj(W_t[r',j]),
+ *   W_t[r,j] = b_t[r,j] - (1/Q) sum_j' b_t[r,j']     (angular mean removed == q = 0 excluded)
+ * and its eigen-decomposition C = V diag(lambda) V^T, lambda descending (the paper's "SVD of C",
+ * :667).  U = first H columns of V.  Sign rule: the largest-|.| entry of each column is positive.
+ *
+ * rsvd_kernel_partials: device, deterministic.  For each fixed chunk c of rsvd_kernel_chunk()
+ *   consecutive templates (the last may be short) writes the un-normalised, unweighted partial
+ *   P_c[r][r'] = sum_{t in c} Re( sum_j b_t[r,j] conj(b_t[r',j]) - (1/Q) S_t[r] conj(S_t[r']) ),
+ *   S_t[r] = sum_j b_t[r,j], in fp64 to partials [ceil(T/chunk)][R][R] (device).  A rank holding
+ *   templates [t0, t0+T) with t0 % chunk == 0 produces exactly the global chunks t0/chunk... so that
+ *   the concatenation over ranks is independent of the sharding.
+ * rsvd_kernel_reduce: device.  Sums partials[0..nchunks) in index order (fixed order => bitwise
+ *   identical for any sharding) and writes C (device fp64 [R][R], exactly symmetric) using the
+ *   device weights w[R] and the global template count T_total.
+ * rsvd_eigen_basis: host only.  Householder tridiagonalisation + implicit QL/QR with Wilkinson
+ *   shifts, fp64, deterministic.  U (host [R][H] row-major), lambda (host [R], may be NULL).
+ * rsvd_build_basis: single-device convenience = partials + reduce + D2H + eigen.  Synchronises. */
+rsvd_status rsvd_kernel_partials(const void *templates, int64_t T, int32_t R, int32_t Q,
+                                 double *partials, rsvd_stream_t stream);
+rsvd_status rsvd_kernel_reduce(const double *partials, int64_t nchunks, int32_t R, int64_t T_total,
+                               int32_t Q, const double *w, double *C, rsvd_stream_t stream);
+rsvd_status rsvd_eigen_basis(const double *C, int32_t R, int32_t H, double *U, double *lambda);
+rsvd_status rsvd_build_basis(const void *templates, int64_t T, int32_t R, int32_t Q,
+                             const double *w_host, int32_t H, double *U_host, double *lambda_host,
+                             rsvd_stream_t stream);
+
+/* ------------------------------------------------------------------ row a1: compress (Step 1)
+ * For each row (image if side == RSVD_SIDE_IMAGE, template otherwise) computes the H principal
+ * image rings' Fourier-Bessel coefficients
+ *   A_q[n,h] = (1/Q) sum_j e^{-2 pi i q j/Q} sum_r U[r,h] sqrt(w_r) a_n[r,j]   (q = 0..Q-1)
+ * (PAPER.md:580-585 with eta_r = sqrt(w_r), reading G2; projection in psi-space then the length-Q
+ * DFT -- the two linear maps commute) and stores them, fp32, in the opaque block layout of `side`.
+ *   rings:  device [n][R][Q] complex64;  w: device fp64 [R];  U: device fp64 [R][H] row-major
+ *   blocks: device, rsvd_block_bytes(n, Q, H) bytes, 16-byte aligned; fully overwritten.
+ * rsvd_blocks_unpack (test/debug): reads blocks back as canonical coefficients
+ *   coeffs: device [n][Q][H] complex64, coeffs[n][q][h] = A_q[n,h]. */
+rsvd_status rsvd_compress(const void *rings, int64_t n, int32_t R, int32_t Q, const double *w,
+                          const double *U, int32_t H, rsvd_side side, void *blocks,
+                          rsvd_stream_t stream);
+rsvd_status rsvd_blocks_unpack(const void *blocks, int64_t n, int32_t Q, int32_t H, rsvd_side side,
+                               void *coeffs, rsvd_stream_t stream);
+
+/* ------------------------------------------------------------------ rows a2-a4: align
+ * Step 2: S_q[m,t] = sum_h conj(A_q[m,h]) B_q[t,h] for all q;
+ * Step 3: X_k = 2 pi sum_q e^{-2 pi i q k/Q} S_q, k = 0..Q-1 (forward sign, G3);
+ * Step 4: the score is Re X_k (G5).
+ * img_blocks from rsvd_compress(side=IMAGE, n=M), tmpl_blocks from rsvd_compress(side=TEMPLATE, n=T).
+ * work: device scratch of work_bytes >= rsvd_align_min_workspace_bytes(Q), 16-byte aligned.
+ *
+ * rsvd_align_argmax, mode RSVD_PER_PAIR: best_val[m*T + t] = max_k Re X_k, best_k[m*T + t] = the
+ *   smallest maximising k (SPEC.md tie rule, G9).  best_key unused (may be NULL).
+ * mode RSVD_PER_IMAGE: for each image m, atomically max-accumulates into best_key[m] the packed key
+ *   (ord(max Re X) << 32) | (0xFFFFFFFF - ((t_offset + t) * Q + k)), ord = order-preserving map of
+ *   float bits, so the maximum key is the largest value with the lexicographically smallest (t, k).
+ *   Requires (t_offset + T) * Q < 2^32.  best_key must be initialised by rsvd_winners_reset (it
+ *   accumulates over calls, e.g. template batches or shards).  best_val/best_k unused (may be NULL).
+ * rsvd_align_landscape: X[m*ld_m + t*ld_t + k] = Re X_k (float32), k contiguous; ld_t >= Q,
+ *   ld_m >= T*ld_t not required (caller strides); X 16-byte aligned when ld_t, ld_m are multiples of 4. */
+rsvd_status rsvd_align_argmax(const void *img_blocks, int64_t M, const void *tmpl_blocks, int64_t T,
+                              int64_t t_offset, int32_t Q, int32_t H, rsvd_reduce mode, void *work,
+                              int64_t work_bytes, float *best_val, int32_t *best_k,
+                              uint64_t *best_key, rsvd_stream_t stream);
+rsvd_status rsvd_align_landscape(const void *img_blocks, int64_t M, const void *tmpl_blocks,
+                                 int64_t T, int32_t Q, int32_t H, void *work, int64_t work_bytes,
+                                 float *X, int64_t ld_m, int64_t ld_t, rsvd_stream_t stream);
+
+/* ------------------------------------------------------------------ per-image winners
+ * rsvd_winners_reset: keys[0..M) = 0 (below every real key).
+ * rsvd_winners_unpack: (val, t, k) from packed keys; val/t/k device [M].
+ * rsvd_combine_winners: keys [G][M] (e.g. after an all-gather of every rank's keys over NVLink);
+ *   out = max over G per image (== the lexicographic (value, -t, -k) maximum), written as packed
+ *   keys to out_keys (may be NULL) and unpacked to val/t/k (each may be NULL). */
+rsvd_status rsvd_winners_reset(uint64_t *keys, int64_t M, rsvd_stream_t stream);
+rsvd_status rsvd_winners_unpack(const uint64_t *keys, int64_t M, int32_t Q, float *val, int32_t *t,
+                                int32_t *k, rsvd_stream_t stream);
+rsvd_status rsvd_combine_winners(const uint64_t *keys, int32_t G, int64_t M, int32_t Q,
+                                 uint64_t *out_keys, float *val, int32_t *t, int32_t *k,
+                                 rsvd_stream_t stream);
+
+/* ------------------------------------------------------------------ instrumentation
+ * rsvd_launch_count: monotonic count of kernels this library has launched in the process.
+ * rsvd_timing_enable(1): from now on every contraction / FFT-reduce / compress / kernel-partials
+ *   launch is bracketed by CUDA events recorded on its own stream (process-global, thread-safe).
+ * rsvd_timing_read: synchronises on the recorded events, returns per-kind total milliseconds and
+ *   launch counts (kinds: 0 contraction, 1 fft_reduce, 2 compress, 3 kernel partials) for the
+ *   spans recorded since the previous read, and recycles the events. */
+int64_t rsvd_launch_count(void);
+void rsvd_timing_enable(int32_t on);
+rsvd_status rsvd_timing_read(double *ms, int64_t *count, int32_t nkinds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSVD_H */

@@ -1,0 +1,254 @@
+"""Torch-facing wrappers of the C ABI (include/rsvd.h): the names mirror the library's entry
+points and every function only marshals arguments.  Tensors are CUDA, contiguous; complex rings
+are torch.complex64 [n, R, Q]; weights w are float64 [R]; packed per-image keys are int64 tensors
+holding the uint64 bit patterns.
+
+The `Aligner` class strings the entry points into the full hot path (rows a0-a4 of SURVEY.md §8):
+basis from the templates -> compress images and templates -> align -> winners."""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import PER_IMAGE, PER_PAIR, SIDE_IMAGE, SIDE_TEMPLATE, RsvdError, check, ptr, require_cuda, stream_handle
+
+__all__ = ["block_bytes", "kernel_chunk", "kernel_partials_bytes", "align_workspace_bytes",
+           "align_min_workspace_bytes", "kernel_partials", "kernel_reduce", "eigen_basis", "build_basis",
+           "compress", "blocks_unpack", "align_argmax", "align_landscape", "winners_reset",
+           "winners_unpack", "combine_winners", "launch_count", "timing_enable", "timing_read", "Aligner", "RsvdError", "PER_PAIR", "PER_IMAGE",
+           "SIDE_IMAGE", "SIDE_TEMPLATE"]
+
+
+# ------------------------------------------------------------------ sizes
+def block_bytes(rows: int, Q: int, H: int) -> int:
+    return int(_lib.lib().rsvd_block_bytes(rows, Q, H))
+
+
+def kernel_chunk() -> int:
+    return int(_lib.lib().rsvd_kernel_chunk())
+
+
+def kernel_partials_bytes(T: int, R: int) -> int:
+    return int(_lib.lib().rsvd_kernel_partials_bytes(T, R))
+
+
+def align_workspace_bytes(M: int, T: int, Q: int, H: int) -> int:
+    return int(_lib.lib().rsvd_align_workspace_bytes(M, T, Q, H))
+
+
+def align_min_workspace_bytes(Q: int) -> int:
+    return int(_lib.lib().rsvd_align_min_workspace_bytes(Q))
+
+
+# ------------------------------------------------------------------ row a0
+def kernel_partials(templates: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    require_cuda(templates)
+    T, R, Q = templates.shape
+    nch = (T + kernel_chunk() - 1) // kernel_chunk()
+    if out is None:
+        out = torch.empty((nch, R, R), dtype=torch.float64, device=templates.device)
+    check(_lib.lib().rsvd_kernel_partials(ptr(templates), T, R, Q, ptr(out), stream_handle(stream)))
+    return out
+
+
+def kernel_reduce(partials: torch.Tensor, T_total: int, Q: int, w: torch.Tensor, out=None, stream=None):
+    require_cuda(partials, w)
+    nch, R, _ = partials.shape
+    if out is None:
+        out = torch.empty((R, R), dtype=torch.float64, device=partials.device)
+    check(_lib.lib().rsvd_kernel_reduce(ptr(partials), nch, R, T_total, Q, ptr(w), ptr(out),
+                                        stream_handle(stream)))
+    return out
+
+
+def eigen_basis(C: np.ndarray, H: int):
+    """Host eigen-solver of the library.  Returns (U [R, H], lambda [R]) as float64 numpy."""
+    C = np.ascontiguousarray(C, dtype=np.float64)
+    R = C.shape[0]
+    U = np.zeros((R, H), dtype=np.float64)
+    lam = np.zeros(R, dtype=np.float64)
+    check(_lib.lib().rsvd_eigen_basis(ptr(C), R, H, ptr(U), ptr(lam)))
+    return U, lam
+
+
+def build_basis(templates: torch.Tensor, w, H: int, stream=None):
+    """rsvd_build_basis: (U [R, H], lambda [R]) float64 numpy, computed from all templates."""
+    require_cuda(templates)
+    T, R, Q = templates.shape
+    w = np.ascontiguousarray(np.asarray(w if not torch.is_tensor(w) else w.cpu().numpy()), dtype=np.float64)
+    U = np.zeros((R, H), dtype=np.float64)
+    lam = np.zeros(R, dtype=np.float64)
+    check(_lib.lib().rsvd_build_basis(ptr(templates), T, R, Q, ptr(w), H, ptr(U), ptr(lam),
+                                      stream_handle(stream)))
+    return U, lam
+
+
+# ------------------------------------------------------------------ row a1
+def compress(rings: torch.Tensor, w: torch.Tensor, U: torch.Tensor, side: int, out=None, stream=None):
+    """rsvd_compress -> opaque block buffer (float32 tensor of block_bytes/4 elements)."""
+    require_cuda(rings, w, U)
+    n, R, Q = rings.shape
+    H = U.shape[1]
+    nb = block_bytes(n, Q, H)
+    if out is None:
+        out = torch.empty(nb // 4, dtype=torch.float32, device=rings.device)
+    elif out.numel() * out.element_size() < nb:
+        raise RsvdError(1, "block buffer too small")
+    check(_lib.lib().rsvd_compress(ptr(rings), n, R, Q, ptr(w), ptr(U), H, side, ptr(out), stream_handle(stream)))
+    return out
+
+
+def blocks_unpack(blocks: torch.Tensor, n: int, Q: int, H: int, side: int, stream=None) -> torch.Tensor:
+    require_cuda(blocks)
+    out = torch.empty((n, Q, H), dtype=torch.complex64, device=blocks.device)
+    check(_lib.lib().rsvd_blocks_unpack(ptr(blocks), n, Q, H, side, ptr(out), stream_handle(stream)))
+    return out
+
+
+# ------------------------------------------------------------------ rows a2-a4
+def align_argmax(img_blocks, M: int, tmpl_blocks, T: int, Q: int, H: int, mode: int, work,
+                 best_val=None, best_k=None, best_key=None, t_offset: int = 0, stream=None):
+    require_cuda(img_blocks, tmpl_blocks, work)
+    dev = img_blocks.device
+    if mode == PER_PAIR:
+        if best_val is None:
+            best_val = torch.empty((M, T), dtype=torch.float32, device=dev)
+        if best_k is None:
+            best_k = torch.empty((M, T), dtype=torch.int32, device=dev)
+    else:
+        if best_key is None:
+            best_key = torch.zeros(M, dtype=torch.int64, device=dev)
+    check(_lib.lib().rsvd_align_argmax(ptr(img_blocks), M, ptr(tmpl_blocks), T, t_offset, Q, H, mode,
+                                       ptr(work), work.numel() * work.element_size(), ptr(best_val),
+                                       ptr(best_k), ptr(best_key), stream_handle(stream)))
+    return (best_val, best_k) if mode == PER_PAIR else best_key
+
+
+def align_landscape(img_blocks, M: int, tmpl_blocks, T: int, Q: int, H: int, work, X=None,
+                    ld_m: int | None = None, ld_t: int | None = None, stream=None):
+    require_cuda(img_blocks, tmpl_blocks, work)
+    if X is None:
+        X = torch.empty((M, T, Q), dtype=torch.float32, device=img_blocks.device)
+        ld_m, ld_t = T * Q, Q
+    check(_lib.lib().rsvd_align_landscape(ptr(img_blocks), M, ptr(tmpl_blocks), T, Q, H, ptr(work),
+                                          work.numel() * work.element_size(), ptr(X), ld_m, ld_t,
+                                          stream_handle(stream)))
+    return X
+
+
+def winners_reset(keys: torch.Tensor, stream=None):
+    require_cuda(keys)
+    check(_lib.lib().rsvd_winners_reset(ptr(keys), keys.numel(), stream_handle(stream)))
+    return keys
+
+
+def winners_unpack(keys: torch.Tensor, Q: int, stream=None):
+    require_cuda(keys)
+    M = keys.numel()
+    val = torch.empty(M, dtype=torch.float32, device=keys.device)
+    t = torch.empty(M, dtype=torch.int32, device=keys.device)
+    k = torch.empty(M, dtype=torch.int32, device=keys.device)
+    check(_lib.lib().rsvd_winners_unpack(ptr(keys), M, Q, ptr(val), ptr(t), ptr(k), stream_handle(stream)))
+    return val, t, k
+
+
+def combine_winners(keys_g: torch.Tensor, Q: int, stream=None):
+    """keys_g [G, M] (all-gathered per-rank keys) -> (keys, val, t, k) of the global winners."""
+    require_cuda(keys_g)
+    G, M = keys_g.shape
+    out = torch.empty(M, dtype=torch.int64, device=keys_g.device)
+    val = torch.empty(M, dtype=torch.float32, device=keys_g.device)
+    t = torch.empty(M, dtype=torch.int32, device=keys_g.device)
+    k = torch.empty(M, dtype=torch.int32, device=keys_g.device)
+    check(_lib.lib().rsvd_combine_winners(ptr(keys_g), G, M, Q, ptr(out), ptr(val), ptr(t), ptr(k),
+                                          stream_handle(stream)))
+    return out, val, t, k
+
+
+# ------------------------------------------------------------------ instrumentation
+TIMING_KINDS = ("contract", "fft_reduce", "compress", "kernel_partials")
+
+
+def launch_count() -> int:
+    return int(_lib.lib().rsvd_launch_count())
+
+
+def timing_enable(on: bool = True):
+    _lib.lib().rsvd_timing_enable(1 if on else 0)
+
+
+def timing_read():
+    """{kind: (total_ms, launches)} for the event-bracketed launches since the last read."""
+    ms = np.zeros(len(TIMING_KINDS), dtype=np.float64)
+    cnt = np.zeros(len(TIMING_KINDS), dtype=np.int64)
+    check(_lib.lib().rsvd_timing_read(ptr(ms), ptr(cnt), len(TIMING_KINDS)))
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(TIMING_KINDS)}
+
+
+# ------------------------------------------------------------------ the full path
+class Aligner:
+    """Many-to-many rotational alignment compressed by the radial-SVD (one GPU).
+
+    >>> al = Aligner(w, H)                       # radial weights of the shared polar grid
+    >>> al.fit(templates)                        # a0: basis from the templates' kernel C
+    >>> res = al.align(images, templates)        # a1-a4: compress both, align, argmax
+    """
+
+    def __init__(self, w, H: int, device="cuda", workspace_bytes: int | None = None):
+        self.H = int(H)
+        self.device = torch.device(device)
+        self.w_host = np.ascontiguousarray(np.asarray(w.cpu() if torch.is_tensor(w) else w), dtype=np.float64)
+        self.w = torch.tensor(self.w_host, dtype=torch.float64, device=self.device)
+        self.U = None
+        self.U_dev = None
+        self.lam = None
+        self._work = None
+        self._work_bytes = workspace_bytes
+
+    def set_basis(self, U):
+        self.U = np.ascontiguousarray(U, dtype=np.float64)
+        self.U_dev = torch.tensor(self.U, device=self.device)
+        return self
+
+    def fit(self, templates: torch.Tensor):
+        U, lam = build_basis(templates, self.w_host, self.H)
+        self.lam = lam
+        return self.set_basis(U)
+
+    def workspace(self, M: int, T: int, Q: int) -> torch.Tensor:
+        nb = self._work_bytes or align_workspace_bytes(M, T, Q, self.H)
+        nb = max(nb, align_min_workspace_bytes(Q))
+        if self._work is None or self._work.numel() * 4 < nb:
+            self._work = torch.empty((nb + 3) // 4, dtype=torch.float32, device=self.device)
+        return self._work
+
+    def compress(self, rings: torch.Tensor, side: int, out=None):
+        return compress(rings, self.w, self.U_dev, side, out=out)
+
+    def align_blocks(self, img_blocks, M, tmpl_blocks, T, Q, mode=PER_IMAGE, t_offset=0, keys=None):
+        work = self.workspace(M, T, Q)
+        if mode == PER_PAIR:
+            return align_argmax(img_blocks, M, tmpl_blocks, T, Q, self.H, PER_PAIR, work)
+        if keys is None:
+            keys = torch.zeros(M, dtype=torch.int64, device=self.device)
+        return align_argmax(img_blocks, M, tmpl_blocks, T, Q, self.H, PER_IMAGE, work, best_key=keys,
+                            t_offset=t_offset)
+
+    def landscape_blocks(self, img_blocks, M, tmpl_blocks, T, Q, X=None, ld_m=None, ld_t=None):
+        return align_landscape(img_blocks, M, tmpl_blocks, T, Q, self.H, self.workspace(M, T, Q), X, ld_m, ld_t)
+
+    def align(self, images: torch.Tensor, templates: torch.Tensor, mode=PER_IMAGE):
+        """Full pass from rings: returns per-pair (val [M,T], k [M,T]) or per-image (val, t, k) [M]."""
+        M, R, Q = images.shape
+        T = templates.shape[0]
+        if self.U is None:
+            self.fit(templates)
+        ib = self.compress(images, SIDE_IMAGE)
+        tb = self.compress(templates, SIDE_TEMPLATE)
+        if mode == PER_PAIR:
+            return self.align_blocks(ib, M, tb, T, Q, PER_PAIR)
+        keys = self.align_blocks(ib, M, tb, T, Q, PER_IMAGE)
+        return winners_unpack(keys, Q)

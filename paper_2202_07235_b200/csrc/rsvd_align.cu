@@ -1,0 +1,463 @@
+// rsvd_align.cu -- rows a2-a4: per-pair contraction over the principal rings (Step 2),
+// length-Q landscape transform (Step 3, :673) and argmax / landscape emission (Step 4, :504-517).
+//
+// Data flow per chunk of (Mc x Tc) pairs, all on `stream`:
+//   contract_kernel   U_q[m,t] = sum_j alpha[q][j][m] beta[q][j][t] = S_q + conj(S_{Q-q}), q = 0..N
+//                     (N = Q/2; S_q = sum_h conj(A_q[m,h]) B_q[t,h]) -> workspace Upk[pair][n]
+//                     (Upk[.][0] packs the two real values (U_0, U_N)).  FP32 SIMT, register tiled.
+//   fft_reduce_kernel Re X_k = 2 pi Re sum_q e^{-2 pi i qk/Q} S_q = 2 pi sum_q e^{-2pi i qk/Q} Y_q,
+//                     Y_q = U_q / 2 (Hermitian part).  Computed as a length-N complex FFT of
+//                     Z_n = (Y_n + conj Y_{N-n}) + i w_Q^n (Y_n - conj Y_{N-n}) whose output z_n
+//                     packs x_{2n} = Re z_n, x_{2n+1} = Im z_n (real-output FFT identity).  Then the
+//                     per-pair argmax (smallest k on ties), the per-image packed-key max, or the
+//                     landscape store.  The M x T x Q landscape never leaves the chip unless asked.
+// The workspace chunk is sized to stay L2-resident between the two kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "rsvd_common.cuh"
+
+namespace rsvd {
+
+// ------------------------------------------------------------------ contraction (Step 2)
+constexpr int CT_TILE = 64;    // m and t tile
+constexpr int CT_KC = 16;      // complex K per pipeline stage
+constexpr int CT_QB = 4;       // q values per CTA
+constexpr int CT_THREADS = 256;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NWAIT>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NWAIT)); }
+
+// grid: (Tc/64, Mc/64, ceil((N+1)/QB)); Upk[(ml * Tc + tl) * N + n]
+__global__ void __launch_bounds__(CT_THREADS) contract_kernel(const float2 *__restrict__ alpha,
+                                                              const float2 *__restrict__ beta,
+                                                              int64_t Mpad, int64_t Tpad, int Kpad, int N,
+                                                              int64_t m0, int64_t t0, int64_t Tc,
+                                                              float2 *__restrict__ Upk) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2 *As = reinterpret_cast<float2 *>(smem_raw);                    // [2][KC][64]
+    float2 *Bs = As + 2 * CT_KC * CT_TILE;                                // [2][KC][64]
+    float2 *stage = Bs + 2 * CT_KC * CT_TILE;                              // [QB][64*64]
+
+    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+    const int64_t bt = (int64_t)blockIdx.x * CT_TILE, bm = (int64_t)blockIdx.y * CT_TILE;
+    const int q0 = blockIdx.z * CT_QB;
+    const int nq = min(CT_QB, N + 1 - q0);
+    const int nk = Kpad / CT_KC;
+    const int iters = nq * nk;
+
+    auto load_stage = [&](int it, int buf) {
+        const int q = q0 + it / nk, kc = it % nk;
+        const float2 *ga = alpha + ((int64_t)q * Kpad + kc * CT_KC) * Mpad + m0 + bm;
+        const float2 *gb = beta + ((int64_t)q * Kpad + kc * CT_KC) * Tpad + t0 + bt;
+        float2 *sa = As + buf * CT_KC * CT_TILE;
+        float2 *sb = Bs + buf * CT_KC * CT_TILE;
+        // KC rows x 64 complex = KC x 32 16-byte chunks per operand
+#pragma unroll
+        for (int c = tid; c < CT_KC * 32; c += CT_THREADS) {
+            const int kk = c >> 5, ch = c & 31;
+            cp_async16(sa + kk * CT_TILE + ch * 2, ga + (int64_t)kk * Mpad + ch * 2);
+            cp_async16(sb + kk * CT_TILE + ch * 2, gb + (int64_t)kk * Tpad + ch * 2);
+        }
+        cp_async_commit();
+    };
+
+    float2 acc[4][4];
+    load_stage(0, 0);
+    for (int it = 0; it < iters; ++it) {
+        const int buf = it & 1;
+        if (it + 1 < iters) {
+            load_stage(it + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int kc = it % nk;
+        if (kc == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+        }
+        const float2 *sa = As + buf * CT_KC * CT_TILE;
+        const float2 *sb = Bs + buf * CT_KC * CT_TILE;
+#pragma unroll
+        for (int kk = 0; kk < CT_KC; ++kk) {
+            const float4 a01 = *reinterpret_cast<const float4 *>(sa + kk * CT_TILE + ty * 4);
+            const float4 a23 = *reinterpret_cast<const float4 *>(sa + kk * CT_TILE + ty * 4 + 2);
+            const float2 a[4] = {make_float2(a01.x, a01.y), make_float2(a01.z, a01.w),
+                                 make_float2(a23.x, a23.y), make_float2(a23.z, a23.w)};
+            float2 b[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = sb[kk * CT_TILE + tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc[i][j].x = fmaf(a[i].x, b[j].x, acc[i][j].x);
+                    acc[i][j].x = fmaf(-a[i].y, b[j].y, acc[i][j].x);
+                    acc[i][j].y = fmaf(a[i].x, b[j].y, acc[i][j].y);
+                    acc[i][j].y = fmaf(a[i].y, b[j].x, acc[i][j].y);
+                }
+        }
+        if (kc == nk - 1) {
+            const int qi = it / nk;
+            float2 *st = stage + qi * CT_TILE * CT_TILE;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) st[(ty * 4 + i) * CT_TILE + tx + 16 * j] = acc[i][j];
+        }
+        __syncthreads();
+    }
+    // write Upk: each pair gets its q0..q0+nq-1 entries (32 B when nq == 4)
+    for (int p = tid; p < CT_TILE * CT_TILE; p += CT_THREADS) {
+        const int ml = p >> 6, tl = p & 63;
+        float2 *dst = Upk + ((bm + ml) * Tc + bt + tl) * (int64_t)N;
+        if (q0 == N) {                 // only q = N: its real part goes to slot 0 .y
+            reinterpret_cast<float *>(dst)[1] = stage[p].x;
+            continue;
+        }
+        if (q0 == 0) {
+            reinterpret_cast<float *>(dst)[0] = stage[p].x;   // U_0 (real) to slot 0 .x
+            for (int qi = 1; qi < nq; ++qi) dst[qi] = stage[qi * CT_TILE * CT_TILE + p];
+            continue;
+        }
+        if (nq == 4) {
+            const float2 v0 = stage[p], v1 = stage[CT_TILE * CT_TILE + p];
+            const float2 v2 = stage[2 * CT_TILE * CT_TILE + p], v3 = stage[3 * CT_TILE * CT_TILE + p];
+            reinterpret_cast<float4 *>(dst + q0)[0] = make_float4(v0.x, v0.y, v1.x, v1.y);
+            reinterpret_cast<float4 *>(dst + q0)[1] = make_float4(v2.x, v2.y, v3.x, v3.y);
+        } else {
+            for (int qi = 0; qi < nq; ++qi) dst[q0 + qi] = stage[qi * CT_TILE * CT_TILE + p];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ FFT + reduce (Steps 3-4)
+enum { MODE_PAIR = 0, MODE_IMAGE = 1, MODE_LANDSCAPE = 2 };
+constexpr int FR_THREADS = 256;
+constexpr int FR_TPAIRS = 64;    // templates per CTA (one image row per CTA)
+
+__device__ __forceinline__ uint32_t ord_f32(float v) {
+    const uint32_t u = __float_as_uint(v);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// grid: (ceil(tcv / 64), mcv).  Upk rows of the chunk have stride Tc pairs.
+template <int LOGN, int MODE>
+__global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(
+    const float2 *__restrict__ Upk, int64_t Tc, int64_t m0, int64_t t0, int64_t tcv, int64_t T,
+    int64_t t_offset, float *__restrict__ best_val, int32_t *__restrict__ best_k,
+    unsigned long long *__restrict__ best_key, float *__restrict__ X, int64_t ld_m, int64_t ld_t) {
+    constexpr int N = 1 << LOGN;
+    constexpr int Q = 2 * N;
+    constexpr int L = N < 32 ? N : 32;
+    constexpr int E = N / L;
+    constexpr int G = 32 / L;                 // pairs per warp in flight
+    constexpr int SLOTS = (FR_THREADS / 32) * G;
+    constexpr int PER_SLOT = FR_TPAIRS / SLOTS;
+    __shared__ float2 twN[E * L];             // W_N^{l k1}
+    __shared__ float2 pre[E * L];             // W_Q^{n}, n = l + L e
+    __shared__ unsigned long long skey;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane / L, l = lane % L;
+    for (int i = tid; i < E * L; i += FR_THREADS) {
+        twN[i] = twiddle_N(i % L, i / L, N);
+        float sn, cs;
+        sincospif(2.0f * (float)((i % L) + L * (i / L)) / (float)Q, &sn, &cs);
+        pre[i] = make_float2(cs, -sn);
+    }
+    if (tid == 0) skey = 0ull;
+    float2 stw[clog2(L) > 0 ? clog2(L) : 1];
+    lane_stage_twiddles<L>(l, stw);
+    __syncthreads();
+
+    const int64_t ml = blockIdx.y;
+    const int64_t m = m0 + ml;
+    const int slot = warp * G + g;
+    const float PI = 3.14159265358979323846f;
+    unsigned long long mykey = 0ull;
+
+    for (int i = 0; i < PER_SLOT; ++i) {
+        const int64_t tl = (int64_t)blockIdx.x * FR_TPAIRS + slot + (int64_t)SLOTS * i;
+        const bool valid = tl < tcv;
+        const float2 *src = Upk + (ml * Tc + (valid ? tl : 0)) * (int64_t)N;
+        float2 u[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) u[e] = src[l + L * e];
+        // mirror M = U_{N-n}
+        float2 z[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int srcl = g * L + ((L - l) & (L - 1));
+            float2 mm;
+            mm.x = __shfl_sync(0xffffffffu, u[E - 1 - e].x, srcl);
+            mm.y = __shfl_sync(0xffffffffu, u[E - 1 - e].y, srcl);
+            if (l == 0) mm = u[(E - e) % E];
+            const float2 uu = u[e];
+            const float2 s = make_float2(uu.x + mm.x, uu.y - mm.y);    // U + conj M
+            const float2 d = make_float2(uu.x - mm.x, uu.y + mm.y);    // U - conj M
+            const float2 wd = c_mul(pre[e * L + l], d);
+            z[e] = make_float2(PI * (s.x - wd.y), PI * (s.y + wd.x)); // pi (s + i w d)
+        }
+        if (l == 0) {   // n = 0: slot 0 packs the reals (U_0, U_N)
+            const float u0 = u[0].x, un = u[0].y;
+            z[0] = make_float2(PI * (u0 + un), PI * (u0 - un));
+        }
+        fft_dist<E, L>(z, l, twN, stw);
+        const int b = (int)(__brev((unsigned)l) >> (32 - clog2(L)));
+        if constexpr (MODE == MODE_LANDSCAPE) {
+            if (valid) {
+                float *dst = X + m * ld_m + (t0 + tl) * ld_t + 2 * E * b;
+#pragma unroll
+                for (int k1 = 0; k1 < E; ++k1)
+                    reinterpret_cast<float2 *>(dst)[k1] = z[brev(k1, clog2(E))];
+            }
+        } else {
+            float bv = -INFINITY;
+            int bk = 0x7fffffff;
+#pragma unroll
+            for (int k1 = 0; k1 < E; ++k1) {
+                const float2 v = z[brev(k1, clog2(E))];
+                const int k = 2 * (k1 + E * b);
+                if (v.x > bv) { bv = v.x; bk = k; }          // indices increase with k1
+                if (v.y > bv) { bv = v.y; bk = k + 1; }
+            }
+#pragma unroll
+            for (int off = L / 2; off >= 1; off >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                const int ok = __shfl_xor_sync(0xffffffffu, bk, off);
+                if (ov > bv || (ov == bv && ok < bk)) { bv = ov; bk = ok; }
+            }
+            if constexpr (MODE == MODE_PAIR) {
+                if (valid && l == 0) {
+                    const int64_t o = m * T + t0 + tl;
+                    best_val[o] = bv;
+                    best_k[o] = bk;
+                }
+            } else {
+                if (valid) {
+                    const uint32_t idx = (uint32_t)((t_offset + t0 + tl) * Q + bk);
+                    const unsigned long long key =
+                        ((unsigned long long)ord_f32(bv) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
+                    mykey = key > mykey ? key : mykey;
+                }
+            }
+        }
+    }
+    if constexpr (MODE == MODE_IMAGE) {
+        if (l == 0 && mykey) atomicMax(&skey, mykey);
+        __syncthreads();
+        if (tid == 0 && skey) atomicMax(best_key + m, skey);
+    }
+}
+
+template <int LOGN>
+static cudaError_t launch_fft(int mode, dim3 grid, cudaStream_t s, const float2 *Upk, int64_t Tc, int64_t m0,
+                              int64_t t0, int64_t tcv, int64_t T, int64_t t_offset, float *best_val,
+                              int32_t *best_k, unsigned long long *best_key, float *X, int64_t ld_m, int64_t ld_t) {
+    if (mode == MODE_PAIR)
+        fft_reduce_kernel<LOGN, MODE_PAIR><<<grid, FR_THREADS, 0, s>>>(Upk, Tc, m0, t0, tcv, T, t_offset, best_val,
+                                                                       best_k, best_key, X, ld_m, ld_t);
+    else if (mode == MODE_IMAGE)
+        fft_reduce_kernel<LOGN, MODE_IMAGE><<<grid, FR_THREADS, 0, s>>>(Upk, Tc, m0, t0, tcv, T, t_offset, best_val,
+                                                                        best_k, best_key, X, ld_m, ld_t);
+    else
+        fft_reduce_kernel<LOGN, MODE_LANDSCAPE><<<grid, FR_THREADS, 0, s>>>(Upk, Tc, m0, t0, tcv, T, t_offset,
+                                                                            best_val, best_k, best_key, X, ld_m, ld_t);
+    return cudaGetLastError();
+}
+
+static size_t contract_smem() {
+    return (size_t)(4 * CT_KC * CT_TILE + CT_QB * CT_TILE * CT_TILE) * sizeof(float2);
+}
+
+struct AlignArgs {
+    const float2 *alpha, *beta;
+    int64_t M, T, t_offset;
+    int Q, H;
+    int mode;
+    void *work;
+    int64_t work_bytes;
+    float *best_val;
+    int32_t *best_k;
+    unsigned long long *best_key;
+    float *X;
+    int64_t ld_m, ld_t;
+};
+
+static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
+    const int N = a.Q / 2;
+    const int Kpad = (int)kpad_of(a.H);
+    const int64_t Mpad = rows_pad_of(a.M), Tpad = rows_pad_of(a.T);
+    // chunk: Mc x Tc pairs (multiples of 64) with Mc * Tc * N * 8 <= work_bytes
+    const int64_t tile_bytes = (int64_t)CT_TILE * CT_TILE * N * (int64_t)sizeof(float2);
+    const int64_t ntiles = a.work_bytes / tile_bytes;
+    if (ntiles < 1) return fail(RSVD_ERR_ARG, "workspace smaller than rsvd_align_min_workspace_bytes(Q)");
+    const int64_t tmax = Tpad / CT_TILE, mmax = Mpad / CT_TILE;
+    int64_t tct = std::max<int64_t>(1, (int64_t)std::sqrt((double)ntiles));
+    tct = std::min(tct, tmax);
+    int64_t mct = std::min(mmax, std::max<int64_t>(1, ntiles / tct));
+    tct = std::min(tmax, std::max(tct, ntiles / mct));      // widen t when rows run out
+    const int64_t Mc = mct * CT_TILE, Tc = tct * CT_TILE;
+    float2 *Upk = reinterpret_cast<float2 *>(a.work);
+    const size_t smem = contract_smem();
+    cudaError_t e = cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_check(e, "contract smem attribute");
+    const int LOGN = ilog2(N);
+    const bool timed = timing_enabled();
+    for (int64_t m0 = 0; m0 < Mpad; m0 += Mc) {
+        const int64_t mc = std::min(Mc, Mpad - m0);
+        const int64_t mcv = std::min(mc, a.M - m0);
+        for (int64_t t0 = 0; t0 < Tpad; t0 += Tc) {
+            const int64_t tc = std::min(Tc, Tpad - t0);
+            const int64_t tcv = std::min(tc, a.T - t0);
+            dim3 g1((unsigned)(tc / CT_TILE), (unsigned)(mc / CT_TILE), (unsigned)((N + 1 + CT_QB - 1) / CT_QB));
+            cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
+            contract_kernel<<<g1, CT_THREADS, smem, s>>>(a.alpha, a.beta, Mpad, Tpad, Kpad, N, m0, t0, Tc, Upk);
+            if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "contract launch");
+            cudaEvent_t ev1 = timed ? timing_event(s) : nullptr;
+            dim3 g2((unsigned)((tcv + FR_TPAIRS - 1) / FR_TPAIRS), (unsigned)mcv);
+            switch (LOGN) {
+                case 4: e = launch_fft<4>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
+                case 5: e = launch_fft<5>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
+                case 6: e = launch_fft<6>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
+                case 7: e = launch_fft<7>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
+                case 8: e = launch_fft<8>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
+                default: e = launch_fft<9>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
+            }
+            if (e != cudaSuccess) return cuda_check(e, "fft_reduce launch");
+            count_launches(2);
+            if (timed) {
+                cudaEvent_t ev2 = timing_event(s);
+                timing_span(ev0, ev1, TK_CONTRACT);
+                timing_span(ev1, ev2, TK_FFT);
+            }
+        }
+    }
+    return RSVD_OK;
+}
+
+static rsvd_status check_common(const void *img, int64_t M, const void *tmpl, int64_t T, int32_t Q, int32_t H,
+                                void *work, int64_t work_bytes) {
+    if (Q <= 0) return fail(RSVD_ERR_ARG, "Q must be positive");
+    if (!is_pow2(Q) || Q < 32 || Q > 1024) return fail(RSVD_ERR_UNSUPPORTED, "Q must be a power of two in [32, 1024]");
+    if (H < 1) return fail(RSVD_ERR_ARG, "H must be >= 1");
+    if (H > 256) return fail(RSVD_ERR_UNSUPPORTED, "H > 256 is not supported");
+    if (M < 0 || T < 0) return fail(RSVD_ERR_ARG, "M and T must be >= 0");
+    if (M > 0x7fffffffLL || T > 0x7fffffffLL) return fail(RSVD_ERR_UNSUPPORTED, "M, T must be < 2^31");
+    if (M == 0 || T == 0) return RSVD_OK;
+    if (!img || !tmpl || !work) return fail(RSVD_ERR_ARG, "NULL pointer");
+    if (!aligned16(img) || !aligned16(tmpl) || !aligned16(work)) return fail(RSVD_ERR_ARG, "buffers must be 16-byte aligned");
+    if (work_bytes < rsvd_align_min_workspace_bytes(Q)) return fail(RSVD_ERR_ARG, "workspace too small");
+    return RSVD_OK;
+}
+
+// ------------------------------------------------------------------ winners
+__device__ __forceinline__ float unord_f32(uint32_t o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+}
+
+__global__ void winners_unpack_kernel(const unsigned long long *__restrict__ keys, int G, int64_t M, int Q,
+                                      unsigned long long *__restrict__ out_keys, float *__restrict__ val,
+                                      int32_t *__restrict__ t, int32_t *__restrict__ k) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    unsigned long long best = 0ull;
+    for (int gi = 0; gi < G; ++gi) {
+        const unsigned long long v = keys[(int64_t)gi * M + m];
+        best = v > best ? v : best;
+    }
+    if (out_keys) out_keys[m] = best;
+    const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFull);
+    if (val) val[m] = best ? unord_f32((uint32_t)(best >> 32)) : -INFINITY;
+    if (t) t[m] = best ? (int32_t)(idx / (uint32_t)Q) : -1;
+    if (k) k[m] = best ? (int32_t)(idx % (uint32_t)Q) : -1;
+}
+
+}  // namespace rsvd
+
+using namespace rsvd;
+
+extern "C" int64_t rsvd_align_min_workspace_bytes(int32_t Q) {
+    if (Q < 2) return -1;
+    return (int64_t)CT_TILE * CT_TILE * (Q / 2) * (int64_t)sizeof(float2);
+}
+
+extern "C" int64_t rsvd_align_workspace_bytes(int64_t M, int64_t T, int32_t Q, int32_t H) {
+    (void)H;
+    if (Q < 2 || M < 0 || T < 0) return -1;
+    const int64_t full = rows_pad_of(std::max<int64_t>(M, 1)) * rows_pad_of(std::max<int64_t>(T, 1)) * (Q / 2) * 8;
+    const int64_t target = 64ll << 20;     // L2-resident chunk
+    return std::max(rsvd_align_min_workspace_bytes(Q), std::min(full, target));
+}
+
+extern "C" rsvd_status rsvd_align_argmax(const void *img_blocks, int64_t M, const void *tmpl_blocks, int64_t T,
+                                         int64_t t_offset, int32_t Q, int32_t H, rsvd_reduce mode, void *work,
+                                         int64_t work_bytes, float *best_val, int32_t *best_k, uint64_t *best_key,
+                                         rsvd_stream_t stream) {
+    rsvd_status st = check_common(img_blocks, M, tmpl_blocks, T, Q, H, work, work_bytes);
+    if (st != RSVD_OK || M == 0 || T == 0) return st;
+    if (mode == RSVD_PER_PAIR) {
+        if (!best_val || !best_k) return fail(RSVD_ERR_ARG, "PER_PAIR needs best_val and best_k");
+    } else if (mode == RSVD_PER_IMAGE) {
+        if (!best_key) return fail(RSVD_ERR_ARG, "PER_IMAGE needs best_key");
+        if (t_offset < 0) return fail(RSVD_ERR_ARG, "t_offset must be >= 0");
+        if ((uint64_t)(t_offset + T) * (uint64_t)Q >= 0xFFFFFFFFull)
+            return fail(RSVD_ERR_UNSUPPORTED, "(t_offset + T) * Q must be < 2^32 for packed keys");
+    } else {
+        return fail(RSVD_ERR_ARG, "bad mode");
+    }
+    AlignArgs a{reinterpret_cast<const float2 *>(img_blocks), reinterpret_cast<const float2 *>(tmpl_blocks),
+                M, T, t_offset, Q, H, mode == RSVD_PER_PAIR ? MODE_PAIR : MODE_IMAGE, work, work_bytes,
+                best_val, best_k, reinterpret_cast<unsigned long long *>(best_key), nullptr, 0, 0};
+    return run_align(a, (cudaStream_t)stream);
+}
+
+extern "C" rsvd_status rsvd_align_landscape(const void *img_blocks, int64_t M, const void *tmpl_blocks, int64_t T,
+                                            int32_t Q, int32_t H, void *work, int64_t work_bytes, float *X,
+                                            int64_t ld_m, int64_t ld_t, rsvd_stream_t stream) {
+    rsvd_status st = check_common(img_blocks, M, tmpl_blocks, T, Q, H, work, work_bytes);
+    if (st != RSVD_OK || M == 0 || T == 0) return st;
+    if (!X) return fail(RSVD_ERR_ARG, "NULL landscape pointer");
+    if (ld_t < Q || ld_m < 0) return fail(RSVD_ERR_ARG, "bad landscape strides");
+    if ((ld_t & 1) || (ld_m & 1) || (reinterpret_cast<uintptr_t>(X) & 7u))
+        return fail(RSVD_ERR_ARG, "landscape strides must be even and X 8-byte aligned");
+    AlignArgs a{reinterpret_cast<const float2 *>(img_blocks), reinterpret_cast<const float2 *>(tmpl_blocks),
+                M, T, 0, Q, H, MODE_LANDSCAPE, work, work_bytes, nullptr, nullptr, nullptr, X, ld_m, ld_t};
+    return run_align(a, (cudaStream_t)stream);
+}
+
+extern "C" rsvd_status rsvd_winners_reset(uint64_t *keys, int64_t M, rsvd_stream_t stream) {
+    if (M < 0) return fail(RSVD_ERR_ARG, "M must be >= 0");
+    if (M == 0) return RSVD_OK;
+    if (!keys) return fail(RSVD_ERR_ARG, "NULL pointer");
+    return cuda_check(cudaMemsetAsync(keys, 0, (size_t)M * sizeof(uint64_t), (cudaStream_t)stream), "winners reset");
+}
+
+extern "C" rsvd_status rsvd_winners_unpack(const uint64_t *keys, int64_t M, int32_t Q, float *val, int32_t *t,
+                                           int32_t *k, rsvd_stream_t stream) {
+    return rsvd_combine_winners(keys, 1, M, Q, nullptr, val, t, k, stream);
+}
+
+extern "C" rsvd_status rsvd_combine_winners(const uint64_t *keys, int32_t G, int64_t M, int32_t Q, uint64_t *out_keys,
+                                            float *val, int32_t *t, int32_t *k, rsvd_stream_t stream) {
+    if (G < 1 || M < 0 || Q < 1) return fail(RSVD_ERR_ARG, "bad sizes");
+    if (M == 0) return RSVD_OK;
+    if (!keys) return fail(RSVD_ERR_ARG, "NULL pointer");
+    winners_unpack_kernel<<<(unsigned)((M + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const unsigned long long *>(keys), G, M, Q, reinterpret_cast<unsigned long long *>(out_keys),
+        val, t, k);
+    count_launches(1);
+    return cuda_check(cudaGetLastError(), "combine launch");
+}

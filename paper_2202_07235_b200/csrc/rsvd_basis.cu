@@ -1,0 +1,215 @@
+// rsvd_basis.cu -- row a0: the template kernel matrix C and its eigenbasis (precompute).
+//
+// C[r][r'] = (1/(T Q)) sqrt(w_r w_r') sum_t Re sum_j W_t[r,j] conj(W_t[r',j]),  W_t = b_t minus its
+// angular mean.  This is Eq. Image_simple_kern (q = 0 excluded) averaged over the
+// targets as in Eq. image_cost_and_kern, written in psi-space by Parseval
+// (sum_{q != 0} conj(xhat_q) yhat_q = (1/Q) sum_j conj(x_j - xbar)(y_j - ybar), xhat = DFT/Q).
+// Constants (2 pi)^3 / (4 sigma_hat^2) are dropped (they do not move eigenvectors; reading G6).
+//
+// Determinism: the per-chunk partials depend only on the chunk's templates and are summed in chunk
+// order, so C (and U) are bitwise identical for any sharding of the templates over GPUs.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <vector>
+
+#include "rsvd_common.cuh"
+
+namespace rsvd {
+
+constexpr int KCHUNK = 32;     // templates per partial (rsvd_kernel_chunk)
+constexpr int BT = 64;         // output tile (rows) of C per CTA
+constexpr int JB = 32;         // angular samples per smem slab
+constexpr int NTHR = 256;
+
+// grid: (ntile, ntile, nchunks), only tiles with ti >= tj.  Thread (ty, tx) owns rows
+// r_a = ti*64 + ty + 16a and r'_b = tj*64 + tx + 16b, a, b < 4.
+__global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__restrict__ tmpl,
+                                                               int64_t T, int R, int Q,
+                                                               double *__restrict__ partials) {
+    const int ti = blockIdx.x, tj = blockIdx.y;
+    if (ti < tj) return;
+    const int64_t c = blockIdx.z;
+    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+    __shared__ float2 xi[BT][JB + 1];
+    __shared__ float2 xj[BT][JB + 1];
+    __shared__ double si[BT][2], sj[BT][2];       // per-template row sums (re, im)
+
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+
+    const int64_t t_begin = c * KCHUNK;
+    const int64_t t_end = min(T, t_begin + KCHUNK);
+    for (int64_t t = t_begin; t < t_end; ++t) {
+        const float2 *bt = tmpl + t * (int64_t)R * Q;
+        if (tid < BT) { si[tid][0] = si[tid][1] = 0.0; sj[tid][0] = sj[tid][1] = 0.0; }
+        for (int j0 = 0; j0 < Q; j0 += JB) {
+            __syncthreads();
+            // load 64 rows x JB samples for both row tiles
+            for (int idx = tid; idx < BT * JB; idx += NTHR) {
+                const int rr = idx / JB, jj = idx % JB;
+                const int r1 = ti * BT + rr, r2 = tj * BT + rr;
+                const int j = j0 + jj;
+                float2 z = make_float2(0.f, 0.f);
+                xi[rr][jj] = (r1 < R && j < Q) ? bt[(int64_t)r1 * Q + j] : z;
+                xj[rr][jj] = (r2 < R && j < Q) ? bt[(int64_t)r2 * Q + j] : z;
+            }
+            __syncthreads();
+            // row sums (fp64, fixed order)
+            if (tid < BT) {
+                double sr = 0, sim = 0, tr = 0, tim = 0;
+                for (int jj = 0; jj < JB; ++jj) {
+                    sr += (double)xi[tid][jj].x; sim += (double)xi[tid][jj].y;
+                    tr += (double)xj[tid][jj].x; tim += (double)xj[tid][jj].y;
+                }
+                si[tid][0] += sr; si[tid][1] += sim;
+                sj[tid][0] += tr; sj[tid][1] += tim;
+            }
+            // Gram: Re(x_r conj(x_r')) = xr xr' + xi xi'
+            for (int jj = 0; jj < JB; ++jj) {
+                double ar[4], ai[4], br[4], bi[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const float2 u = xi[ty + 16 * a][jj];
+                    ar[a] = u.x; ai[a] = u.y;
+                }
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const float2 u = xj[tx + 16 * b][jj];
+                    br[b] = u.x; bi[b] = u.y;
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) acc[a][b] = fma(ar[a], br[b], fma(ai[a], bi[b], acc[a][b]));
+            }
+        }
+        __syncthreads();
+        // remove the angular mean: - (1/Q) Re(S_r conj(S_r'))
+        const double invQ = 1.0 / (double)Q;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const double re = si[ty + 16 * a][0] * sj[tx + 16 * b][0] + si[ty + 16 * a][1] * sj[tx + 16 * b][1];
+                acc[a][b] -= re * invQ;
+            }
+    }
+    double *out = partials + c * (int64_t)R * R;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int r1 = ti * BT + ty + 16 * a, r2 = tj * BT + tx + 16 * b;
+            if (r1 < R && r2 < R) out[(int64_t)r1 * R + r2] = acc[a][b];
+        }
+}
+
+// C[r][r'] = sqrt(w_r w_r') / (T Q) * sum_c P_c[max(r,r')][min(r,r')] (lower triangle is the
+// computed one; reading it for both halves makes C exactly symmetric).
+__global__ void kernel_reduce_kernel(const double *__restrict__ partials, int64_t nchunks, int R,
+                                     double scale, const double *__restrict__ w, double *__restrict__ C) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)R * R) return;
+    const int r = (int)(idx / R), s = (int)(idx % R);
+    const int hi = r > s ? r : s, lo = r > s ? s : r;
+    // tiles with ti < tj were skipped: the element (hi, lo) always lies in a computed tile
+    double acc = 0.0;
+    for (int64_t c = 0; c < nchunks; ++c) acc += partials[c * (int64_t)R * R + (int64_t)hi * R + lo];
+    C[idx] = acc * scale * sqrt(w[r]) * sqrt(w[s]);
+}
+
+}  // namespace rsvd
+
+using namespace rsvd;
+
+extern "C" int64_t rsvd_kernel_chunk(void) { return KCHUNK; }
+
+extern "C" int64_t rsvd_kernel_partials_bytes(int64_t T, int32_t R) {
+    if (T < 0 || R <= 0) return -1;
+    return (T + KCHUNK - 1) / KCHUNK * (int64_t)R * R * (int64_t)sizeof(double);
+}
+
+static rsvd_status check_grid(int32_t R, int32_t Q) {
+    if (R <= 0) return fail(RSVD_ERR_ARG, "R must be positive");
+    if (R > 256) return fail(RSVD_ERR_UNSUPPORTED, "R > 256 is not supported");
+    if (Q <= 0) return fail(RSVD_ERR_ARG, "Q must be positive");
+    if (!is_pow2(Q) || Q < 32 || Q > 1024)
+        return fail(RSVD_ERR_UNSUPPORTED, "Q must be a power of two in [32, 1024]");
+    return RSVD_OK;
+}
+
+extern "C" rsvd_status rsvd_kernel_partials(const void *templates, int64_t T, int32_t R, int32_t Q,
+                                            double *partials, rsvd_stream_t stream) {
+    rsvd_status st = check_grid(R, Q);
+    if (st != RSVD_OK) return st;
+    if (T < 0) return fail(RSVD_ERR_ARG, "T must be >= 0");
+    if (T == 0) return RSVD_OK;
+    if (!templates || !partials) return fail(RSVD_ERR_ARG, "NULL pointer");
+    if (!aligned16(templates) || (reinterpret_cast<uintptr_t>(partials) & 7u))
+        return fail(RSVD_ERR_ARG, "misaligned pointer");
+    const int nt = (R + BT - 1) / BT;
+    const int64_t nchunks = (T + KCHUNK - 1) / KCHUNK;
+    if (nchunks > 65535) return fail(RSVD_ERR_UNSUPPORTED, "too many template chunks in one call");
+    dim3 grid(nt, nt, (unsigned)nchunks);
+    const bool timed = timing_enabled();
+    cudaEvent_t ev0 = timed ? timing_event((cudaStream_t)stream) : nullptr;
+    kernel_partials_kernel<<<grid, NTHR, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const float2 *>(templates), T, R, Q, partials);
+    count_launches(1);
+    if (timed) timing_span(ev0, timing_event((cudaStream_t)stream), TK_BASIS);
+    return cuda_check(cudaGetLastError(), "kernel_partials launch");
+}
+
+extern "C" rsvd_status rsvd_kernel_reduce(const double *partials, int64_t nchunks, int32_t R,
+                                          int64_t T_total, int32_t Q, const double *w, double *C,
+                                          rsvd_stream_t stream) {
+    rsvd_status st = check_grid(R, Q);
+    if (st != RSVD_OK) return st;
+    if (nchunks <= 0 || T_total <= 0) return fail(RSVD_ERR_ARG, "need at least one template chunk");
+    if (!partials || !w || !C) return fail(RSVD_ERR_ARG, "NULL pointer");
+    const double scale = 1.0 / ((double)T_total * (double)Q);
+    const int64_t n = (int64_t)R * R;
+    kernel_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        partials, nchunks, R, scale, w, C);
+    count_launches(1);
+    return cuda_check(cudaGetLastError(), "kernel_reduce launch");
+}
+
+extern "C" rsvd_status rsvd_build_basis(const void *templates, int64_t T, int32_t R, int32_t Q,
+                                        const double *w_host, int32_t H, double *U_host,
+                                        double *lambda_host, rsvd_stream_t stream) {
+    rsvd_status st = check_grid(R, Q);
+    if (st != RSVD_OK) return st;
+    if (T <= 0) return fail(RSVD_ERR_ARG, "T must be >= 1 to build a basis");
+    if (H < 1 || H > R) return fail(RSVD_ERR_UNSUPPORTED, "H must satisfy 1 <= H <= R");
+    if (!templates || !w_host || !U_host) return fail(RSVD_ERR_ARG, "NULL pointer");
+    for (int r = 0; r < R; ++r)
+        if (!std::isfinite(w_host[r]) || !(w_host[r] > 0.0))
+            return fail(RSVD_ERR_ARG, "weights must be finite and > 0");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nchunks = (T + KCHUNK - 1) / KCHUNK;
+    const size_t pbytes = (size_t)nchunks * R * R * sizeof(double);
+    void *scratch = nullptr;
+    const size_t wbytes = (size_t)R * sizeof(double), cbytes = (size_t)R * R * sizeof(double);
+    cudaError_t e = cudaMallocAsync(&scratch, pbytes + wbytes + cbytes, s);
+    if (e != cudaSuccess) return cuda_check(e, "cudaMallocAsync(basis scratch)");
+    double *partials = (double *)scratch;
+    double *w_dev = partials + (size_t)nchunks * R * R;
+    double *C_dev = w_dev + R;
+    std::vector<double> C((size_t)R * R);
+    st = RSVD_OK;
+    if ((e = cudaMemcpyAsync(w_dev, w_host, wbytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        st = cuda_check(e, "copy w");
+    if (st == RSVD_OK) st = rsvd_kernel_partials(templates, T, R, Q, partials, stream);
+    if (st == RSVD_OK) st = rsvd_kernel_reduce(partials, nchunks, R, T, Q, w_dev, C_dev, stream);
+    if (st == RSVD_OK && (e = cudaMemcpyAsync(C.data(), C_dev, cbytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        st = cuda_check(e, "copy C");
+    cudaFreeAsync(scratch, s);
+    if (st != RSVD_OK) return st;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_check(e, "basis sync");
+    return rsvd_eigen_basis(C.data(), R, H, U_host, lambda_host);
+}

@@ -1,0 +1,185 @@
+// rsvd_common.cuh -- shared device helpers of librsvd (CUDA path only; the oracle shares nothing).
+//
+// Holds: status/error plumbing, complex float2 arithmetic, and the distributed forward FFT used by
+// both Step 1 (rsvd_compress: length-Q DFT of principal rings) and Step 3
+// (rsvd_align: length-Q/2 DFT of the packed Hermitian spectrum).
+//
+// Distributed FFT layout ("four-step", N = L * E): a group of L lanes (L = min(32, N), a power of
+// two) owns one length-N vector; lane l holds v[e] = x[l + L e], e < E.  fft_dist computes
+//   X[k] = sum_n x[n] e^{-2 pi i n k / N}
+// as (1) an in-register radix-2 DIF DFT of length E over e, (2) the twiddle W_N^{l k1},
+// (3) a radix-2 DIF DFT of length L across lanes with warp shuffles.  On return lane l register
+// brev_E(k1) holds X[k1 + E * brev_L(l)].
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/rsvd.h"
+
+namespace rsvd {
+
+// ------------------------------------------------------------------ status plumbing
+void set_error(const std::string &msg);
+rsvd_status fail(rsvd_status st, const std::string &msg);
+rsvd_status cuda_check(cudaError_t e, const char *what);
+
+// launch counter (rsvd_launch_count) and optional per-kernel event timing (rsvd_timing_*)
+void count_launches(int n);
+bool timing_enabled();
+cudaEvent_t timing_event(cudaStream_t s);
+void timing_span(cudaEvent_t a, cudaEvent_t b, int kind);
+enum { TK_CONTRACT = 0, TK_FFT = 1, TK_COMPRESS = 2, TK_BASIS = 3 };
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+inline int ilog2(int64_t x) {
+    int r = 0;
+    while ((int64_t(1) << r) < x) ++r;
+    return r;
+}
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Block layout constants (opaque to callers; rsvd_block_bytes / rsvd_blocks_unpack are the API).
+// blocks: float2 [(Q/2 + 1)][Kpad][rows_pad], Kpad = round_up(2H, KPAD), rows_pad = round_up(rows, ROWPAD)
+constexpr int KPAD = 16;
+constexpr int ROWPAD = 64;
+inline int64_t kpad_of(int H) { return round_up(2 * (int64_t)H, KPAD); }
+inline int64_t rows_pad_of(int64_t rows) { return round_up(rows, ROWPAD); }
+
+// ------------------------------------------------------------------ complex helpers
+__host__ __device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__host__ __device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
+
+// cos(2 pi i / 64) from a quarter-wave table of exact literals (compile-time folded when i is).
+__host__ __device__ constexpr float cos64q(int i) {
+    return i == 0 ? 1.00000000000000000000f : i == 1 ? 0.99518472667219692873f
+         : i == 2 ? 0.98078528040323043058f : i == 3 ? 0.95694033573220882438f
+         : i == 4 ? 0.92387953251128673848f : i == 5 ? 0.88192126434835504956f
+         : i == 6 ? 0.83146961230254523567f : i == 7 ? 0.77301045336273699338f
+         : i == 8 ? 0.70710678118654757274f : i == 9 ? 0.63439328416364548779f
+         : i == 10 ? 0.55557023301960228867f : i == 11 ? 0.47139673682599780857f
+         : i == 12 ? 0.38268343236508983729f : i == 13 ? 0.29028467725446233105f
+         : i == 14 ? 0.19509032201612833135f : i == 15 ? 0.09801714032956077016f : 0.0f;
+}
+__host__ __device__ constexpr float cos64(int i) {
+    return ((i & 63) <= 16) ? cos64q(i & 63)
+         : ((i & 63) <= 32) ? -cos64q(32 - (i & 63))
+         : ((i & 63) <= 48) ? -cos64q((i & 63) - 32) : cos64q(64 - (i & 63));
+}
+__host__ __device__ constexpr float sin64(int i) { return cos64(i - 16); }
+
+__host__ __device__ constexpr int brev(int x, int bits) {
+    int r = 0;
+    for (int b = 0; b < bits; ++b) r |= ((x >> b) & 1) << (bits - 1 - b);
+    return r;
+}
+__host__ __device__ constexpr int clog2(int x) { return x <= 1 ? 0 : 1 + clog2(x >> 1); }
+
+// multiply by W_M^i = e^{-2 pi i * i / M} for compile-time M | 64 (M <= 64)
+template <int M, int I>
+__device__ __forceinline__ float2 c_mul_w(float2 d) {
+    constexpr int idx = (I * (64 / M)) & 63;
+    if constexpr (idx == 0) {
+        return d;
+    } else if constexpr (idx == 16) {           // e^{-i pi/2} = -i
+        return make_float2(d.y, -d.x);
+    } else if constexpr (idx == 32) {
+        return make_float2(-d.x, -d.y);
+    } else if constexpr (idx == 48) {           // +i
+        return make_float2(-d.y, d.x);
+    } else {
+        return c_mul(d, make_float2(cos64(idx), -sin64(idx)));
+    }
+}
+
+// In-register radix-2 DIF DFT of length E (E | 32): v[brev_E(k)] = sum_e v_in[e] W_E^{e k}.
+template <int E, int SPAN, int START, int I>
+struct DifBfly {
+    static __device__ __forceinline__ void run(float2 (&v)[E]) {
+        float2 a = v[START + I], b = v[START + I + SPAN];
+        v[START + I] = c_add(a, b);
+        v[START + I + SPAN] = c_mul_w<2 * SPAN, I>(c_sub(a, b));
+        if constexpr (I + 1 < SPAN) DifBfly<E, SPAN, START, I + 1>::run(v);
+    }
+};
+template <int E, int SPAN, int START>
+struct DifGroup {
+    static __device__ __forceinline__ void run(float2 (&v)[E]) {
+        DifBfly<E, SPAN, START, 0>::run(v);
+        if constexpr (START + 2 * SPAN < E) DifGroup<E, SPAN, START + 2 * SPAN>::run(v);
+    }
+};
+template <int E, int SPAN>
+struct DifStage {
+    static __device__ __forceinline__ void run(float2 (&v)[E]) {
+        DifGroup<E, SPAN, 0>::run(v);
+        if constexpr (SPAN > 1) DifStage<E, SPAN / 2>::run(v);
+    }
+};
+template <int E>
+__device__ __forceinline__ void dif_reg(float2 (&v)[E]) {
+    if constexpr (E > 1) DifStage<E, E / 2>::run(v);
+}
+
+// Radix-2 DIF DFT of length L across the lanes of an L-lane group (lanes l ^ h exchange).
+// stw[s] = W_{2h}^{l & (h-1)} for stage s (h = L/2 >> s), computed by lane_stage_twiddles.
+template <int E, int L>
+__device__ __forceinline__ void dif_lanes(float2 (&v)[E], int l, const float2 (&stw)[clog2(L) > 0 ? clog2(L) : 1]) {
+#pragma unroll
+    for (int s = 0; s < clog2(L); ++s) {
+        const int h = (L >> 1) >> s;
+        const bool upper = (l & h) != 0;
+        const float2 tw = stw[s];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            float2 p;
+            p.x = __shfl_xor_sync(0xffffffffu, v[e].x, h);
+            p.y = __shfl_xor_sync(0xffffffffu, v[e].y, h);
+            const float2 sum = c_add(v[e], p);
+            const float2 dif = c_mul(c_sub(p, v[e]), tw);
+            v[e] = upper ? dif : sum;
+        }
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void lane_stage_twiddles(int l, float2 (&stw)[clog2(L) > 0 ? clog2(L) : 1]) {
+#pragma unroll
+    for (int s = 0; s < clog2(L); ++s) {
+        const int h = (L >> 1) >> s;
+        float sn, cs;
+        sincospif((float)(l & (h - 1)) / (float)h, &sn, &cs);   // e^{-i pi j / h} = W_{2h}^j
+        stw[s] = make_float2(cs, -sn);
+    }
+    if constexpr (clog2(L) == 0) stw[0] = make_float2(1.f, 0.f);
+}
+
+// W_N^{(l * k1) mod N} for k1 < E, stored at tw[k1 * L + l] (N = L * E).
+__device__ __forceinline__ float2 twiddle_N(int l, int k1, int N) {
+    float sn, cs;
+    sincospif(2.0f * (float)((l * k1) & (N - 1)) / (float)N, &sn, &cs);
+    return make_float2(cs, -sn);
+}
+
+// Full distributed forward FFT (see file header).  twN: pointer to this lane's column of the
+// (k1, l) twiddle table (stride L), typically in shared memory.
+template <int E, int L>
+__device__ __forceinline__ void fft_dist(float2 (&v)[E], int l, const float2 *__restrict__ twN,
+                                         const float2 (&stw)[clog2(L) > 0 ? clog2(L) : 1]) {
+    dif_reg<E>(v);
+#pragma unroll
+    for (int k1 = 1; k1 < E; ++k1) {
+        const int r = brev(k1, clog2(E));
+        v[r] = c_mul(v[r], twN[k1 * L + l]);
+    }
+    dif_lanes<E, L>(v, l, stw);
+}
+
+}  // namespace rsvd

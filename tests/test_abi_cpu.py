@@ -1,0 +1,91 @@
+"""CPU-only checks of the C ABI: the library builds for sm_100a, loads, exports every symbol that
+include/rsvd.h declares (and the binding declares them all), and its host-only entry points
+(sizes, the fp64 eigen-solver, argument validation that fails before any launch) behave."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2202_07235_b200 import build
+    build.build()
+    from paper_2202_07235_b200 import _lib
+    return _lib.lib()
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "rsvd.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rsvd_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_symbols_exported_and_bound(lib):
+    from paper_2202_07235_b200 import _lib
+    names = _declared()
+    assert len(names) >= 20
+    bound = {n for n, _, _ in _lib.SIGNATURES}
+    for n in names:
+        assert hasattr(lib, n), f"{n} declared in rsvd.h but not exported"
+        assert n in bound, f"{n} not bound in _lib.SIGNATURES"
+
+
+def test_sizes(lib):
+    from paper_2202_07235_b200 import api
+    assert api.block_bytes(16384, 512, 24) == 257 * 48 * 16384 * 8
+    assert api.block_bytes(1, 32, 1) == 17 * 16 * 64 * 8
+    assert api.kernel_chunk() == 32
+    assert api.kernel_partials_bytes(8192, 128) == 256 * 128 * 128 * 8
+    assert api.align_min_workspace_bytes(512) == 64 * 64 * 256 * 8
+    assert lib.rsvd_abi_version() == 1
+
+
+def test_eigen_solver_matches_lapack(lib):
+    from paper_2202_07235_b200 import api
+    rng = np.random.default_rng(0)
+    for R in [1, 3, 16, 64, 128, 256]:
+        A = rng.standard_normal((R, R + 2))
+        C = A @ A.T
+        U, lam = api.eigen_basis(C, R)
+        ref = np.sort(np.linalg.eigvalsh(C))[::-1]
+        assert np.abs(lam - ref).max() <= 1e-13 * ref[0]
+        assert np.linalg.norm(C @ U - U * lam) <= 1e-12 * ref[0]
+        assert np.abs(U.T @ U - np.eye(R)).max() <= 1e-13
+        # sign rule: largest-|.| entry of each column is positive
+        assert np.all(U[np.abs(U).argmax(0), np.arange(R)] > 0)
+    # low-rank PSD (the synthetic kernels are numerically low-rank): deterministic, orthonormal
+    A = rng.standard_normal((128, 13))
+    C = A @ A.T
+    U1, l1 = api.eigen_basis(C, 64)
+    U2, l2 = api.eigen_basis(C, 64)
+    assert np.array_equal(U1, U2) and np.array_equal(l1, l2)
+    assert np.abs(U1.T @ U1 - np.eye(64)).max() <= 1e-13
+
+
+def test_eigen_solver_errors(lib):
+    from paper_2202_07235_b200 import api
+    with pytest.raises(api.RsvdError) as e:
+        api.eigen_basis(np.full((4, 4), np.inf), 2)
+    assert e.value.status == 4
+    with pytest.raises(api.RsvdError) as e:
+        api.eigen_basis(np.eye(4), 5)
+    assert e.value.status == 2
+
+
+def test_validation_before_launch(lib):
+    """Bad arguments are rejected on the host (no device needed)."""
+    assert lib.rsvd_compress(None, 4, 8, 48, None, None, 2, 0, None, None) == 2       # Q not pow2
+    assert lib.rsvd_compress(None, 4, 8, 2048, None, None, 2, 0, None, None) == 2     # Q too large
+    assert lib.rsvd_compress(None, 4, 300, 64, None, None, 2, 0, None, None) == 2     # R > 256
+    assert lib.rsvd_compress(None, 4, 8, 64, None, None, 9, 0, None, None) == 2       # H > R
+    assert lib.rsvd_compress(None, -1, 8, 64, None, None, 2, 0, None, None) == 1      # negative n
+    assert lib.rsvd_compress(None, 4, 8, 64, None, None, 2, 0, None, None) == 1       # NULL
+    assert lib.rsvd_compress(None, 0, 8, 64, None, None, 2, 0, None, None) == 0       # empty: no-op
+    assert lib.rsvd_align_argmax(None, 0, None, 0, 0, 64, 2, 0, None, 0, None, None, None, None) == 0
+    assert lib.rsvd_align_argmax(None, 3, None, 3, 0, 96, 2, 0, None, 0, None, None, None, None) == 2
+    assert lib.rsvd_kernel_reduce(None, 0, 8, 1, 64, None, None, None) == 1
+    assert b"Q" in lib.rsvd_last_error() or len(lib.rsvd_last_error()) > 0

@@ -1,0 +1,238 @@
+"""CUDA path vs the fp64 oracle, element by element (-m gpu).  Every call goes through the C ABI
+(librsvd.so via the ctypes binding).  Tolerances: DESIGN.md "Tolerance rules"."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import ref
+from synth import make_dataset, radial_grid, sample_pairs
+from tests.gpu_helpers import (TOL_FP32, assert_argmax_gated, assert_landscape_close, assert_per_image,
+                               cuda, to_np)
+
+pytestmark = pytest.mark.gpu
+
+api = pytest.importorskip("paper_2202_07235_b200.api")
+
+
+def _gpu_path(images, templates, w, U, H, landscape=True, per_pair=True, per_image=True, work_bytes=None):
+    """images/templates: complex64 numpy or torch; w: fp64 [R]; U: fp64 [R, H]."""
+    A = cuda(images)
+    B = cuda(templates)
+    M, R, Q = A.shape
+    T = B.shape[0]
+    wd, Ud = cuda(w, torch.float64), cuda(U, torch.float64)
+    ib = api.compress(A, wd, Ud, api.SIDE_IMAGE)
+    tb = api.compress(B, wd, Ud, api.SIDE_TEMPLATE)
+    nb = work_bytes or api.align_workspace_bytes(M, T, Q, H)
+    work = torch.empty(nb // 4, dtype=torch.float32, device="cuda")
+    out = {}
+    if landscape:
+        out["X"] = to_np(api.align_landscape(ib, M, tb, T, Q, H, work))
+    if per_pair:
+        v, k = api.align_argmax(ib, M, tb, T, Q, H, api.PER_PAIR, work)
+        out["val"], out["k"] = to_np(v), to_np(k)
+    if per_image:
+        keys = torch.zeros(M, dtype=torch.int64, device="cuda")
+        api.winners_reset(keys)
+        api.align_argmax(ib, M, tb, T, Q, H, api.PER_IMAGE, work, best_key=keys)
+        v, t, k = api.winners_unpack(keys, Q)
+        out["img"] = (to_np(v), to_np(t), to_np(k))
+    torch.cuda.synchronize()
+    return out
+
+
+def _check_all(out, X_ref, tol=TOL_FP32):
+    M, T, Q = X_ref.shape
+    tol_abs = tol * np.abs(X_ref).max()
+    if "X" in out:
+        assert_landscape_close(out["X"], X_ref, tol)
+    if "val" in out:
+        assert np.abs(out["val"] - X_ref.max(-1)).max() <= tol_abs
+        assert_argmax_gated(out["k"].reshape(-1), X_ref.reshape(-1, Q), tol_abs)
+    if "img" in out:
+        assert_per_image(*out["img"], X_ref, tol_abs)
+
+
+def _all_pairs(M, T):
+    ia, ib = np.meshgrid(np.arange(M), np.arange(T), indexing="ij")
+    return ia.ravel(), ib.ravel()
+
+
+# ------------------------------------------------------------------ Tiny: everything, all pairs
+def test_tiny_all_pairs_rank_H_and_full_rank():
+    d = make_dataset("tiny")
+    A, B, w = to_np(d.images), to_np(d.templates), to_np(d.w)
+    M, T, Q, R = A.shape[0], B.shape[0], d.Q, d.R
+    ia, ib = _all_pairs(M, T)
+    for H in [4, R]:
+        U, lam = api.build_basis(cuda(B), w, H)
+        X_ref = ref.landscape_rank(A, B, w, U, ia, ib).real.reshape(M, T, Q)
+        _check_all(_gpu_path(A, B, w, U, H), X_ref)
+    # H = R: the library path reproduces the uncompressed direct sum O1
+    X_full = ref.landscape_full(A, B, w, ia, ib).real.reshape(M, T, Q)
+    U, _ = api.build_basis(cuda(B), w, R)
+    out = _gpu_path(A, B, w, U, R, per_pair=False, per_image=False)
+    assert_landscape_close(out["X"], X_full)
+
+
+def test_basis_parity_and_determinism():
+    for name, T in [("tiny", None), ("small", 256)]:
+        d = make_dataset(name, T=T, M=8)
+        B, w = to_np(d.templates), to_np(d.w)
+        R = d.R
+        U, lam = api.build_basis(cuda(B), w, R)
+        U2, lam2 = api.build_basis(cuda(B), w, R)
+        assert np.array_equal(U, U2) and np.array_equal(lam, lam2)        # bitwise reproducible
+        C_ref = ref.kernel_C(B, w)
+        Ur, lr = ref.basis(C_ref, R)
+        assert np.abs(lam - lr).max() <= 1e-12 * lr[0]
+        assert np.linalg.norm(C_ref @ U - U * lam[None, :]) <= 1e-11 * lr[0]
+        # projector agreement on the non-null eigenspace up to each well-separated gap
+        nz = int((lr > 1e-9 * lr[0]).sum())
+        for h in range(1, nz):
+            relgap = (lr[h - 1] - lr[h]) / lr[0]
+            if relgap < 1e-6:
+                continue
+            P = U[:, :h] @ U[:, :h].T
+            Pr = Ur[:, :h] @ Ur[:, :h].T
+            assert np.linalg.norm(P - Pr, 2) <= 1e-9 / relgap, (name, h, relgap)
+
+
+def test_compress_parity():
+    d = make_dataset("small", M=40, T=24)
+    A, B, w = to_np(d.images), to_np(d.templates), to_np(d.w)
+    H = 8
+    U, _ = api.build_basis(cuda(B), w, H)
+    for rings, side in [(A, api.SIDE_IMAGE), (B, api.SIDE_TEMPLATE)]:
+        blocks = api.compress(cuda(rings), cuda(w, torch.float64), cuda(U, torch.float64), side)
+        got = to_np(api.blocks_unpack(blocks, rings.shape[0], d.Q, H, side))       # [n, Q, H]
+        coef = ref.fb_coefficients(rings)                                           # [n, R, Q]
+        want = np.einsum("rh,nrq->nqh", U * np.sqrt(w)[:, None], coef)
+        err = np.abs(got - want).max() / np.abs(want).max()
+        assert err <= 2e-6, err
+
+
+def test_small_full_argmax_sampled_pairs():
+    d = make_dataset("small", device="cuda")
+    H = 8
+    U, _ = api.build_basis(d.templates, to_np(d.w), H)
+    M, T, Q = d.images.shape[0], d.templates.shape[0], d.Q
+    out = _gpu_path(d.images, d.templates, to_np(d.w), U, H, landscape=False, per_image=True)
+    m, t = sample_pairs("small", M, T, 4096, 1024, to_np(d.t_true))
+    A, B, w = to_np(d.images), to_np(d.templates), to_np(d.w)
+    X_ref = ref.landscape_rank(A, B, w, U, m, t).real
+    tol_abs = TOL_FP32 * np.abs(X_ref).max()
+    assert np.abs(out["val"][m, t] - X_ref.max(-1)).max() <= tol_abs
+    assert_argmax_gated(out["k"][m, t], X_ref, tol_abs)
+    # per-image winners of a few images over all templates
+    for mm in [0, 1, 517, 1023]:
+        Xi = ref.landscape_rank(A, B, w, U, np.full(T, mm), np.arange(T)).real
+        v, tt, kk = (x[mm:mm + 1] for x in out["img"])
+        assert_per_image(v, tt, kk, Xi[None], TOL_FP32 * max(np.abs(Xi).max(), np.abs(X_ref).max()))
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("M,T,R,Q,H", [
+    (1, 1, 4, 32, 1),          # minimum Q, H = 1, single pair
+    (70, 130, 9, 32, 9),       # ragged tiles, H = R, odd R
+    (65, 3, 16, 64, 5),        # ragged, tiny T
+    (3, 67, 12, 128, 7),
+    (2, 5, 8, 1024, 3),        # maximum Q
+    (9, 11, 33, 256, 33),      # K = 2H not a multiple of 16
+])
+def test_edge_shapes_random_rings(M, T, R, Q, H):
+    rng = np.random.default_rng(M * 1000 + T)
+    A = (rng.standard_normal((M, R, Q)) + 1j * rng.standard_normal((M, R, Q))).astype(np.complex64)
+    B = (rng.standard_normal((T, R, Q)) + 1j * rng.standard_normal((T, R, Q))).astype(np.complex64)
+    k, w = radial_grid(R)
+    U, _ = api.build_basis(cuda(B), w, H)
+    ia, ib = _all_pairs(M, T)
+    X_ref = ref.landscape_rank(A, B, w, U, ia, ib).real.reshape(M, T, Q)
+    _check_all(_gpu_path(A, B, w, U, H), X_ref)
+
+
+def test_small_workspace_many_chunks():
+    """Minimum workspace forces one 64x64 tile per chunk: results identical to one big chunk."""
+    d = make_dataset("small", M=200, T=150)
+    A, B, w = to_np(d.images), to_np(d.templates), to_np(d.w)
+    U, _ = api.build_basis(cuda(B), w, 8)
+    big = _gpu_path(A, B, w, U, 8, landscape=True)
+    small = _gpu_path(A, B, w, U, 8, landscape=True, work_bytes=api.align_min_workspace_bytes(d.Q))
+    for key in ["X", "val", "k"]:
+        assert np.array_equal(big[key], small[key])
+    for a, b in zip(big["img"], small["img"]):
+        assert np.array_equal(a, b)
+
+
+def test_ties_smallest_index():
+    """Constant landscapes (all-zero rings): per-pair k = 0, per-image (t, k) = (0, 0)."""
+    M, T, R, Q, H = 3, 5, 4, 64, 2
+    A = np.zeros((M, R, Q), np.complex64)
+    B = np.zeros((T, R, Q), np.complex64)
+    k, w = radial_grid(R)
+    U = np.eye(R)[:, :H]
+    out = _gpu_path(A, B, w, U, H)
+    assert np.all(out["k"] == 0) and np.all(out["val"] == 0)
+    v, t, kk = out["img"]
+    assert np.all(t == 0) and np.all(kk == 0)
+
+
+def test_on_grid_rotation_recovered_exactly():
+    """P2 through the library: image = template cyclically shifted by k0 -> argmax k0 (H = R)."""
+    rng = np.random.default_rng(11)
+    R, Q = 8, 128
+    B = (rng.standard_normal((4, R, Q)) + 1j * rng.standard_normal((4, R, Q))).astype(np.complex64)
+    shifts = np.array([0, 1, 77, 127])
+    A = np.stack([np.roll(B[i], s, axis=-1) for i, s in enumerate(shifts)])
+    k, w = radial_grid(R)
+    U, _ = api.build_basis(cuda(B), w, R)
+    out = _gpu_path(A, B, w, U, R, landscape=False)
+    assert list(np.diag(out["k"])) == list(shifts)
+    v, t, kk = out["img"]
+    assert list(t) == [0, 1, 2, 3] and list(kk) == list(shifts)
+
+
+def test_empty_problems_are_noops():
+    R, Q, H = 4, 64, 2
+    k, w = radial_grid(R)
+    wd, Ud = cuda(w, torch.float64), cuda(np.eye(R)[:, :H], torch.float64)
+    blocks = torch.empty(16, dtype=torch.float32, device="cuda")
+    lib = api._lib.lib()
+    assert lib.rsvd_compress(blocks.data_ptr(), 0, R, Q, wd.data_ptr(), Ud.data_ptr(), H, 0,
+                             blocks.data_ptr(), None) == 0
+    work = torch.empty(api.align_min_workspace_bytes(Q) // 4, dtype=torch.float32, device="cuda")
+    assert lib.rsvd_align_argmax(blocks.data_ptr(), 0, blocks.data_ptr(), 5, 0, Q, H, 0, work.data_ptr(),
+                                 work.numel() * 4, None, None, None, None) == 0
+
+
+def test_error_paths():
+    R, Q, H = 4, 64, 2
+    k, w = radial_grid(R)
+    lib = api._lib.lib()
+    rings = torch.zeros((2, R, Q), dtype=torch.complex64, device="cuda")
+    wd, Ud = cuda(w, torch.float64), cuda(np.eye(R)[:, :H], torch.float64)
+    blocks = torch.empty(api.block_bytes(2, Q, H) // 4, dtype=torch.float32, device="cuda")
+    p = rings.data_ptr()
+    assert lib.rsvd_compress(p, 2, R, 48, wd.data_ptr(), Ud.data_ptr(), H, 0, blocks.data_ptr(), None) == 2
+    assert lib.rsvd_compress(p, 2, R, 16, wd.data_ptr(), Ud.data_ptr(), H, 0, blocks.data_ptr(), None) == 2
+    assert lib.rsvd_compress(p, 2, R, Q, wd.data_ptr(), Ud.data_ptr(), R + 1, 0, blocks.data_ptr(), None) == 2
+    assert lib.rsvd_compress(p, -1, R, Q, wd.data_ptr(), Ud.data_ptr(), H, 0, blocks.data_ptr(), None) == 1
+    assert lib.rsvd_compress(None, 2, R, Q, wd.data_ptr(), Ud.data_ptr(), H, 0, blocks.data_ptr(), None) == 1
+    assert lib.rsvd_compress(p + 8, 2, R, Q, wd.data_ptr(), Ud.data_ptr(), H, 0, blocks.data_ptr(), None) == 1
+    assert lib.rsvd_compress(p, 2, R, Q, wd.data_ptr(), Ud.data_ptr(), H, 7, blocks.data_ptr(), None) == 1
+    bad_w = w.copy()
+    bad_w[1] = np.nan
+    U = np.zeros((R, H))
+    assert lib.rsvd_build_basis(p, 2, R, Q, bad_w.ctypes.data, H, U.ctypes.data, None, None) == 1
+    bad_w[1] = -1.0
+    assert lib.rsvd_build_basis(p, 2, R, Q, bad_w.ctypes.data, H, U.ctypes.data, None, None) == 1
+    work = torch.empty(1024, dtype=torch.float32, device="cuda")
+    b = blocks.data_ptr()
+    assert lib.rsvd_align_argmax(b, 2, b, 2, 0, Q, H, 0, work.data_ptr(), 4096, b, b, None, None) == 1  # small work
+    big = torch.empty(api.align_min_workspace_bytes(Q) // 4, dtype=torch.float32, device="cuda")
+    assert lib.rsvd_align_argmax(b, 2, b, 2, 0, Q, H, 0, big.data_ptr(), big.numel() * 4, None, None, None, None) == 1
+    assert lib.rsvd_align_argmax(b, 2, b, 2, 0, Q, H, 1, big.data_ptr(), big.numel() * 4, None, None, None, None) == 1
+    assert lib.rsvd_align_argmax(b, 2, b, 2, 1 << 30, Q, H, 1, big.data_ptr(), big.numel() * 4, None, None, b,
+                                 None) == 2
+    assert lib.rsvd_align_argmax(b, 2, b, 2, 0, Q, H, 9, big.data_ptr(), big.numel() * 4, b, b, b, None) == 1
+    assert len(lib.rsvd_last_error()) > 0
