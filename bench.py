@@ -52,6 +52,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--work-mb", type=int, default=None, help="align workspace (default: library recommendation)")
     return p.parse_args()
 
 
@@ -207,7 +208,8 @@ def run_ours(args):
     w_dev = ds.w.contiguous()
     ib = torch.empty(api.block_bytes(M, Q, H) // 4, dtype=torch.float32, device=dev)
     tb = torch.empty(max(api.block_bytes(T_loc, Q, H), 16) // 4, dtype=torch.float32, device=dev)
-    work = torch.empty(api.align_workspace_bytes(M, T_loc, Q, H) // 4, dtype=torch.float32, device=dev)
+    wbytes = args.work_mb * (1 << 20) if args.work_mb else api.align_workspace_bytes(M, T_loc, Q, H)
+    work = torch.empty(wbytes // 4, dtype=torch.float32, device=dev)
     keys = torch.zeros(M, dtype=torch.int64, device=dev)
     U_dev = torch.zeros((R, H), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
@@ -363,7 +365,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "M": M, "T": T, "R": R, "Q": Q, "H": H, "mode": "per_image",
-                       "parallelism": f"template-sharded x{world} (NCCL all-gather of winners)",
+                       "workspace_mb": round(wbytes / 2**20, 1), "parallelism": f"template-sharded x{world} (NCCL all-gather of winners)",
                        "l2": "inputs larger than L2 (rings %.1f GB per step)" % ((images.numel() + T * R * Q) * 8 / 1e9),
                        "seed": 220207235},
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,

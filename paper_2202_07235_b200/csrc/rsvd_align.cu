@@ -3,12 +3,10 @@
 //
 // Data flow per chunk of (Mc x Tc) pairs, all on `stream`:
 //   contract_kernel   U_q[m,t] = sum_j alpha[q][j][m] beta[q][j][t] = S_q + conj(S_{Q-q}), q = 0..N
-//                     (N = Q/2; S_q = sum_h conj(A_q[m,h]) B_q[t,h]) -> workspace Upk[pair][n]
-//                     (Upk[.][0] packs the two real values (U_0, U_N)).  FP32 SIMT, register tiled.
-//   fft_reduce_kernel Re X_k = 2 pi Re sum_q e^{-2 pi i qk/Q} S_q = 2 pi sum_q e^{-2pi i qk/Q} Y_q,
-//                     Y_q = U_q / 2 (Hermitian part).  Computed as a length-N complex FFT of
-//                     Z_n = (Y_n + conj Y_{N-n}) + i w_Q^n (Y_n - conj Y_{N-n}) whose output z_n
-//                     packs x_{2n} = Re z_n, x_{2n+1} = Im z_n (real-output FFT identity).  Then the
+//                     (N = Q/2; S_q = sum_h conj(A_q[m,h]) B_q[t,h]) -> workspace Upk[n][m][t] (q-major,
+//                     coalesced stores; Upk[0] packs the two real values (U_0, U_N)).  FP32 SIMT,
+//                     register tiled, cp.async double-buffered operand tiles.
+//   fft_reduce_kernel (rsvd_fft.cuh) Re X_k = 2 pi Re sum_q e^{-2 pi i qk/Q} S_q, fused with the
 //                     per-pair argmax (smallest k on ties), the per-image packed-key max, or the
 //                     landscape store.  The M x T x Q landscape never leaves the chip unless asked.
 // The workspace chunk is sized to stay L2-resident between the two kernels.
@@ -18,10 +16,12 @@
 #include <cmath>
 
 #include "rsvd_common.cuh"
+#include "rsvd_fft.cuh"
 
 namespace rsvd {
 
 // ------------------------------------------------------------------ contraction (Step 2)
+// Spectrum workspace layout (q-major): Upk[(n * Mc + ml) * Tc + tl], n in [0, N), ml < Mc, tl < Tc.
 constexpr int CT_TILE = 64;    // m and t tile
 constexpr int CT_KC = 16;      // complex K per pipeline stage
 constexpr int CT_QB = 4;       // q values per CTA
@@ -35,16 +35,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int NWAIT>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NWAIT)); }
 
-// grid: (Tc/64, Mc/64, ceil((N+1)/QB)); Upk[(ml * Tc + tl) * N + n]
-__global__ void __launch_bounds__(CT_THREADS) contract_kernel(const float2 *__restrict__ alpha,
-                                                              const float2 *__restrict__ beta,
-                                                              int64_t Mpad, int64_t Tpad, int Kpad, int N,
-                                                              int64_t m0, int64_t t0, int64_t Tc,
-                                                              float2 *__restrict__ Upk) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2 *As = reinterpret_cast<float2 *>(smem_raw);                    // [2][KC][64]
-    float2 *Bs = As + 2 * CT_KC * CT_TILE;                                // [2][KC][64]
-    float2 *stage = Bs + 2 * CT_KC * CT_TILE;                              // [QB][64*64]
+// grid: (Tc/64, Mc/64, ceil((N+1)/QB)).  Thread (ty, tx) owns m = ty*4 + i, t = tx + 16 j.
+__global__ void __launch_bounds__(CT_THREADS, 3) contract_kernel(const float2 *__restrict__ alpha,
+                                                                 const float2 *__restrict__ beta,
+                                                                 int64_t Mpad, int64_t Tpad, int Kpad, int N,
+                                                                 int64_t m0, int64_t t0, int64_t Mc, int64_t Tc,
+                                                                 float2 *__restrict__ Upk) {
+    __shared__ __align__(16) float2 As[2][CT_KC][CT_TILE];
+    __shared__ __align__(16) float2 Bs[2][CT_KC][CT_TILE];
 
     const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
     const int64_t bt = (int64_t)blockIdx.x * CT_TILE, bm = (int64_t)blockIdx.y * CT_TILE;
@@ -57,14 +55,11 @@ __global__ void __launch_bounds__(CT_THREADS) contract_kernel(const float2 *__re
         const int q = q0 + it / nk, kc = it % nk;
         const float2 *ga = alpha + ((int64_t)q * Kpad + kc * CT_KC) * Mpad + m0 + bm;
         const float2 *gb = beta + ((int64_t)q * Kpad + kc * CT_KC) * Tpad + t0 + bt;
-        float2 *sa = As + buf * CT_KC * CT_TILE;
-        float2 *sb = Bs + buf * CT_KC * CT_TILE;
-        // KC rows x 64 complex = KC x 32 16-byte chunks per operand
 #pragma unroll
         for (int c = tid; c < CT_KC * 32; c += CT_THREADS) {
             const int kk = c >> 5, ch = c & 31;
-            cp_async16(sa + kk * CT_TILE + ch * 2, ga + (int64_t)kk * Mpad + ch * 2);
-            cp_async16(sb + kk * CT_TILE + ch * 2, gb + (int64_t)kk * Tpad + ch * 2);
+            cp_async16(&As[buf][kk][ch * 2], ga + (int64_t)kk * Mpad + ch * 2);
+            cp_async16(&Bs[buf][kk][ch * 2], gb + (int64_t)kk * Tpad + ch * 2);
         }
         cp_async_commit();
     };
@@ -87,17 +82,15 @@ __global__ void __launch_bounds__(CT_THREADS) contract_kernel(const float2 *__re
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
         }
-        const float2 *sa = As + buf * CT_KC * CT_TILE;
-        const float2 *sb = Bs + buf * CT_KC * CT_TILE;
 #pragma unroll
         for (int kk = 0; kk < CT_KC; ++kk) {
-            const float4 a01 = *reinterpret_cast<const float4 *>(sa + kk * CT_TILE + ty * 4);
-            const float4 a23 = *reinterpret_cast<const float4 *>(sa + kk * CT_TILE + ty * 4 + 2);
+            const float4 a01 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4]);
+            const float4 a23 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4 + 2]);
             const float2 a[4] = {make_float2(a01.x, a01.y), make_float2(a01.z, a01.w),
                                  make_float2(a23.x, a23.y), make_float2(a23.z, a23.w)};
             float2 b[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = sb[kk * CT_TILE + tx + 16 * j];
+            for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk][tx + 16 * j];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -108,180 +101,25 @@ __global__ void __launch_bounds__(CT_THREADS) contract_kernel(const float2 *__re
                     acc[i][j].y = fmaf(a[i].y, b[j].x, acc[i][j].y);
                 }
         }
-        if (kc == nk - 1) {
-            const int qi = it / nk;
-            float2 *st = stage + qi * CT_TILE * CT_TILE;
+        if (kc == nk - 1) {          // q finished: coalesced q-major store (16 lanes = 128 B per row)
+            const int q = q0 + it / nk;
+            const int n = (q == N) ? 0 : q;
+            float2 *dst = Upk + ((int64_t)n * Mc + bm) * Tc + bt;
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) st[(ty * 4 + i) * CT_TILE + tx + 16 * j] = acc[i][j];
+                for (int j = 0; j < 4; ++j) {
+                    float2 *p = dst + (int64_t)(ty * 4 + i) * Tc + tx + 16 * j;
+                    if (q == 0) reinterpret_cast<float *>(p)[0] = acc[i][j].x;        // U_0 (real)
+                    else if (q == N) reinterpret_cast<float *>(p)[1] = acc[i][j].x;   // U_N (real)
+                    else *p = acc[i][j];
+                }
         }
         __syncthreads();
     }
-    // write Upk: each pair gets its q0..q0+nq-1 entries (32 B when nq == 4)
-    for (int p = tid; p < CT_TILE * CT_TILE; p += CT_THREADS) {
-        const int ml = p >> 6, tl = p & 63;
-        float2 *dst = Upk + ((bm + ml) * Tc + bt + tl) * (int64_t)N;
-        if (q0 == N) {                 // only q = N: its real part goes to slot 0 .y
-            reinterpret_cast<float *>(dst)[1] = stage[p].x;
-            continue;
-        }
-        if (q0 == 0) {
-            reinterpret_cast<float *>(dst)[0] = stage[p].x;   // U_0 (real) to slot 0 .x
-            for (int qi = 1; qi < nq; ++qi) dst[qi] = stage[qi * CT_TILE * CT_TILE + p];
-            continue;
-        }
-        if (nq == 4) {
-            const float2 v0 = stage[p], v1 = stage[CT_TILE * CT_TILE + p];
-            const float2 v2 = stage[2 * CT_TILE * CT_TILE + p], v3 = stage[3 * CT_TILE * CT_TILE + p];
-            reinterpret_cast<float4 *>(dst + q0)[0] = make_float4(v0.x, v0.y, v1.x, v1.y);
-            reinterpret_cast<float4 *>(dst + q0)[1] = make_float4(v2.x, v2.y, v3.x, v3.y);
-        } else {
-            for (int qi = 0; qi < nq; ++qi) dst[q0 + qi] = stage[qi * CT_TILE * CT_TILE + p];
-        }
-    }
 }
 
-// ------------------------------------------------------------------ FFT + reduce (Steps 3-4)
-enum { MODE_PAIR = 0, MODE_IMAGE = 1, MODE_LANDSCAPE = 2 };
-constexpr int FR_THREADS = 256;
-constexpr int FR_TPAIRS = 64;    // templates per CTA (one image row per CTA)
-
-__device__ __forceinline__ uint32_t ord_f32(float v) {
-    const uint32_t u = __float_as_uint(v);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-
-// grid: (ceil(tcv / 64), mcv).  Upk rows of the chunk have stride Tc pairs.
-template <int LOGN, int MODE>
-__global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(
-    const float2 *__restrict__ Upk, int64_t Tc, int64_t m0, int64_t t0, int64_t tcv, int64_t T,
-    int64_t t_offset, float *__restrict__ best_val, int32_t *__restrict__ best_k,
-    unsigned long long *__restrict__ best_key, float *__restrict__ X, int64_t ld_m, int64_t ld_t) {
-    constexpr int N = 1 << LOGN;
-    constexpr int Q = 2 * N;
-    constexpr int L = N < 32 ? N : 32;
-    constexpr int E = N / L;
-    constexpr int G = 32 / L;                 // pairs per warp in flight
-    constexpr int SLOTS = (FR_THREADS / 32) * G;
-    constexpr int PER_SLOT = FR_TPAIRS / SLOTS;
-    __shared__ float2 twN[E * L];             // W_N^{l k1}
-    __shared__ float2 pre[E * L];             // W_Q^{n}, n = l + L e
-    __shared__ unsigned long long skey;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = lane / L, l = lane % L;
-    for (int i = tid; i < E * L; i += FR_THREADS) {
-        twN[i] = twiddle_N(i % L, i / L, N);
-        float sn, cs;
-        sincospif(2.0f * (float)((i % L) + L * (i / L)) / (float)Q, &sn, &cs);
-        pre[i] = make_float2(cs, -sn);
-    }
-    if (tid == 0) skey = 0ull;
-    float2 stw[clog2(L) > 0 ? clog2(L) : 1];
-    lane_stage_twiddles<L>(l, stw);
-    __syncthreads();
-
-    const int64_t ml = blockIdx.y;
-    const int64_t m = m0 + ml;
-    const int slot = warp * G + g;
-    const float PI = 3.14159265358979323846f;
-    unsigned long long mykey = 0ull;
-
-    for (int i = 0; i < PER_SLOT; ++i) {
-        const int64_t tl = (int64_t)blockIdx.x * FR_TPAIRS + slot + (int64_t)SLOTS * i;
-        const bool valid = tl < tcv;
-        const float2 *src = Upk + (ml * Tc + (valid ? tl : 0)) * (int64_t)N;
-        float2 u[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) u[e] = src[l + L * e];
-        // mirror M = U_{N-n}
-        float2 z[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const int srcl = g * L + ((L - l) & (L - 1));
-            float2 mm;
-            mm.x = __shfl_sync(0xffffffffu, u[E - 1 - e].x, srcl);
-            mm.y = __shfl_sync(0xffffffffu, u[E - 1 - e].y, srcl);
-            if (l == 0) mm = u[(E - e) % E];
-            const float2 uu = u[e];
-            const float2 s = make_float2(uu.x + mm.x, uu.y - mm.y);    // U + conj M
-            const float2 d = make_float2(uu.x - mm.x, uu.y + mm.y);    // U - conj M
-            const float2 wd = c_mul(pre[e * L + l], d);
-            z[e] = make_float2(PI * (s.x - wd.y), PI * (s.y + wd.x)); // pi (s + i w d)
-        }
-        if (l == 0) {   // n = 0: slot 0 packs the reals (U_0, U_N)
-            const float u0 = u[0].x, un = u[0].y;
-            z[0] = make_float2(PI * (u0 + un), PI * (u0 - un));
-        }
-        fft_dist<E, L>(z, l, twN, stw);
-        const int b = (int)(__brev((unsigned)l) >> (32 - clog2(L)));
-        if constexpr (MODE == MODE_LANDSCAPE) {
-            if (valid) {
-                float *dst = X + m * ld_m + (t0 + tl) * ld_t + 2 * E * b;
-#pragma unroll
-                for (int k1 = 0; k1 < E; ++k1)
-                    reinterpret_cast<float2 *>(dst)[k1] = z[brev(k1, clog2(E))];
-            }
-        } else {
-            float bv = -INFINITY;
-            int bk = 0x7fffffff;
-#pragma unroll
-            for (int k1 = 0; k1 < E; ++k1) {
-                const float2 v = z[brev(k1, clog2(E))];
-                const int k = 2 * (k1 + E * b);
-                if (v.x > bv) { bv = v.x; bk = k; }          // indices increase with k1
-                if (v.y > bv) { bv = v.y; bk = k + 1; }
-            }
-#pragma unroll
-            for (int off = L / 2; off >= 1; off >>= 1) {
-                const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-                const int ok = __shfl_xor_sync(0xffffffffu, bk, off);
-                if (ov > bv || (ov == bv && ok < bk)) { bv = ov; bk = ok; }
-            }
-            if constexpr (MODE == MODE_PAIR) {
-                if (valid && l == 0) {
-                    const int64_t o = m * T + t0 + tl;
-                    best_val[o] = bv;
-                    best_k[o] = bk;
-                }
-            } else {
-                if (valid) {
-                    const uint32_t idx = (uint32_t)((t_offset + t0 + tl) * Q + bk);
-                    const unsigned long long key =
-                        ((unsigned long long)ord_f32(bv) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
-                    mykey = key > mykey ? key : mykey;
-                }
-            }
-        }
-    }
-    if constexpr (MODE == MODE_IMAGE) {
-        if (l == 0 && mykey) atomicMax(&skey, mykey);
-        __syncthreads();
-        if (tid == 0 && skey) atomicMax(best_key + m, skey);
-    }
-}
-
-template <int LOGN>
-static cudaError_t launch_fft(int mode, dim3 grid, cudaStream_t s, const float2 *Upk, int64_t Tc, int64_t m0,
-                              int64_t t0, int64_t tcv, int64_t T, int64_t t_offset, float *best_val,
-                              int32_t *best_k, unsigned long long *best_key, float *X, int64_t ld_m, int64_t ld_t) {
-    if (mode == MODE_PAIR)
-        fft_reduce_kernel<LOGN, MODE_PAIR><<<grid, FR_THREADS, 0, s>>>(Upk, Tc, m0, t0, tcv, T, t_offset, best_val,
-                                                                       best_k, best_key, X, ld_m, ld_t);
-    else if (mode == MODE_IMAGE)
-        fft_reduce_kernel<LOGN, MODE_IMAGE><<<grid, FR_THREADS, 0, s>>>(Upk, Tc, m0, t0, tcv, T, t_offset, best_val,
-                                                                        best_k, best_key, X, ld_m, ld_t);
-    else
-        fft_reduce_kernel<LOGN, MODE_LANDSCAPE><<<grid, FR_THREADS, 0, s>>>(Upk, Tc, m0, t0, tcv, T, t_offset,
-                                                                            best_val, best_k, best_key, X, ld_m, ld_t);
-    return cudaGetLastError();
-}
-
-static size_t contract_smem() {
-    return (size_t)(4 * CT_KC * CT_TILE + CT_QB * CT_TILE * CT_TILE) * sizeof(float2);
-}
-
+// ------------------------------------------------------------------ driver
 struct AlignArgs {
     const float2 *alpha, *beta;
     int64_t M, T, t_offset;
@@ -295,6 +133,18 @@ struct AlignArgs {
     float *X;
     int64_t ld_m, ld_t;
 };
+
+static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const float2 *Upk, int64_t Mc, int64_t Tc,
+                                  int64_t m0, int64_t t0, int64_t mcv, int64_t tcv, const FftOut &o) {
+    switch (LOGN) {
+        case 4: return launch_fft<4>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
+        case 5: return launch_fft<5>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
+        case 6: return launch_fft<6>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
+        case 7: return launch_fft<7>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
+        case 8: return launch_fft<8>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
+        default: return launch_fft<9>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
+    }
+}
 
 static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const int N = a.Q / 2;
@@ -311,9 +161,8 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     tct = std::min(tmax, std::max(tct, ntiles / mct));      // widen t when rows run out
     const int64_t Mc = mct * CT_TILE, Tc = tct * CT_TILE;
     float2 *Upk = reinterpret_cast<float2 *>(a.work);
-    const size_t smem = contract_smem();
-    cudaError_t e = cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_check(e, "contract smem attribute");
+    const FftOut o{a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t, a.T, a.t_offset};
+    cudaError_t e;
     const int LOGN = ilog2(N);
     const bool timed = timing_enabled();
     for (int64_t m0 = 0; m0 < Mpad; m0 += Mc) {
@@ -324,18 +173,10 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
             const int64_t tcv = std::min(tc, a.T - t0);
             dim3 g1((unsigned)(tc / CT_TILE), (unsigned)(mc / CT_TILE), (unsigned)((N + 1 + CT_QB - 1) / CT_QB));
             cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
-            contract_kernel<<<g1, CT_THREADS, smem, s>>>(a.alpha, a.beta, Mpad, Tpad, Kpad, N, m0, t0, Tc, Upk);
+            contract_kernel<<<g1, CT_THREADS, 0, s>>>(a.alpha, a.beta, Mpad, Tpad, Kpad, N, m0, t0, Mc, Tc, Upk);
             if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "contract launch");
             cudaEvent_t ev1 = timed ? timing_event(s) : nullptr;
-            dim3 g2((unsigned)((tcv + FR_TPAIRS - 1) / FR_TPAIRS), (unsigned)mcv);
-            switch (LOGN) {
-                case 4: e = launch_fft<4>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
-                case 5: e = launch_fft<5>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
-                case 6: e = launch_fft<6>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
-                case 7: e = launch_fft<7>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
-                case 8: e = launch_fft<8>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
-                default: e = launch_fft<9>(a.mode, g2, s, Upk, Tc, m0, t0, tcv, a.T, a.t_offset, a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t); break;
-            }
+            e = launch_fft_any(LOGN, a.mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
             if (e != cudaSuccess) return cuda_check(e, "fft_reduce launch");
             count_launches(2);
             if (timed) {
