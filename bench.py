@@ -53,6 +53,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--work-mb", type=int, default=None, help="align workspace (default: library recommendation)")
+    p.add_argument("--path", default=None, choices=["auto", "simt", "tc"], help="contraction path override")
     return p.parse_args()
 
 
@@ -206,8 +207,11 @@ def run_ours(args):
     M = images.shape[0]
     T_loc = tmpl.shape[0]
     w_dev = ds.w.contiguous()
-    ib = torch.empty(api.block_bytes(M, Q, H) // 4, dtype=torch.float32, device=dev)
-    tb = torch.empty(max(api.block_bytes(T_loc, Q, H), 16) // 4, dtype=torch.float32, device=dev)
+    if args.path:
+        api.set_path({"simt": api.PATH_SIMT, "tc": api.PATH_TC, "auto": api.PATH_AUTO}[args.path])
+    path = api.path_for(Q, H)
+    ib = torch.empty(api.block_bytes(M, Q, H, api.SIDE_IMAGE) // 4, dtype=torch.float32, device=dev)
+    tb = torch.empty(max(api.block_bytes(T_loc, Q, H, api.SIDE_TEMPLATE), 16) // 4, dtype=torch.float32, device=dev)
     wbytes = args.work_mb * (1 << 20) if args.work_mb else api.align_workspace_bytes(M, T_loc, Q, H)
     work = torch.empty(wbytes // 4, dtype=torch.float32, device=dev)
     keys = torch.zeros(M, dtype=torch.int64, device=dev)

@@ -55,13 +55,21 @@ typedef enum { RSVD_PER_PAIR = 0, RSVD_PER_IMAGE = 1 } rsvd_reduce;
 
 /* Thread-local message describing the last non-OK status returned on this thread. */
 const char *rsvd_last_error(void);
-/* ABI version of this header (bumped when a signature or the block layout changes). */
+/* ABI version of this header (bumped when a signature or the block layout changes): 2. */
 int32_t rsvd_abi_version(void);
 
 /* ------------------------------------------------------------------ sizes */
-/* Bytes of one compressed block buffer holding `rows` images or templates at (Q, H).
- * The block layout is opaque; read it back only through rsvd_blocks_unpack. */
-int64_t rsvd_block_bytes(int64_t rows, int32_t Q, int32_t H);
+/* Bytes of one compressed block buffer holding `rows` images (side IMAGE) or templates (side
+ * TEMPLATE) at (Q, H).  The layout is opaque (it depends on the contraction path, see
+ * rsvd_path_for); read it back only through rsvd_blocks_unpack. */
+int64_t rsvd_block_bytes(int64_t rows, int32_t Q, int32_t H, rsvd_side side);
+/* Contraction path used for (Q, H): 1 = FP32 SIMT, 2 = tcgen05 tensor cores with 3xTF32 error
+ * compensation (~fp32 accuracy).  Default (AUTO): tensor cores whenever a row's H x Q coefficient
+ * block fits in shared memory (H * Q <= 24576), else SIMT.  rsvd_set_path(0 auto | 1 simt | 2 tc)
+ * overrides it process-wide (also env RSVD_PATH=auto|simt|tc); blocks must be produced and consumed
+ * under the same path. */
+int32_t rsvd_path_for(int32_t Q, int32_t H);
+void rsvd_set_path(int32_t path);
 /* Templates per fixed chunk of the kernel-matrix partial sums (rsvd_kernel_partials). */
 int64_t rsvd_kernel_chunk(void);
 /* Bytes of the partial-sum buffer for T templates with R rings: ceil(T/chunk) * R * R doubles. */

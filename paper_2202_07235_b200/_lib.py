@@ -21,7 +21,9 @@ _P, _I32, _I64, _D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_v
 SIGNATURES = [
     ("rsvd_last_error", ctypes.c_char_p, []),
     ("rsvd_abi_version", _I32, []),
-    ("rsvd_block_bytes", _I64, [_I64, _I32, _I32]),
+    ("rsvd_block_bytes", _I64, [_I64, _I32, _I32, _I32]),
+    ("rsvd_path_for", _I32, [_I32, _I32]),
+    ("rsvd_set_path", None, [_I32]),
     ("rsvd_kernel_chunk", _I64, []),
     ("rsvd_kernel_partials_bytes", _I64, [_I64, _I32]),
     ("rsvd_align_workspace_bytes", _I64, [_I64, _I64, _I32, _I32]),

@@ -15,7 +15,7 @@ import torch
 from . import _lib
 from ._lib import PER_IMAGE, PER_PAIR, SIDE_IMAGE, SIDE_TEMPLATE, RsvdError, check, ptr, require_cuda, stream_handle
 
-__all__ = ["block_bytes", "kernel_chunk", "kernel_partials_bytes", "align_workspace_bytes",
+__all__ = ["block_bytes", "path_for", "set_path", "PATH_AUTO", "PATH_SIMT", "PATH_TC", "kernel_chunk", "kernel_partials_bytes", "align_workspace_bytes",
            "align_min_workspace_bytes", "kernel_partials", "kernel_reduce", "eigen_basis", "build_basis",
            "compress", "blocks_unpack", "align_argmax", "align_landscape", "winners_reset",
            "winners_unpack", "combine_winners", "launch_count", "timing_enable", "timing_read", "Aligner", "RsvdError", "PER_PAIR", "PER_IMAGE",
@@ -23,8 +23,20 @@ __all__ = ["block_bytes", "kernel_chunk", "kernel_partials_bytes", "align_worksp
 
 
 # ------------------------------------------------------------------ sizes
-def block_bytes(rows: int, Q: int, H: int) -> int:
-    return int(_lib.lib().rsvd_block_bytes(rows, Q, H))
+def block_bytes(rows: int, Q: int, H: int, side: int = SIDE_IMAGE) -> int:
+    return int(_lib.lib().rsvd_block_bytes(rows, Q, H, side))
+
+
+PATH_AUTO, PATH_SIMT, PATH_TC = 0, 1, 2
+
+
+def path_for(Q: int, H: int) -> int:
+    """1 = FP32 SIMT contraction, 2 = tcgen05 3xTF32 contraction (include/rsvd.h)."""
+    return int(_lib.lib().rsvd_path_for(Q, H))
+
+
+def set_path(path: int):
+    _lib.lib().rsvd_set_path(int(path))
 
 
 def kernel_chunk() -> int:
@@ -92,7 +104,7 @@ def compress(rings: torch.Tensor, w: torch.Tensor, U: torch.Tensor, side: int, o
     require_cuda(rings, w, U)
     n, R, Q = rings.shape
     H = U.shape[1]
-    nb = block_bytes(n, Q, H)
+    nb = block_bytes(n, Q, H, side)
     if out is None:
         out = torch.empty(nb // 4, dtype=torch.float32, device=rings.device)
     elif out.numel() * out.element_size() < nb:

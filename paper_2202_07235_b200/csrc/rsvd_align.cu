@@ -149,17 +149,20 @@ static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const floa
 static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const int N = a.Q / 2;
     const int Kpad = (int)kpad_of(a.H);
-    const int64_t Mpad = rows_pad_of(a.M), Tpad = rows_pad_of(a.T);
-    // chunk: Mc x Tc pairs (multiples of 64) with Mc * Tc * N * 8 <= work_bytes
-    const int64_t tile_bytes = (int64_t)CT_TILE * CT_TILE * N * (int64_t)sizeof(float2);
+    const bool tc = resolve_path(a.Q, a.H) == PATH_TC;
+    const int64_t TILE = tc ? 128 : CT_TILE;
+    const int64_t Mpad = tc ? tc_rows_pad(a.M) : rows_pad_of(a.M);
+    const int64_t Tpad = tc ? tc_rows_pad(a.T) : rows_pad_of(a.T);
+    // chunk: Mc x Tc pairs (multiples of TILE) with Mc * Tc * N * 8 <= work_bytes
+    const int64_t tile_bytes = TILE * TILE * N * (int64_t)sizeof(float2);
     const int64_t ntiles = a.work_bytes / tile_bytes;
     if (ntiles < 1) return fail(RSVD_ERR_ARG, "workspace smaller than rsvd_align_min_workspace_bytes(Q)");
-    const int64_t tmax = Tpad / CT_TILE, mmax = Mpad / CT_TILE;
+    const int64_t tmax = Tpad / TILE, mmax = Mpad / TILE;
     int64_t tct = std::max<int64_t>(1, (int64_t)std::sqrt((double)ntiles));
     tct = std::min(tct, tmax);
     int64_t mct = std::min(mmax, std::max<int64_t>(1, ntiles / tct));
     tct = std::min(tmax, std::max(tct, ntiles / mct));      // widen t when rows run out
-    const int64_t Mc = mct * CT_TILE, Tc = tct * CT_TILE;
+    const int64_t Mc = mct * TILE, Tc = tct * TILE;
     float2 *Upk = reinterpret_cast<float2 *>(a.work);
     const FftOut o{a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t, a.T, a.t_offset};
     cudaError_t e;
@@ -169,12 +172,18 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
         const int64_t mc = std::min(Mc, Mpad - m0);
         const int64_t mcv = std::min(mc, a.M - m0);
         for (int64_t t0 = 0; t0 < Tpad; t0 += Tc) {
-            const int64_t tc = std::min(Tc, Tpad - t0);
-            const int64_t tcv = std::min(tc, a.T - t0);
-            dim3 g1((unsigned)(tc / CT_TILE), (unsigned)(mc / CT_TILE), (unsigned)((N + 1 + CT_QB - 1) / CT_QB));
+            const int64_t tc_ = std::min(Tc, Tpad - t0);
+            const int64_t tcv = std::min(tc_, a.T - t0);
             cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
-            contract_kernel<<<g1, CT_THREADS, 0, s>>>(a.alpha, a.beta, Mpad, Tpad, Kpad, N, m0, t0, Mc, Tc, Upk);
-            if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "contract launch");
+            if (tc) {
+                e = launch_contract_tc(reinterpret_cast<const float *>(a.alpha), reinterpret_cast<const float *>(a.beta),
+                                       a.H, N, Mpad, Tpad, m0, t0, mc, tc_, Mc, Tc, Upk, s);
+                if (e != cudaSuccess) return cuda_check(e, "contract (tcgen05) launch");
+            } else {
+                dim3 g1((unsigned)(tc_ / CT_TILE), (unsigned)(mc / CT_TILE), (unsigned)((N + 1 + CT_QB - 1) / CT_QB));
+                contract_kernel<<<g1, CT_THREADS, 0, s>>>(a.alpha, a.beta, Mpad, Tpad, Kpad, N, m0, t0, Mc, Tc, Upk);
+                if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "contract launch");
+            }
             cudaEvent_t ev1 = timed ? timing_event(s) : nullptr;
             e = launch_fft_any(LOGN, a.mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
             if (e != cudaSuccess) return cuda_check(e, "fft_reduce launch");
@@ -232,13 +241,13 @@ using namespace rsvd;
 
 extern "C" int64_t rsvd_align_min_workspace_bytes(int32_t Q) {
     if (Q < 2) return -1;
-    return (int64_t)CT_TILE * CT_TILE * (Q / 2) * (int64_t)sizeof(float2);
+    return (int64_t)128 * 128 * (Q / 2) * (int64_t)sizeof(float2);     // one 128 x 128 pair tile (either path)
 }
 
 extern "C" int64_t rsvd_align_workspace_bytes(int64_t M, int64_t T, int32_t Q, int32_t H) {
     (void)H;
     if (Q < 2 || M < 0 || T < 0) return -1;
-    const int64_t full = rows_pad_of(std::max<int64_t>(M, 1)) * rows_pad_of(std::max<int64_t>(T, 1)) * (Q / 2) * 8;
+    const int64_t full = tc_rows_pad(std::max<int64_t>(M, 1)) * tc_rows_pad(std::max<int64_t>(T, 1)) * (Q / 2) * 8;
     const int64_t target = 64ll << 20;     // L2-resident chunk
     return std::max(rsvd_align_min_workspace_bytes(Q), std::min(full, target));
 }

@@ -149,8 +149,9 @@ static cudaError_t launch_compress(const float2 *rings, int64_t n, int R, const 
 
 using namespace rsvd;
 
-extern "C" int64_t rsvd_block_bytes(int64_t rows, int32_t Q, int32_t H) {
+extern "C" int64_t rsvd_block_bytes(int64_t rows, int32_t Q, int32_t H, rsvd_side side) {
     if (rows < 0 || Q < 2 || H < 1) return -1;
+    if (resolve_path(Q, H) == PATH_TC) return tc_block_bytes(rows, Q, H, side);
     return (int64_t)(Q / 2 + 1) * kpad_of(H) * rows_pad_of(rows) * (int64_t)sizeof(float2);
 }
 
@@ -169,10 +170,25 @@ extern "C" rsvd_status rsvd_compress(const void *rings, int64_t n, int32_t R, in
     if (!rings || !w || !U || !blocks) return fail(RSVD_ERR_ARG, "NULL pointer");
     if (!aligned16(rings) || !aligned16(blocks)) return fail(RSVD_ERR_ARG, "complex buffers must be 16-byte aligned");
     cudaStream_t s = (cudaStream_t)stream;
+    if (resolve_path(Q, H) == PATH_TC) {
+        if (tc_rows_pad(n) > n) {
+            cudaError_t e = cudaMemsetAsync(blocks, 0, (size_t)tc_block_bytes(n, Q, H, side), s);
+            if (e != cudaSuccess) return cuda_check(e, "memset blocks");
+        }
+        const bool timed = timing_enabled();
+        cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
+        cudaError_t e = launch_compress_tc(reinterpret_cast<const float2 *>(rings), n, R, Q, w, U, H, side,
+                                           reinterpret_cast<float *>(blocks), s);
+        if (e == cudaSuccess) {
+            count_launches(1);
+            if (timed) timing_span(ev0, timing_event(s), TK_COMPRESS);
+        }
+        return cuda_check(e, "compress (tc layout) launch");
+    }
     const int Kpad = (int)kpad_of(H);
     const int64_t rows_pad = rows_pad_of(n);
     if (Kpad > 2 * H || rows_pad > n) {
-        cudaError_t e = cudaMemsetAsync(blocks, 0, (size_t)rsvd_block_bytes(n, Q, H), s);
+        cudaError_t e = cudaMemsetAsync(blocks, 0, (size_t)rsvd_block_bytes(n, Q, H, side), s);
         if (e != cudaSuccess) return cuda_check(e, "memset blocks");
     }
     const float2 *rg = reinterpret_cast<const float2 *>(rings);
@@ -196,6 +212,12 @@ extern "C" rsvd_status rsvd_blocks_unpack(const void *blocks, int64_t n, int32_t
     if (n < 0) return fail(RSVD_ERR_ARG, "n must be >= 0");
     if (n == 0) return RSVD_OK;
     if (!blocks || !coeffs) return fail(RSVD_ERR_ARG, "NULL pointer");
+    if (resolve_path(Q, H) == PATH_TC) {
+        cudaError_t e = launch_unpack_tc(reinterpret_cast<const float *>(blocks), n, Q, H, side,
+                                         reinterpret_cast<float2 *>(coeffs), (cudaStream_t)stream);
+        count_launches(1);
+        return cuda_check(e, "unpack (tc layout) launch");
+    }
     const int64_t total = n * (int64_t)Q * H;
     unpack_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         reinterpret_cast<const float2 *>(blocks), n, Q, H, side, rows_pad_of(n), (int)kpad_of(H),

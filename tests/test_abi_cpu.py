@@ -36,12 +36,24 @@ def test_header_symbols_exported_and_bound(lib):
 
 def test_sizes(lib):
     from paper_2202_07235_b200 import api
-    assert api.block_bytes(16384, 512, 24) == 257 * 48 * 16384 * 8
-    assert api.block_bytes(1, 32, 1) == 17 * 16 * 64 * 8
+    api.set_path(api.PATH_SIMT)
+    try:
+        assert api.path_for(512, 24) == api.PATH_SIMT
+        assert api.block_bytes(16384, 512, 24) == 257 * 48 * 16384 * 8
+        assert api.block_bytes(1, 32, 1) == 17 * 16 * 64 * 8
+        api.set_path(api.PATH_TC)
+        assert api.path_for(512, 24) == api.PATH_TC
+        # TC layout: (N+1) q x KB k-blocks x (hi, lo) x rows padded to 128 x 128 B; templates 2 rows each
+        assert api.block_bytes(16384, 512, 24, api.SIDE_IMAGE) == 257 * 3 * 2 * 16384 * 128
+        assert api.block_bytes(8192, 512, 24, api.SIDE_TEMPLATE) == 257 * 3 * 2 * 8192 * 128 * 2
+        assert api.path_for(1024, 256) == api.PATH_SIMT        # H x Q block too large for the TC compress
+    finally:
+        api.set_path(api.PATH_AUTO)
+    assert api.path_for(512, 24) == api.PATH_TC
     assert api.kernel_chunk() == 32
     assert api.kernel_partials_bytes(8192, 128) == 256 * 128 * 128 * 8
-    assert api.align_min_workspace_bytes(512) == 64 * 64 * 256 * 8
-    assert lib.rsvd_abi_version() == 1
+    assert api.align_min_workspace_bytes(512) == 128 * 128 * 256 * 8
+    assert lib.rsvd_abi_version() == 2
 
 
 def test_eigen_solver_matches_lapack(lib):

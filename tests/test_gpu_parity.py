@@ -14,6 +14,14 @@ pytestmark = pytest.mark.gpu
 api = pytest.importorskip("paper_2202_07235_b200.api")
 
 
+@pytest.fixture(autouse=True, params=["simt", "tc"])
+def contraction_path(request):
+    """Every parity test runs on both contraction paths (FP32 SIMT and tcgen05 3xTF32)."""
+    api.set_path(api.PATH_SIMT if request.param == "simt" else api.PATH_TC)
+    yield request.param
+    api.set_path(api.PATH_AUTO)
+
+
 def _gpu_path(images, templates, w, U, H, landscape=True, per_pair=True, per_image=True, work_bytes=None):
     """images/templates: complex64 numpy or torch; w: fp64 [R]; U: fp64 [R, H]."""
     A = cuda(images)
@@ -152,7 +160,7 @@ def test_edge_shapes_random_rings(M, T, R, Q, H):
 
 
 def test_small_workspace_many_chunks():
-    """Minimum workspace forces one 64x64 tile per chunk: results identical to one big chunk."""
+    """Minimum workspace forces many small chunks: results identical to one big chunk."""
     d = make_dataset("small", M=200, T=150)
     A, B, w = to_np(d.images), to_np(d.templates), to_np(d.w)
     U, _ = api.build_basis(cuda(B), w, 8)
@@ -211,7 +219,7 @@ def test_error_paths():
     lib = api._lib.lib()
     rings = torch.zeros((2, R, Q), dtype=torch.complex64, device="cuda")
     wd, Ud = cuda(w, torch.float64), cuda(np.eye(R)[:, :H], torch.float64)
-    blocks = torch.empty(api.block_bytes(2, Q, H) // 4, dtype=torch.float32, device="cuda")
+    blocks = torch.empty(api.block_bytes(2, Q, H, api.SIDE_TEMPLATE) // 4, dtype=torch.float32, device="cuda")
     p = rings.data_ptr()
     assert lib.rsvd_compress(p, 2, R, 48, wd.data_ptr(), Ud.data_ptr(), H, 0, blocks.data_ptr(), None) == 2
     assert lib.rsvd_compress(p, 2, R, 16, wd.data_ptr(), Ud.data_ptr(), H, 0, blocks.data_ptr(), None) == 2
