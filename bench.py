@@ -282,31 +282,49 @@ def run_ours(args):
     pairs = M * T
     value = pairs / (ms_step / 1e3)
 
-    # dominant kernel roofline: the contraction (FP32 SIMT, ALU bound)
+    # dominant-kernel roofline (the kernel with the larger measured share of the step)
     pk, pk_kind = peaks()
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_peak = sm_count * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12      # TFLOP/s
+    tf32_peak = pk.get("bf16_tflops", 1656.1) * (1.1 / 2.25)                       # dtype ratio, nominal
     f_contr, f_fft = flops_per_pair(H, Q)
     c_ms, c_n = ktime["contract"]
     f_ms, f_n = ktime["fft_reduce"]
-    contr_flops = args.steps * M * T_loc * f_contr
-    achieved = contr_flops / (c_ms / 1e3) / 1e12 if c_ms > 0 else None
-    traffic = None
+    n_pairs_timed = args.steps * M * T_loc
+    traffic_all = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get(args.config, {}).get("contract_kernel_bytes_per_launch")
+                traffic_all = json.load(f).get(args.config, {})
         except Exception:
-            traffic = None
-    roof = {"bound": "alu", "kernel": "contract_kernel (Step 2 contraction, FP32 SIMT)",
-            "achieved": round(achieved, 3) if achieved else None, "peak": round(fp32_peak, 2),
-            "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4) if achieved else None,
-            "traffic": traffic,
-            "peak_note": f"{sm_count} SMs x 128 FP32 lanes x 2 flop x {pk.get('sm_max_mhz', 1965.0):.0f} MHz "
-                         f"(sm_max_mhz from MEASURED_PEAKS.json, {pk_kind})",
-            "avg_launch_ms": round(c_ms / max(c_n, 1), 4), "launches": c_n,
-            "algorithmic_flops_per_pair": f_contr}
+            traffic_all = {}
+    if c_ms >= f_ms:
+        achieved = n_pairs_timed * f_contr / (c_ms / 1e3) / 1e12 if c_ms > 0 else None
+        if path == api.PATH_TC:
+            peak, bound = tf32_peak / 3.0, "tensor"
+            kname = "contract_tc_kernel (Step 2, tcgen05 kind::tf32, 3xTF32)"
+            note = (f"TF32 dense = measured bf16 {pk.get('bf16_tflops', 1656.1):.1f} TF/s ({pk_kind}) x nominal "
+                    f"1.1/2.25; 3xTF32 executes 3 MMAs per algorithmic MAC -> peak/3 for algorithmic flops")
+        else:
+            peak, bound = fp32_peak, "alu"
+            kname = "contract_kernel (Step 2, FP32 SIMT)"
+            note = (f"{sm_count} SMs x 128 FP32 lanes x 2 flop x {pk.get('sm_max_mhz', 1965.0):.0f} MHz "
+                    f"(sm_max_mhz from MEASURED_PEAKS.json, {pk_kind})")
+        k_ms, k_n, fpp, tkey = c_ms, c_n, f_contr, "contract_bytes_per_launch"
+    else:
+        achieved = n_pairs_timed * f_fft / (f_ms / 1e3) / 1e12 if f_ms > 0 else None
+        peak, bound = fp32_peak, "alu"
+        kname = "fft_reduce_kernel (Steps 3-4, FP32 SIMT)"
+        note = (f"{sm_count} SMs x 128 FP32 lanes x 2 flop x {pk.get('sm_max_mhz', 1965.0):.0f} MHz "
+                f"(sm_max_mhz from MEASURED_PEAKS.json, {pk_kind}); algorithmic 5 Q log2 Q per pair")
+        k_ms, k_n, fpp, tkey = f_ms, f_n, f_fft, "fft_bytes_per_launch"
+    roof = {"bound": bound, "kernel": kname,
+            "achieved": round(achieved, 3) if achieved else None, "peak": round(peak, 2),
+            "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if achieved else None,
+            "traffic": traffic_all.get(tkey), "peak_note": note,
+            "avg_launch_ms": round(k_ms / max(k_n, 1), 4), "launches": k_n,
+            "algorithmic_flops_per_pair": fpp, "contraction_path": "tc" if path == api.PATH_TC else "simt"}
     t_roof = pairs * (f_contr + f_fft) / (fp32_peak * 1e12) / world
     step_roof = {"t_roof_ms": round(t_roof * 1e3, 3), "frac": round(t_roof * 1e3 / ms_step, 4),
                  "definition": "M*T*(8HQ + 5Q log2 Q) / (G * FP32 peak) vs measured step (SURVEY.md 8(d))",

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(CT_THREADS, 3) contract_kernel(const float2 *_
                                                                  const float2 *__restrict__ beta,
                                                                  int64_t Mpad, int64_t Tpad, int Kpad, int N,
                                                                  int64_t m0, int64_t t0, int64_t Mc, int64_t Tc,
-                                                                 float2 *__restrict__ Upk) {
+                                                                 float *__restrict__ Upk) {
     __shared__ __align__(16) float2 As[2][CT_KC][CT_TILE];
     __shared__ __align__(16) float2 Bs[2][CT_KC][CT_TILE];
 
@@ -84,13 +84,14 @@ __global__ void __launch_bounds__(CT_THREADS, 3) contract_kernel(const float2 *_
         }
 #pragma unroll
         for (int kk = 0; kk < CT_KC; ++kk) {
-            const float4 a01 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4]);
-            const float4 a23 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4 + 2]);
-            const float2 a[4] = {make_float2(a01.x, a01.y), make_float2(a01.z, a01.w),
-                                 make_float2(a23.x, a23.y), make_float2(a23.z, a23.w)};
-            float2 b[4];
+            // thread (ty, tx) owns images m = tx + 16 i and templates t = ty * 4 + j
+            const float4 b01 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][ty * 4]);
+            const float4 b23 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][ty * 4 + 2]);
+            const float2 b[4] = {make_float2(b01.x, b01.y), make_float2(b01.z, b01.w),
+                                 make_float2(b23.x, b23.y), make_float2(b23.z, b23.w)};
+            float2 a[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk][tx + 16 * j];
+            for (int i = 0; i < 4; ++i) a[i] = As[buf][kk][tx + 16 * i];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -101,18 +102,19 @@ __global__ void __launch_bounds__(CT_THREADS, 3) contract_kernel(const float2 *_
                     acc[i][j].y = fmaf(a[i].y, b[j].x, acc[i][j].y);
                 }
         }
-        if (kc == nk - 1) {          // q finished: coalesced q-major store (16 lanes = 128 B per row)
+        if (kc == nk - 1) {          // q finished: planar [n][t][m] stores, 16 lanes = 64 contiguous bytes
             const int q = q0 + it / nk;
             const int n = (q == N) ? 0 : q;
-            float2 *dst = Upk + ((int64_t)n * Mc + bm) * Tc + bt;
+            float *const re = Upk, *const im = Upk + (int64_t)N * Mc * Tc;
+            const int64_t o = ((int64_t)n * Tc + bt) * Mc + bm;
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    float2 *p = dst + (int64_t)(ty * 4 + i) * Tc + tx + 16 * j;
-                    if (q == 0) reinterpret_cast<float *>(p)[0] = acc[i][j].x;        // U_0 (real)
-                    else if (q == N) reinterpret_cast<float *>(p)[1] = acc[i][j].x;   // U_N (real)
-                    else *p = acc[i][j];
+                    const int64_t p = o + (int64_t)(ty * 4 + j) * Mc + tx + 16 * i;
+                    if (q == 0) re[p] = acc[i][j].x;                 // U_0 (real) -> re plane slot 0
+                    else if (q == N) im[p] = acc[i][j].x;            // U_N (real) -> im plane slot 0
+                    else { re[p] = acc[i][j].x; im[p] = acc[i][j].y; }
                 }
         }
         __syncthreads();
@@ -134,7 +136,7 @@ struct AlignArgs {
     int64_t ld_m, ld_t;
 };
 
-static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const float2 *Upk, int64_t Mc, int64_t Tc,
+static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const float *Upk, int64_t Mc, int64_t Tc,
                                   int64_t m0, int64_t t0, int64_t mcv, int64_t tcv, const FftOut &o) {
     switch (LOGN) {
         case 4: return launch_fft<4>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
@@ -150,30 +152,31 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const int N = a.Q / 2;
     const int Kpad = (int)kpad_of(a.H);
     const bool tc = resolve_path(a.Q, a.H) == PATH_TC;
-    const int64_t TILE = tc ? 128 : CT_TILE;
-    const int64_t Mpad = tc ? tc_rows_pad(a.M) : rows_pad_of(a.M);
-    const int64_t Tpad = tc ? tc_rows_pad(a.T) : rows_pad_of(a.T);
-    // chunk: Mc x Tc pairs (multiples of TILE) with Mc * Tc * N * 8 <= work_bytes
-    const int64_t tile_bytes = TILE * TILE * N * (int64_t)sizeof(float2);
+    // pair tiles: SIMT 64 x 64; TC 64 images x 256 templates (one tcgen05 CTA tile)
+    const int64_t TM = 64, TT = tc ? 256 : CT_TILE;
+    const int64_t Mpad = tc ? tc_rows_pad_side(a.M, RSVD_SIDE_IMAGE) : rows_pad_of(a.M);
+    const int64_t Tpad = tc ? tc_rows_pad_side(a.T, RSVD_SIDE_TEMPLATE) : rows_pad_of(a.T);
+    // chunk: Mc x Tc pairs (multiples of the tile) with Mc * Tc * N * 8 <= work_bytes.  Chunks are
+    // visited t-outer / m-inner, so a chunk's template blocks stay in L2 while image blocks stream.
+    const int64_t tile_bytes = TM * TT * N * (int64_t)sizeof(float2);
     const int64_t ntiles = a.work_bytes / tile_bytes;
     if (ntiles < 1) return fail(RSVD_ERR_ARG, "workspace smaller than rsvd_align_min_workspace_bytes(Q)");
-    const int64_t tmax = Tpad / TILE, mmax = Mpad / TILE;
-    int64_t tct = std::max<int64_t>(1, (int64_t)std::sqrt((double)ntiles));
-    tct = std::min(tct, tmax);
+    const int64_t tmax = Tpad / TT, mmax = Mpad / TM;
+    int64_t tct = std::min<int64_t>(tmax, tc ? 1 : std::max<int64_t>(1, (int64_t)std::sqrt((double)ntiles)));
     int64_t mct = std::min(mmax, std::max<int64_t>(1, ntiles / tct));
     tct = std::min(tmax, std::max(tct, ntiles / mct));      // widen t when rows run out
-    const int64_t Mc = mct * TILE, Tc = tct * TILE;
-    float2 *Upk = reinterpret_cast<float2 *>(a.work);
+    const int64_t Mc = mct * TM, Tc = tct * TT;
+    float *Upk = reinterpret_cast<float *>(a.work);
     const FftOut o{a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t, a.T, a.t_offset};
     cudaError_t e;
     const int LOGN = ilog2(N);
     const bool timed = timing_enabled();
-    for (int64_t m0 = 0; m0 < Mpad; m0 += Mc) {
-        const int64_t mc = std::min(Mc, Mpad - m0);
-        const int64_t mcv = std::min(mc, a.M - m0);
-        for (int64_t t0 = 0; t0 < Tpad; t0 += Tc) {
-            const int64_t tc_ = std::min(Tc, Tpad - t0);
-            const int64_t tcv = std::min(tc_, a.T - t0);
+    for (int64_t t0 = 0; t0 < Tpad; t0 += Tc) {
+        const int64_t tc_ = std::min(Tc, Tpad - t0);
+        const int64_t tcv = std::min(tc_, a.T - t0);
+        for (int64_t m0 = 0; m0 < Mpad; m0 += Mc) {
+            const int64_t mc = std::min(Mc, Mpad - m0);
+            const int64_t mcv = std::min(mc, a.M - m0);
             cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
             if (tc) {
                 e = launch_contract_tc(reinterpret_cast<const float *>(a.alpha), reinterpret_cast<const float *>(a.beta),

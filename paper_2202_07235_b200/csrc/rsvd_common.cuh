@@ -40,12 +40,13 @@ int resolve_path(int Q, int H);
 bool tc_supported(int Q, int H);
 int tc_kb(int H);
 int64_t tc_rows_pad(int64_t rows);
+int64_t tc_rows_pad_side(int64_t rows, int side);
 int64_t tc_block_bytes(int64_t rows, int Q, int H, int side);
 cudaError_t launch_compress_tc(const float2 *rings, int64_t n, int R, int Q, const double *w, const double *U, int H,
                                int side, float *blocks, cudaStream_t s);
 cudaError_t launch_unpack_tc(const float *blocks, int64_t n, int Q, int H, int side, float2 *coeffs, cudaStream_t s);
 cudaError_t launch_contract_tc(const float *Atc, const float *Btc, int H, int N, int64_t Mpad, int64_t Tpad,
-                               int64_t m0, int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float2 *Upk,
+                               int64_t m0, int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk,
                                cudaStream_t s);
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }

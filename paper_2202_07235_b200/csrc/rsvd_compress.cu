@@ -171,7 +171,7 @@ extern "C" rsvd_status rsvd_compress(const void *rings, int64_t n, int32_t R, in
     if (!aligned16(rings) || !aligned16(blocks)) return fail(RSVD_ERR_ARG, "complex buffers must be 16-byte aligned");
     cudaStream_t s = (cudaStream_t)stream;
     if (resolve_path(Q, H) == PATH_TC) {
-        if (tc_rows_pad(n) > n) {
+        if (tc_rows_pad_side(n, side) > n) {
             cudaError_t e = cudaMemsetAsync(blocks, 0, (size_t)tc_block_bytes(n, Q, H, side), s);
             if (e != cudaSuccess) return cuda_check(e, "memset blocks");
         }

@@ -2,13 +2,14 @@
 // spectrum (forward sign per DESIGN.md G3) fused with the argmax over gamma
 // or the landscape store.
 //
-// Input: the contraction's workspace Upk[(n * Mc + ml) * Tc + tl] (q-major), n < N = Q/2, holding
+// Input: the contraction's planar workspace (re plane, then im plane, each [(n * Mc + ml) * Tc + tl]
+// floats, q-major), n < N = Q/2, holding
 // U_n = S_n + conj(S_{Q-n}) for n in [1, N) and (U_0, U_N) packed in slot 0.  With Y = U/2 (the
 // Hermitian part of S, whose transform is Re X), the real length-Q transform is computed as one
 // complex length-N FFT of Z_n = (Y_n + conj Y_{N-n}) + i W_Q^n (Y_n - conj Y_{N-n}); its output
 // z_n = x_{2n} + i x_{2n+1} with Re X_k = 2 pi x_k.
 //
-// Schedule: persistent CTAs loop over work items (one image row x TB templates); the TB spectra of
+// Schedule: persistent CTAs loop over work items (one template x TB images); the TB spectra of
 // the next item are prefetched into shared memory with cp.async while the current item is
 // transformed (double buffer).  Per pair (one warp): Z formation from the staged spectra,
 // in-register DIF of length E = N/32 over x[l + 32 e], twiddle W_N^{l k1}, one warp transpose through
@@ -29,9 +30,9 @@ __device__ __forceinline__ uint32_t ord_f32(float v) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit_fr() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int NWAIT>
@@ -62,7 +63,7 @@ struct FftOut {
 };
 
 template <int LOGN, int MODE>
-__global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float2 *__restrict__ Upk, int64_t Mc,
+__global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float *__restrict__ Upk, int64_t Mc,
                                                                 int64_t Tc, int64_t m0, int64_t t0, int64_t mcv,
                                                                 int64_t tcv, FftOut out) {
     constexpr int N = 1 << LOGN;
@@ -78,16 +79,20 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float2 *__
     unsigned long long *skey = reinterpret_cast<unsigned long long *>(pre + N);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t ntb = (tcv + TB - 1) / TB;
-    const int64_t nitems = mcv * ntb;
+    // work item = (template tl, block of TB consecutive images); workspace [plane][n][t][m]
+    const int64_t nmb = (mcv + TB - 1) / TB;
+    const int64_t nitems = tcv * nmb;
 
+    const int64_t plane = (int64_t)N * Mc * Tc;
     auto stage = [&](int64_t item, int buf) {
-        const int64_t ml = item / ntb, tb0 = (item % ntb) * TB;
-        float2 *S = Sbuf + buf * C::SBUF;
-        const float2 *src = Upk + ml * Tc + tb0;
+        const int64_t tl = item / nmb, mb0 = (item % nmb) * TB;
+        float *S = reinterpret_cast<float *>(Sbuf + buf * C::SBUF);
+        const float *src = Upk + tl * Mc + mb0;
         for (int i = tid; i < N * TB; i += FR_THREADS) {
             const int n = i / TB, c = i % TB;
-            cp_async8(S + n * SROW + c, src + (int64_t)n * Mc * Tc + c);
+            const float *g = src + (int64_t)n * Mc * Tc + c;
+            cp_async4(S + 2 * (n * SROW + c), g);
+            cp_async4(S + 2 * (n * SROW + c) + 1, g + plane);
         }
         cp_async_commit_fr();
     };
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float2 *__
         sincospif(2.0f * (float)i / (float)Q, &sn, &cs);
         pre[i] = make_float2(cs, -sn);
     }
-    if (tid == 0) *skey = 0ull;
+    (void)skey;
 
     const float PI = 3.14159265358979323846f;
     // per-lane constants
@@ -124,17 +129,15 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float2 *__
         }
         __syncthreads();
         const float2 *S = Sbuf + buf * C::SBUF;
-        const int64_t ml = item / ntb, tb0 = (item % ntb) * TB;
-        const int64_t m = m0 + ml;
-        unsigned long long mykey = 0ull;
-        bool leader = lane == 0;
+        const int64_t tl = item / nmb, mb0 = (item % nmb) * TB;
+        const int64_t t = t0 + tl;
 
         if constexpr (E == 1) {
-            leader = l1 == 0;
             const float2 one = make_float2(1.f, 0.f);
             for (int tt = warp * GP + g1; tt < TB; tt += FR_WARPS * GP) {
-                const int64_t tl = tb0 + tt;
-                const bool valid = tl < tcv;
+                const int64_t ml = mb0 + tt;
+                const bool valid = ml < mcv;
+                const int64_t m = m0 + ml;
                 float2 z[1];
                 const float2 u = S[l1 * SROW + tt];
                 if (l1 == 0) {
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float2 *__
                 const float vx = PI * z[0].x, vy = PI * z[0].y;
                 if constexpr (MODE == MODE_LANDSCAPE) {
                     if (valid)
-                        reinterpret_cast<float2 *>(out.X + m * out.ld_m + (t0 + tl) * out.ld_t)[b] = make_float2(vx, vy);
+                        reinterpret_cast<float2 *>(out.X + m * out.ld_m + t * out.ld_t)[b] = make_float2(vx, vy);
                 } else {
                     float bv = vx;
                     int bk = 2 * b;
@@ -164,22 +167,23 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float2 *__
                     }
                     if constexpr (MODE == MODE_PAIR) {
                         if (valid && l1 == 0) {
-                            out.best_val[m * out.T + t0 + tl] = bv;
-                            out.best_k[m * out.T + t0 + tl] = bk;
+                            out.best_val[m * out.T + t] = bv;
+                            out.best_k[m * out.T + t] = bk;
                         }
                     } else if (valid) {
-                        const uint32_t idx = (uint32_t)((out.t_offset + t0 + tl) * Q + bk);
+                        const uint32_t idx = (uint32_t)((out.t_offset + t) * Q + bk);
                         const unsigned long long key =
                             ((unsigned long long)ord_f32(bv) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
-                        mykey = key > mykey ? key : mykey;
+                        if (l1 == 0) atomicMax(out.best_key + m, key);
                     }
                 }
             }
         } else {
             const int l = lane;
             for (int tt = warp; tt < TB; tt += FR_WARPS) {
-                const int64_t tl = tb0 + tt;
-                const bool valid = tl < tcv;
+                const int64_t ml = mb0 + tt;
+                const bool valid = ml < mcv;
+                const int64_t m = m0 + ml;
                 float2 z[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float2 *__
                 const int b = (int)(__brev((unsigned)s2) >> (32 - clog2(G)));
                 if constexpr (MODE == MODE_LANDSCAPE) {
                     if (valid) {
-                        float2 *dst = reinterpret_cast<float2 *>(out.X + m * out.ld_m + (t0 + tl) * out.ld_t);
+                        float2 *dst = reinterpret_cast<float2 *>(out.X + m * out.ld_m + t * out.ld_t);
 #pragma unroll
                         for (int k2a = 0; k2a < E; ++k2a) {
                             const float2 v = z[brev(k2a, clog2(E))];
@@ -234,24 +238,16 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float2 *__
                     bv *= PI;
                     if constexpr (MODE == MODE_PAIR) {
                         if (valid && l == 0) {
-                            out.best_val[m * out.T + t0 + tl] = bv;
-                            out.best_k[m * out.T + t0 + tl] = bk;
+                            out.best_val[m * out.T + t] = bv;
+                            out.best_k[m * out.T + t] = bk;
                         }
                     } else if (valid) {
-                        const uint32_t idx = (uint32_t)((out.t_offset + t0 + tl) * Q + bk);
+                        const uint32_t idx = (uint32_t)((out.t_offset + t) * Q + bk);
                         const unsigned long long key =
                             ((unsigned long long)ord_f32(bv) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
-                        mykey = key > mykey ? key : mykey;
+                        if (l == 0) atomicMax(out.best_key + m, key);
                     }
                 }
-            }
-        }
-        if constexpr (MODE == MODE_IMAGE) {
-            if (leader && mykey) atomicMax(skey, mykey);
-            __syncthreads();
-            if (tid == 0) {
-                if (*skey) atomicMax(out.best_key + m, *skey);
-                *skey = 0ull;
             }
         }
         __syncthreads();       // stage buffer `buf` is refilled by the next iteration's prefetch
@@ -270,7 +266,7 @@ inline int num_sms() {
 }
 
 template <int LOGN, int MODE>
-static cudaError_t launch_fft_mode(cudaStream_t s, const float2 *Upk, int64_t Mc, int64_t Tc, int64_t m0, int64_t t0,
+static cudaError_t launch_fft_mode(cudaStream_t s, const float *Upk, int64_t Mc, int64_t Tc, int64_t m0, int64_t t0,
                                    int64_t mcv, int64_t tcv, const FftOut &out) {
     using C = FftCfg<(1 << LOGN)>;
     const size_t smem = C::smem_bytes();
@@ -282,14 +278,14 @@ static cudaError_t launch_fft_mode(cudaStream_t s, const float2 *Upk, int64_t Mc
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fft_reduce_kernel<LOGN, MODE>, FR_THREADS, smem);
         if (e != cudaSuccess || occ < 1) occ = 1;
     }
-    const int64_t nitems = mcv * ((tcv + C::TB - 1) / C::TB);
+    const int64_t nitems = tcv * ((mcv + C::TB - 1) / C::TB);
     const int64_t grid = std::min<int64_t>(nitems, (int64_t)num_sms() * occ);
     fft_reduce_kernel<LOGN, MODE><<<(unsigned)grid, FR_THREADS, smem, s>>>(Upk, Mc, Tc, m0, t0, mcv, tcv, out);
     return cudaGetLastError();
 }
 
 template <int LOGN>
-static cudaError_t launch_fft(int mode, cudaStream_t s, const float2 *Upk, int64_t Mc, int64_t Tc, int64_t m0,
+static cudaError_t launch_fft(int mode, cudaStream_t s, const float *Upk, int64_t Mc, int64_t Tc, int64_t m0,
                               int64_t t0, int64_t mcv, int64_t tcv, const FftOut &out) {
     if (mode == MODE_PAIR) return launch_fft_mode<LOGN, MODE_PAIR>(s, Upk, Mc, Tc, m0, t0, mcv, tcv, out);
     if (mode == MODE_IMAGE) return launch_fft_mode<LOGN, MODE_IMAGE>(s, Upk, Mc, Tc, m0, t0, mcv, tcv, out);

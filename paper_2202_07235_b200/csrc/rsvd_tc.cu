@@ -1,26 +1,31 @@
-// rsvd_tc.cu -- tensor-core path of Step 1 storage and Step 2 (the q-batched complex contraction,
-// PAPER.md:672) on sm_100a: tcgen05.mma kind::tf32 with 3xTF32 error compensation.
+// rsvd_tc.cu -- tensor-core path of Step 2 (the q-batched complex contraction) on
+// sm_100a: tcgen05.mma kind::tf32 with 3xTF32 error compensation, plus the compact block layout it
+// consumes (written by compress) and the path selection.
 //
-// Real embedding of the complex contraction U_q[m,t] = sum_j alpha[q][j][m] beta[q][j][t]
-// (alpha/beta as in rsvd_compress.cu):  A'[m][2j + c] = (Re, Im) alpha_j, and two B rows per template,
-//   B'[2t][.]   = (Re beta_j, -Im beta_j)   ->  D[m][2t]   = Re U
-//   B'[2t+1][.] = (Im beta_j,  Re beta_j)   ->  D[m][2t+1] = Im U
-// Each fp32 operand x is split x = hi + lo with hi, lo TF32-rounded; D = Ahi Bhi + Ahi Blo + Alo Bhi
-// recovers ~fp32 accuracy (the dropped Alo Blo term is ~2^-22 relative).
+// Real embedding of U_q[m,t] = sum_j alpha[q][j][m] beta[q][j][t] (alpha/beta: rsvd_compress.cu):
+// two A rows per image and one B row per template,
+//   A_re[m] = (Re a_j, -Im a_j)_j ,  A_im[m] = (Im a_j, Re a_j)_j ,  B[t] = (Re b_j, Im b_j)_j
+//   D[m][t] = A_re . B = Re U ,  D[64 + m][t] = A_im . B = Im U.
+// Each fp32 operand x = hi + lo (both TF32-rounded); D = Ahi Bhi + Ahi Blo + Alo Bhi recovers ~fp32
+// accuracy (the dropped Alo Blo term is ~2^-22 relative).
 //
-// Block layout (TC): 128-row x 32-float K-major sub-tiles stored pre-swizzled exactly as the
-// UMMA SWIZZLE_128B canonical layout expects (16-byte chunk c of row r at chunk c ^ (r & 7)):
-//   images    A[q][mtile][kb][hi|lo][128 rows][32]   (mtile = 128 images)
-//   templates B[q][ttile][kb][hi|lo][256 rows][32]   (ttile = 128 templates = 256 B-rows)
-// q = 0..N (N = Q/2), kb < KB = ceil(4H/32).  One stage of the contraction is then two contiguous
-// bulk copies (cp.async.bulk, mbarrier complete_tx): 32 KB of A and 64 KB of B.
+// Block layout (compact TC layout; same bytes as the SIMT layout): K-major rows of interleaved
+// complex fp32, 16 complex (128 B) per k-block row, pre-swizzled the way UMMA SWIZZLE_128B expects
+// (16-byte chunk c of row r stored at chunk c ^ (r & 7)):
+//   images    A[q][mtile][kb][64 rows][32 floats]    (mtile = 64 images, 8 KB per sub-tile)
+//   templates B[q][ttile][kb][256 rows][32 floats]   (ttile = 256 templates, 32 KB per sub-tile)
+// q = 0..N (N = Q/2), kb < KB = ceil(2H/16).  The in-shared-memory expansion to (Re, Im) rows and
+// hi/lo parts preserves the position of every 16-byte chunk (64 + r = r mod 8), so producers copy
+// chunk i of global to chunk i of shared memory with arithmetic only.
 //
-// contract_tc_kernel: one CTA per (128 x 128 pair tile, group of q), 6 warps:
-//   warp 0  producer: bulk-copies (q, kb) stages into a 2-deep smem ring;
-//   warp 1  TMEM allocator + MMA issuer: per stage 4 k-steps x 3 tcgen05.mma (M=128, N=256, K=8) into
-//           one of two 256-column TMEM accumulators; tcgen05.commit releases smem / signals epilogue;
-//   warps 2-5 epilogue: tcgen05.ld 32x32b of their 32 lanes, store U_q rows q-major to the spectrum
-//           workspace (same layout as the SIMT contraction), release the accumulator.
+// contract_tc_kernel: one CTA per (64-image x 256-template tile, group of q), 13 warps:
+//   warp 0      TMEM allocator + MMA issuer: per stage 4 k-steps x 3 tcgen05.mma (M=128, N=256, K=8)
+//               into one of two 256-column TMEM accumulators; tcgen05.commit frees the smem stage /
+//               signals the epilogue;
+//   warps 1-4   epilogue: tcgen05.ld 32x32b of their 32 TMEM lanes; lanes 0-63 hold Re U, 64-127 Im U;
+//               stores to the planar spectrum workspace (re plane | im plane), releases the accumulator;
+//   warps 5-12  producers: LDG the compact (q, kb) sub-tiles (40 KB), expand to A hi/lo (2 x 16 KB) and
+//               B hi/lo (2 x 32 KB) in a 2-deep shared-memory ring, fence.proxy.async, arrive.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -31,17 +36,21 @@
 
 namespace rsvd {
 
-constexpr int TC_THREADS = 192;
+constexpr int TC_THREADS = 13 * 32;
+constexpr int TC_PROD_WARPS = 8;
 constexpr int TC_STAGES = 2;
-constexpr uint32_t TC_A_BYTES = 2u * 128u * 128u;    // hi + lo, 128 rows x 128 B
-constexpr uint32_t TC_B_BYTES = 2u * 256u * 128u;    // hi + lo, 256 rows x 128 B
-constexpr uint32_t TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
+constexpr int TC_MT = 64;                           // images per tile
+constexpr int TC_TT = 256;                          // templates per tile
+constexpr uint32_t TC_A_BYTES = 128u * 128u;        // one of hi / lo: 128 rows x 128 B
+constexpr uint32_t TC_B_BYTES = 256u * 128u;
+constexpr uint32_t TC_STAGE_BYTES = 2 * TC_A_BYTES + 2 * TC_B_BYTES;    // 96 KB
 constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_BYTES + 1024 + 256;
 
-int tc_kb(int H) { return (int)((4 * (int64_t)H + 31) / 32); }
-int64_t tc_rows_pad(int64_t rows) { return round_up(rows, 128); }
+int tc_kb(int H) { return (int)((2 * (int64_t)H + 15) / 16); }
+int64_t tc_rows_pad_side(int64_t rows, int side) { return round_up(rows, side == RSVD_SIDE_TEMPLATE ? TC_TT : TC_MT); }
+int64_t tc_rows_pad(int64_t rows) { return round_up(rows, 256); }
 int64_t tc_block_bytes(int64_t rows, int Q, int H, int side) {
-    return (int64_t)(Q / 2 + 1) * tc_kb(H) * 2 * tc_rows_pad(rows) * 128 * (side == RSVD_SIDE_TEMPLATE ? 2 : 1);
+    return (int64_t)(Q / 2 + 1) * tc_kb(H) * tc_rows_pad_side(rows, side) * 128;
 }
 
 // ------------------------------------------------------------------ PTX helpers
@@ -75,17 +84,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b)) : "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
-    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(b)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_mma_tf32(uint32_t dtmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -112,11 +110,24 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ float tf32_rn(float x) {
+    uint32_t u = __float_as_uint(x);
+    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x0FFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;
+    return __uint_as_float(u);
+}
+__device__ __forceinline__ void split4(float4 v, float4 &hi, float4 &lo) {
+    hi.x = tf32_rn(v.x); lo.x = tf32_rn(v.x - hi.x);
+    hi.y = tf32_rn(v.y); lo.y = tf32_rn(v.y - hi.y);
+    hi.z = tf32_rn(v.z); lo.z = tf32_rn(v.z - hi.z);
+    hi.w = tf32_rn(v.w); lo.w = tf32_rn(v.w - hi.w);
+}
+
 // ------------------------------------------------------------------ contraction kernel
-// grid: ntiles_chunk * nqg.  Chunk tiles are (Mc/128) x (Tc/128); item -> (tile, q-group).
+// grid: ntiles_chunk * nqg; chunk tiles (Mc/64) x (Tc/256); item -> (tile, q-group).
+// Upk planar: re plane [(n*Mc + ml)*Tc + tl], im plane at + N*Mc*Tc (floats).
 __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
-    const float *__restrict__ Atc, const float *__restrict__ Btc, int KB, int N, int64_t MT, int64_t NT, int64_t mt0,
-    int64_t nt0, int ntl, int qg, int nqg, int64_t Mc, int64_t Tc, float2 *__restrict__ Upk) {
+    const float *__restrict__ Acmp, const float *__restrict__ Bcmp, int KB, int N, int64_t MT, int64_t NT,
+    int64_t mt0, int64_t nt0, int ntl, int qg, int nqg, int64_t Mc, int64_t Tc, float *__restrict__ Upk) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint64_t *bars = reinterpret_cast<uint64_t *>(base + TC_STAGES * TC_STAGE_BYTES);
@@ -132,9 +143,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
     const int q_end = min(N + 1, q_begin + qg);
     const int nqi = max(0, q_end - q_begin);
 
-    if (warp == 1) {
+    if (warp == 0) {
         if (lane == 0) {
-            for (int s = 0; s < TC_STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
+            for (int s = 0; s < TC_STAGES; ++s) { mbar_init(full + s, TC_PROD_WARPS); mbar_init(empty + s, 1); }
             for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 4); }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
@@ -149,24 +160,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {
-            int it = 0;
-            for (int qi = 0; qi < nqi; ++qi) {
-                const int q = q_begin + qi;
-                for (int kb = 0; kb < KB; ++kb, ++it) {
-                    const int s = it % TC_STAGES;
-                    const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
-                    mbar_wait(empty + s, ph ^ 1u);
-                    unsigned char *sa = base + s * TC_STAGE_BYTES;
-                    mbar_expect_tx(full + s, TC_STAGE_BYTES);
-                    const float *ga = Atc + (((int64_t)q * MT + mt) * KB + kb) * (int64_t)(2 * 128 * 32);
-                    const float *gb = Btc + (((int64_t)q * NT + nt) * KB + kb) * (int64_t)(2 * 256 * 32);
-                    bulk_g2s(sa, ga, TC_A_BYTES, full + s);
-                    bulk_g2s(sa + TC_A_BYTES, gb, TC_B_BYTES, full + s);
-                }
-            }
-        }
-    } else if (warp == 1) {
+        // ---------------- MMA issuer
         if (lane == 0) {
             const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
                                    ((uint32_t)(128 >> 4) << 24);
@@ -181,8 +175,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
                     mbar_wait(full + s, (uint32_t)(it / TC_STAGES) & 1u);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(base + s * TC_STAGE_BYTES);
-                    const uint64_t a_hi = sw128_desc(sa), a_lo = sw128_desc(sa + 128 * 128);
-                    const uint64_t b_hi = sw128_desc(sa + TC_A_BYTES), b_lo = sw128_desc(sa + TC_A_BYTES + 256 * 128);
+                    const uint64_t a_hi = sw128_desc(sa), a_lo = sw128_desc(sa + TC_A_BYTES);
+                    const uint64_t b_hi = sw128_desc(sa + 2 * TC_A_BYTES), b_lo = sw128_desc(sa + 2 * TC_A_BYTES + TC_B_BYTES);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const uint64_t o = (uint64_t)(2 * k);          // +32 B per K=8 tf32 step
@@ -190,79 +184,126 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
                         tc_mma_tf32(dt, a_hi + o, b_lo + o, idesc, 1u);
                         tc_mma_tf32(dt, a_lo + o, b_hi + o, idesc, 1u);
                     }
-                    tc_commit(empty + s);          // smem stage free once these MMAs complete
+                    tc_commit(empty + s);          // stage free once these MMAs complete
                 }
                 tc_commit(tfull + acc);            // accumulator ready for the epilogue
             }
         }
-    } else {
+    } else if (warp <= 4) {
+        // ---------------- epilogue
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
         const int row = quad * 32 + lane;
+        const bool re_rows = row < 64;
+        const int64_t ml = (int64_t)mt_l * TC_MT + (row & 63);
+        float *const plane_re = Upk, *const plane_im = Upk + (int64_t)N * Mc * Tc;
         for (int qi = 0; qi < nqi; ++qi) {
             const int acc = qi & 1;
             mbar_wait(tfull + acc, ((uint32_t)qi >> 1) & 1u);
             tc_fence_after();
             const int q = q_begin + qi;
+            // q = 0: Re U_0 -> re plane slot 0; q = N: Re U_N -> im plane slot 0; Im rows of both dropped
+            const bool store = (q != 0 && q != N) || re_rows;
+            float *plane = (q == N) ? plane_im : ((q == 0 || re_rows) ? plane_re : plane_im);
             const int n = (q == N) ? 0 : q;
-            float2 *dst = Upk + ((int64_t)n * Mc + (int64_t)mt_l * 128 + row) * Tc + (int64_t)nt_l * 128;
+            // workspace [n][t][m]: the 32 lanes hold 32 consecutive images -> each store is one 128-B line
+            float *dst = plane + ((int64_t)n * Tc + (int64_t)nt_l * TC_TT) * Mc + ml;
             const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256);
 #pragma unroll 1
             for (int c0 = 0; c0 < 256; c0 += 32) {
                 uint32_t v[32];
                 tmem_ld32(tbase + (uint32_t)c0, v);
-                float2 *d = dst + c0 / 2;
-                if (q == 0) {
+                if (store) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) reinterpret_cast<float *>(d + i)[0] = __uint_as_float(v[2 * i]);
-                } else if (q == N) {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) reinterpret_cast<float *>(d + i)[1] = __uint_as_float(v[2 * i]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        reinterpret_cast<float4 *>(d)[i] =
-                            make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                        __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+                    for (int i = 0; i < 32; ++i) dst[(int64_t)(c0 + i) * Mc] = __uint_as_float(v[i]);
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty + acc);
         }
+    } else {
+        // ---------------- producers: global compact tiles -> expanded hi/lo operand stages
+        // Register ping-pong: the loads of stage it+1 are in flight while stage it waits for its smem
+        // slot and is expanded, so one global-load latency is hidden per stage.
+        const int pt = tid - 5 * 32;               // 0..255
+        const int total = nqi * KB;
+        auto load = [&](int it, float4 (&ra)[2], float4 (&rb)[8]) {
+            const int q = q_begin + it / KB, kb = it % KB;
+            const float4 *gA = reinterpret_cast<const float4 *>(
+                Acmp + (((int64_t)q * MT + mt) * KB + kb) * (int64_t)(TC_MT * 32));
+            const float4 *gB = reinterpret_cast<const float4 *>(
+                Bcmp + (((int64_t)q * NT + nt) * KB + kb) * (int64_t)(TC_TT * 32));
+#pragma unroll
+            for (int i = 0; i < 2; ++i) ra[i] = __ldg(gA + pt + 256 * i);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) rb[i] = __ldg(gB + pt + 256 * i);
+        };
+        auto expand = [&](int it, const float4 (&ra)[2], const float4 (&rb)[8]) {
+            const int s = it % TC_STAGES;
+            mbar_wait(empty + s, ((uint32_t)(it / TC_STAGES) & 1u) ^ 1u);
+            float4 *sAhi = reinterpret_cast<float4 *>(base + s * TC_STAGE_BYTES);
+            float4 *sAlo = sAhi + TC_A_BYTES / 16;
+            float4 *sBhi = sAlo + TC_A_BYTES / 16;
+            float4 *sBlo = sBhi + TC_B_BYTES / 16;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int idx = pt + 256 * i;               // image row idx/8, chunk position idx%8
+                const float4 v = ra[i];
+                float4 hi, lo;
+                split4(make_float4(v.x, -v.y, v.z, -v.w), hi, lo);     // A_re row
+                sAhi[idx] = hi;
+                sAlo[idx] = lo;
+                split4(make_float4(v.y, v.x, v.w, v.z), hi, lo);       // A_im row (row + 64, same chunk)
+                sAhi[512 + idx] = hi;
+                sAlo[512 + idx] = lo;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int idx = pt + 256 * i;
+                float4 hi, lo;
+                split4(rb[i], hi, lo);
+                sBhi[idx] = hi;
+                sBlo[idx] = lo;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full + s);
+        };
+        float4 ra0[2], rb0[8], ra1[2], rb1[8];
+        if (total > 0) load(0, ra0, rb0);
+        for (int it = 0; it < total; it += 2) {
+            if (it + 1 < total) load(it + 1, ra1, rb1);
+            expand(it, ra0, rb0);
+            if (it + 1 >= total) break;
+            if (it + 2 < total) load(it + 2, ra0, rb0);
+            expand(it + 1, ra1, rb1);
+        }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
 }
 
-// ------------------------------------------------------------------ TC block emission (Step 1 tail)
-__device__ __forceinline__ float tf32_rn(float x) {
-    uint32_t u = __float_as_uint(x);
-    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x0FFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;
-    return __uint_as_float(u);
-}
-
-// Emits the TC blocks of one row (image or template) from its coefficients at[h][q] (smem, [H][Q]).
-// 8 lanes write one 128-byte swizzled row (one 16-byte chunk each).
+// ------------------------------------------------------------------ compact TC block emission (Step 1 tail)
+// Emits the compact TC rows of one row (image or template) from its coefficients at[h][q] (smem,
+// [H][Q]); 8 lanes write one 128-byte swizzled row (one 16-byte chunk each).
 __device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, int64_t row, int64_t ntiles,
                              float *__restrict__ blocks) {
     const int N = Q / 2;
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int ch = tid & 7;
-    const int64_t tile = row / 128;
-    const int rr = (int)(row % 128);
-    const int nc = side == RSVD_SIDE_TEMPLATE ? 2 : 1;          // B rows per template
-    const int rows_tile = 128 * nc;
-    const int total = (N + 1) * KB * nc;                      // (q, kb, c) rows; hi and lo both written
+    const int rows_tile = side == RSVD_SIDE_TEMPLATE ? TC_TT : TC_MT;
+    const int64_t tile = row / rows_tile;
+    const int r = (int)(row % rows_tile);
+    const int total = (N + 1) * KB;
     for (int idx = tid >> 3; idx < total; idx += nthr >> 3) {
-        const int c = idx % nc;
-        const int kb = (idx / nc) % KB;
-        const int q = idx / (nc * KB);
-        const int r = rr * nc + c;                           // row inside the tile
-        float v[4];
+        const int kb = idx % KB;
+        const int q = idx / KB;
+        float4 v;
+        float2 c2[2];
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj) {
             const int j = kb * 16 + ch * 2 + jj;              // complex index of alpha/beta
@@ -274,19 +315,11 @@ __device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, i
                 a = at[(j - H) * Q + ((Q - q) & (Q - 1))];
                 if (side == RSVD_SIDE_TEMPLATE) a = c_conj(a);
             }
-            if (side == RSVD_SIDE_IMAGE) { v[2 * jj] = a.x; v[2 * jj + 1] = a.y; }
-            else if (c == 0) { v[2 * jj] = a.x; v[2 * jj + 1] = -a.y; }
-            else { v[2 * jj] = a.y; v[2 * jj + 1] = a.x; }
+            c2[jj] = a;
         }
-        const int64_t sub = (((int64_t)q * ntiles + tile) * KB + kb) * 2;   // hi sub-tile index
-        const int64_t off = (int64_t)r * 32 + (int64_t)(((ch ^ (r & 7))) * 4);
-        float4 hi, lo;
-        hi.x = tf32_rn(v[0]); lo.x = tf32_rn(v[0] - hi.x);
-        hi.y = tf32_rn(v[1]); lo.y = tf32_rn(v[1] - hi.y);
-        hi.z = tf32_rn(v[2]); lo.z = tf32_rn(v[2] - hi.z);
-        hi.w = tf32_rn(v[3]); lo.w = tf32_rn(v[3] - hi.w);
-        *reinterpret_cast<float4 *>(blocks + sub * rows_tile * 32 + off) = hi;
-        *reinterpret_cast<float4 *>(blocks + (sub + 1) * rows_tile * 32 + off) = lo;
+        v = make_float4(c2[0].x, c2[0].y, c2[1].x, c2[1].y);
+        const int64_t sub = ((int64_t)q * ntiles + tile) * KB + kb;
+        *reinterpret_cast<float4 *>(blocks + (sub * rows_tile + r) * 32 + ((ch ^ (r & 7)) * 4)) = v;
     }
 }
 
@@ -381,8 +414,8 @@ static cudaError_t launch_compress_tc_q(const float2 *rings, int64_t n, int R, c
     const size_t smem = compress_tc_smem(1 << LOGQ, H, R);
     cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel<LOGQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int64_t nrows_tile = tc_rows_pad(n) / 128;
-    compress_tc_kernel<LOGQ><<<(unsigned)n, 256, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H), nrows_tile, blocks);
+    const int64_t ntiles = tc_rows_pad_side(n, side) / (side == RSVD_SIDE_TEMPLATE ? TC_TT : TC_MT);
+    compress_tc_kernel<LOGQ><<<(unsigned)n, 256, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H), ntiles, blocks);
     return cudaGetLastError();
 }
 
@@ -398,7 +431,7 @@ cudaError_t launch_compress_tc(const float2 *rings, int64_t n, int R, int Q, con
     }
 }
 
-// canonical coefficients from TC blocks (hi + lo), test / debug path
+// canonical coefficients from compact TC blocks, test / debug path
 __global__ void unpack_tc_kernel(const float *__restrict__ blocks, int64_t n, int Q, int H, int side, int KB,
                                  int64_t ntiles, float2 *__restrict__ coeffs) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -410,15 +443,11 @@ __global__ void unpack_tc_kernel(const float *__restrict__ blocks, int64_t n, in
     const int qq = q <= N ? q : Q - q;
     const int j = q <= N ? h : H + h;
     const int kb = j / 16, ch = (j % 16) / 2, jj = j % 2;
-    const int nc = side == RSVD_SIDE_TEMPLATE ? 2 : 1;
-    const int r = (int)(row % 128) * nc;                 // c = 0 row (template: (Re, -Im))
-    const int64_t sub = (((int64_t)qq * ntiles + row / 128) * KB + kb) * 2;
-    const int64_t off = (int64_t)r * 32 + (int64_t)((ch ^ (r & 7)) * 4) + 2 * jj;
-    const int64_t rt = 128 * nc * 32;
-    const float x = blocks[sub * rt + off] + blocks[(sub + 1) * rt + off];
-    const float y = blocks[sub * rt + off + 1] + blocks[(sub + 1) * rt + off + 1];
-    float2 v = side == RSVD_SIDE_IMAGE ? make_float2(x, y) : make_float2(x, -y);   // alpha_j / beta_j
-    // undo the conj placement of the block layout
+    const int rows_tile = side == RSVD_SIDE_TEMPLATE ? TC_TT : TC_MT;
+    const int r = (int)(row % rows_tile);
+    const int64_t sub = ((int64_t)qq * ntiles + row / rows_tile) * KB + kb;
+    const int64_t off = (sub * rows_tile + r) * 32 + (int64_t)((ch ^ (r & 7)) * 4) + 2 * jj;
+    float2 v = make_float2(blocks[off], blocks[off + 1]);          // alpha_j / beta_j
     if (q <= N) { if (side == RSVD_SIDE_IMAGE) v = c_conj(v); }
     else { if (side == RSVD_SIDE_TEMPLATE) v = c_conj(v); }
     coeffs[idx] = v;
@@ -426,14 +455,14 @@ __global__ void unpack_tc_kernel(const float *__restrict__ blocks, int64_t n, in
 
 cudaError_t launch_unpack_tc(const float *blocks, int64_t n, int Q, int H, int side, float2 *coeffs, cudaStream_t s) {
     const int64_t total = n * (int64_t)Q * H;
-    unpack_tc_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(blocks, n, Q, H, side, tc_kb(H),
-                                                                     tc_rows_pad(n) / 128, coeffs);
+    const int64_t ntiles = tc_rows_pad_side(n, side) / (side == RSVD_SIDE_TEMPLATE ? TC_TT : TC_MT);
+    unpack_tc_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(blocks, n, Q, H, side, tc_kb(H), ntiles, coeffs);
     return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ contraction launch (one chunk)
-cudaError_t launch_contract_tc(const float *Atc, const float *Btc, int H, int N, int64_t Mpad, int64_t Tpad,
-                               int64_t m0, int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float2 *Upk,
+cudaError_t launch_contract_tc(const float *Acmp, const float *Bcmp, int H, int N, int64_t Mpad, int64_t Tpad,
+                               int64_t m0, int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk,
                                cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
@@ -442,7 +471,7 @@ cudaError_t launch_contract_tc(const float *Atc, const float *Btc, int H, int N,
         attr = true;
     }
     const int KB = tc_kb(H);
-    const int mtl = (int)(mc / 128), ntl = (int)(tc / 128);
+    const int mtl = (int)(mc / TC_MT), ntl = (int)(tc / TC_TT);
     const int ntiles = mtl * ntl;
     const int target = 148;
     int nqg = std::max(1, (target + ntiles - 1) / ntiles);
@@ -450,7 +479,7 @@ cudaError_t launch_contract_tc(const float *Atc, const float *Btc, int H, int N,
     const int qg = (N + 1 + nqg - 1) / nqg;
     nqg = (N + 1 + qg - 1) / qg;
     contract_tc_kernel<<<(unsigned)(ntiles * nqg), TC_THREADS, TC_SMEM, s>>>(
-        Atc, Btc, KB, N, Mpad / 128, Tpad / 128, m0 / 128, t0 / 128, ntl, qg, nqg, Mc, Tc, Upk);
+        Acmp, Bcmp, KB, N, Mpad / TC_MT, Tpad / TC_TT, m0 / TC_MT, t0 / TC_TT, ntl, qg, nqg, Mc, Tc, Upk);
     return cudaGetLastError();
 }
 

@@ -43,9 +43,11 @@ def test_sizes(lib):
         assert api.block_bytes(1, 32, 1) == 17 * 16 * 64 * 8
         api.set_path(api.PATH_TC)
         assert api.path_for(512, 24) == api.PATH_TC
-        # TC layout: (N+1) q x KB k-blocks x (hi, lo) x rows padded to 128 x 128 B; templates 2 rows each
-        assert api.block_bytes(16384, 512, 24, api.SIDE_IMAGE) == 257 * 3 * 2 * 16384 * 128
-        assert api.block_bytes(8192, 512, 24, api.SIDE_TEMPLATE) == 257 * 3 * 2 * 8192 * 128 * 2
+        # compact TC layout: (N+1) q x KB = ceil(2H/16) k-block rows of 128 B; images padded to 64,
+        # templates to 256 rows
+        assert api.block_bytes(16384, 512, 24, api.SIDE_IMAGE) == 257 * 3 * 16384 * 128
+        assert api.block_bytes(8192, 512, 24, api.SIDE_TEMPLATE) == 257 * 3 * 8192 * 128
+        assert api.block_bytes(10, 64, 4, api.SIDE_TEMPLATE) == 33 * 1 * 256 * 128
         assert api.path_for(1024, 256) == api.PATH_SIMT        # H x Q block too large for the TC compress
     finally:
         api.set_path(api.PATH_AUTO)
