@@ -148,19 +148,22 @@ __device__ __forceinline__ void dif_reg(float2 (&v)[E]) {
 // stw[s] = W_{2h}^{l & (h-1)} for stage s (h = L/2 >> s), computed by lane_stage_twiddles.
 template <int E, int L>
 __device__ __forceinline__ void dif_lanes(float2 (&v)[E], int l, const float2 (&stw)[clog2(L) > 0 ? clog2(L) : 1]) {
+    // Select-free butterfly: lower lanes v + p, upper lanes (p - v) * tw, written as
+    // (p + sgn v) * tw' with per-lane sgn = -1 / +1 and tw' = tw / 1.  The last stage (h = 1) has
+    // tw = W_2^0 = 1 on every lane, so its multiply is skipped.
 #pragma unroll
     for (int s = 0; s < clog2(L); ++s) {
         const int h = (L >> 1) >> s;
         const bool upper = (l & h) != 0;
-        const float2 tw = stw[s];
+        const float sgn = upper ? -1.f : 1.f;
+        const float2 tw = upper ? stw[s] : make_float2(1.f, 0.f);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             float2 p;
             p.x = __shfl_xor_sync(0xffffffffu, v[e].x, h);
             p.y = __shfl_xor_sync(0xffffffffu, v[e].y, h);
-            const float2 sum = c_add(v[e], p);
-            const float2 dif = c_mul(c_sub(p, v[e]), tw);
-            v[e] = upper ? dif : sum;
+            const float2 t = make_float2(fmaf(sgn, v[e].x, p.x), fmaf(sgn, v[e].y, p.y));
+            v[e] = (h == 1) ? t : c_mul(t, tw);
         }
     }
 }

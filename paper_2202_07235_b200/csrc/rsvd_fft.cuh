@@ -48,9 +48,11 @@ struct FftCfg {
     static constexpr int P = 32 + G;               // transpose row stride (8-byte units); P = G mod 16
     static constexpr int SROW = TB + 1;            // staged spectrum row stride (odd: conflict-free columns)
     static constexpr int SBUF = N * SROW;          // float2 per stage buffer
+    static constexpr int V = TB / 4;               // float4 per plane row of an item
+    static constexpr int RPP = FR_THREADS / V;     // rows per staging pass
+    static constexpr int PASSES = (N + RPP - 1) / RPP;
     static constexpr size_t smem_bytes() {
-        return (size_t)2 * SBUF * 8 + (E > 1 ? (size_t)FR_WARPS * E * P * 8 : 0) + (size_t)E * 32 * 8 +
-               (size_t)E * G * 8 + (size_t)N * 8 + 16;
+        return (size_t)SBUF * 8 + (E > 1 ? (size_t)FR_WARPS * E * P * 8 : 0) + (size_t)N * 8 + 16;
     }
 };
 
@@ -71,42 +73,56 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float *__r
     using C = FftCfg<N>;
     constexpr int L = C::L, E = C::E, G = C::G, GP = C::GP, TB = C::TB, P = C::P, SROW = C::SROW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2 *Sbuf = reinterpret_cast<float2 *>(smem_raw);               // [2][N][SROW] staged spectra
-    float2 *Xs = Sbuf + 2 * C::SBUF;                                    // [warps][E][P] transpose scratch
-    float2 *twN = Xs + (E > 1 ? FR_WARPS * E * P : 0);                 // [E][32]  W_N^{l k1}
-    float2 *tw32 = twN + E * 32;                                        // [E][G]   W_32^{s k}
-    float2 *pre = tw32 + E * G;                                         // [N]      W_Q^n
-    unsigned long long *skey = reinterpret_cast<unsigned long long *>(pre + N);
+    float2 *S = reinterpret_cast<float2 *>(smem_raw);                  // [N][SROW] staged spectra
+    float2 *Xs = S + C::SBUF;                                           // [warps][E][P] transpose scratch
+    float2 *pre = Xs + (E > 1 ? FR_WARPS * E * P : 0);                 // [N]      W_Q^n (E == 1 path)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // work item = (template tl, block of TB consecutive images); workspace [plane][n][t][m]
     const int64_t nmb = (mcv + TB - 1) / TB;
     const int64_t nitems = tcv * nmb;
 
-    const int64_t plane = (int64_t)N * Mc * Tc;
-    auto stage = [&](int64_t item, int buf) {
-        const int64_t tl = item / nmb, mb0 = (item % nmb) * TB;
-        float *S = reinterpret_cast<float *>(Sbuf + buf * C::SBUF);
-        const float *src = Upk + tl * Mc + mb0;
-        for (int i = tid; i < N * TB; i += FR_THREADS) {
-            const int n = i / TB, c = i % TB;
-            const float *g = src + (int64_t)n * Mc * Tc + c;
-            cp_async4(S + 2 * (n * SROW + c), g);
-            cp_async4(S + 2 * (n * SROW + c) + 1, g + plane);
+    // Staging: 16-byte loads of the re / im plane rows of an item into registers (issued one item
+    // ahead, so their latency hides behind the transform), then 8-byte stores of (re, im) pairs into
+    // the odd-stride interleaved tile S[n][SROW] (conflict-free both ways).
+    const int64_t plane4 = (int64_t)N * Mc * Tc / 4;
+    const int64_t row4 = Mc * Tc / 4;
+    const int n0 = tid / C::V, c4 = tid % C::V;
+    float4 rre[C::PASSES], rim[C::PASSES];
+    auto load = [&](int64_t it) {
+        const int64_t tl = it / nmb, mb0 = (it % nmb) * TB;
+        const float4 *g = reinterpret_cast<const float4 *>(Upk + tl * Mc + mb0) + (int64_t)n0 * row4 + c4;
+#pragma unroll
+        for (int j = 0; j < C::PASSES; ++j) {
+            if (n0 + j * C::RPP < N) {
+                rre[j] = __ldg(g + (int64_t)j * C::RPP * row4);
+                rim[j] = __ldg(g + (int64_t)j * C::RPP * row4 + plane4);
+            }
         }
-        cp_async_commit_fr();
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int j = 0; j < C::PASSES; ++j) {
+            const int n = n0 + j * C::RPP;
+            if (n < N) {
+                float2 *d = S + n * SROW + 4 * c4;
+                d[0] = make_float2(rre[j].x, rim[j].x);
+                d[1] = make_float2(rre[j].y, rim[j].y);
+                d[2] = make_float2(rre[j].z, rim[j].z);
+                d[3] = make_float2(rre[j].w, rim[j].w);
+            }
+        }
     };
 
     int64_t item = blockIdx.x;
-    if (item < nitems) stage(item, 0);
-    for (int i = tid; i < E * 32 && E > 1; i += FR_THREADS) twN[i] = twiddle_N(i % 32, i / 32, N);
-    for (int i = tid; i < E * G && E > 1; i += FR_THREADS) tw32[i] = twiddle_N(i % G, i / G, 32);
-    for (int i = tid; i < N; i += FR_THREADS) {
+    if (item < nitems) { load(item); store(); }
+    if (item + gridDim.x < nitems) load(item + gridDim.x);
+    for (int i = tid; i < N && E == 1; i += FR_THREADS) {
         float sn, cs;
         sincospif(2.0f * (float)i / (float)Q, &sn, &cs);
         pre[i] = make_float2(cs, -sn);
     }
-    (void)skey;
+    __syncthreads();
 
     const float PI = 3.14159265358979323846f;
     // per-lane constants
@@ -117,18 +133,17 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float *__r
     lane_stage_twiddles<L>(l1, stwL);
     lane_stage_twiddles<G>(s2, stwG);
     float2 *xw = Xs + warp * E * P;
+    float2 preR[E], twNR[E], tw32R[E];                   // per-lane twiddles (E > 1 path)
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        float sn, cs;
+        sincospif(2.0f * (float)(lane + 32 * e) / (float)Q, &sn, &cs);
+        preR[e] = make_float2(cs, -sn);                  // W_Q^{l + 32 e}
+        twNR[e] = twiddle_N(lane, e, N);                 // W_N^{l e}
+        tw32R[e] = twiddle_N(s2, e, 32);                 // W_32^{s e}
+    }
 
-    for (int k = 0; item < nitems; item += gridDim.x, ++k) {
-        const int buf = k & 1;
-        const int64_t next = item + gridDim.x;
-        if (next < nitems) {
-            stage(next, buf ^ 1);
-            cp_async_wait_fr<1>();
-        } else {
-            cp_async_wait_fr<0>();
-        }
-        __syncthreads();
-        const float2 *S = Sbuf + buf * C::SBUF;
+    for (; item < nitems; item += gridDim.x) {
         const int64_t tl = item / nmb, mb0 = (item % nmb) * TB;
         const int64_t t = t0 + tl;
 
@@ -180,6 +195,9 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float *__r
             }
         } else {
             const int l = lane;
+            // affine per-lane row pointers: u at rows l + 32e, mirror at rows N - l - 32e
+            const float2 *su = S + l * SROW;
+            const float2 *sm_ = S + (N - l) * SROW;
             for (int tt = warp; tt < TB; tt += FR_WARPS) {
                 const int64_t ml = mb0 + tt;
                 const bool valid = ml < mcv;
@@ -187,12 +205,11 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float *__r
                 float2 z[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    const int n = l + 32 * e;
-                    const float2 u = S[n * SROW + tt];
-                    const float2 mm = S[((N - n) & (N - 1)) * SROW + tt];
+                    const float2 u = su[e * 32 * SROW + tt];
+                    const float2 mm = sm_[tt - e * 32 * SROW];                 // row N - n (l = 0, e = 0: unused)
                     const float2 sm = make_float2(u.x + mm.x, u.y - mm.y);     // U + conj M
                     const float2 d = make_float2(u.x - mm.x, u.y + mm.y);      // U - conj M
-                    const float2 wd = c_mul(pre[n], d);
+                    const float2 wd = c_mul(preR[e], d);
                     z[e] = make_float2(sm.x - wd.y, sm.y + wd.x);              // (s + i w d), pi applied last
                 }
                 if (l == 0) z[0] = make_float2(S[tt].x + S[tt].y, S[tt].x - S[tt].y);   // n = 0: (U_0, U_N)
@@ -200,7 +217,7 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float *__r
 #pragma unroll
                 for (int k1 = 1; k1 < E; ++k1) {
                     const int r = brev(k1, clog2(E));
-                    z[r] = c_mul(z[r], twN[k1 * 32 + l]);
+                    z[r] = c_mul(z[r], twNR[k1]);
                 }
                 __syncwarp();
 #pragma unroll
@@ -208,7 +225,13 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float *__r
                 __syncwarp();
 #pragma unroll
                 for (int u = 0; u < E; ++u) z[u] = xw[k1p * P + s2 + G * u];
-                fft_dist<E, G>(z, s2, tw32, stwG);
+                dif_reg<E>(z);
+#pragma unroll
+                for (int k = 1; k < E; ++k) {
+                    const int r = brev(k, clog2(E));
+                    z[r] = c_mul(z[r], tw32R[k]);
+                }
+                dif_lanes<E, G>(z, s2, stwG);
                 const int b = (int)(__brev((unsigned)s2) >> (32 - clog2(G)));
                 if constexpr (MODE == MODE_LANDSCAPE) {
                     if (valid) {
@@ -250,7 +273,13 @@ __global__ void __launch_bounds__(FR_THREADS) fft_reduce_kernel(const float *__r
                 }
             }
         }
-        __syncthreads();       // stage buffer `buf` is refilled by the next iteration's prefetch
+        __syncthreads();                                 // everyone is done with S
+        const int64_t next = item + gridDim.x;
+        if (next < nitems) {
+            store();                                     // item `next` (loaded one iteration ago)
+            if (next + gridDim.x < nitems) load(next + gridDim.x);
+        }
+        __syncthreads();
     }
 }
 
