@@ -1,0 +1,134 @@
+"""Full-size parity (-m gpu): BASELINE.json's Medium, Large and Translations configs run through the
+C ABI in the same launch configuration bench.py times (default path, 128 MB spectrum workspace), and
+the outputs are checked on seeded samples the fp64 oracle can compute one pair at a time.
+Tolerance: max|X_gpu - X_ref| <= 1e-5 max|X_ref| over the compared sample."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import ref
+from synth import make_dataset, sample_pairs
+from tests.gpu_helpers import TOL_FP32, assert_argmax_gated, assert_landscape_close, cuda, to_np
+
+pytestmark = pytest.mark.gpu
+api = pytest.importorskip("paper_2202_07235_b200.api")
+WORK = 128 << 20
+
+
+def _rows(t, idx):
+    return t[torch.as_tensor(np.asarray(idx), device=t.device)].cpu().numpy()
+
+
+def _blocks(d, U, H):
+    wd, Ud = d.w.contiguous(), cuda(U, torch.float64)
+    return (api.compress(d.images, wd, Ud, api.SIDE_IMAGE), api.compress(d.templates, wd, Ud, api.SIDE_TEMPLATE))
+
+
+@pytest.fixture(scope="module")
+def medium():
+    return make_dataset("medium", device="cuda")
+
+
+@pytest.mark.parametrize("H", [64, 32, 16, 8])
+def test_medium_full_per_pair_sampled(medium, H):
+    d = medium
+    M, T, Q, R = d.images.shape[0], d.templates.shape[0], d.Q, d.R
+    w = to_np(d.w)
+    U, lam = api.build_basis(d.templates, w, H)
+    ib, tb = _blocks(d, U, H)
+    work = torch.empty(WORK // 4, dtype=torch.float32, device="cuda")
+    val, k = api.align_argmax(ib, M, tb, T, Q, H, api.PER_PAIR, work)
+    torch.cuda.synchronize()
+    m, t = sample_pairs("medium", M, T, 256, 64, to_np(d.t_true))
+    um, im_ = np.unique(m, return_inverse=True)
+    ut, it_ = np.unique(t, return_inverse=True)
+    A, B = _rows(d.images, um), _rows(d.templates, ut)
+    X_ref = ref.landscape_rank(A, B, w, U, im_, it_).real
+    tol_abs = TOL_FP32 * np.abs(X_ref).max()
+    v_gpu, k_gpu = to_np(val)[m, t], to_np(k)[m, t]
+    assert np.abs(v_gpu - X_ref.max(-1)).max() <= tol_abs
+    assert_argmax_gated(k_gpu, X_ref, tol_abs)
+    # Medium report: rank-H vs full landscape on the sampled pairs -- reported,
+    # not gated (truncation, not kernel error)
+    X_full = ref.landscape_full(A, B, w, im_, it_).real
+    if H == R:
+        assert np.abs(X_ref - X_full).max() <= 1e-10 * np.abs(X_full).max()
+    f = ref.backward_fraction(X_ref, X_full)
+    agree = float((ref.argmax_first(X_ref) == ref.argmax_first(X_full)).mean())
+    Xc, Fc = X_ref - X_ref.mean(-1, keepdims=True), X_full - X_full.mean(-1, keepdims=True)
+    print(f"\nmedium H={H}: lambda_H/lambda_1={lam[H - 1] / lam[0]:.3e} rel_frob={ref.rel_frobenius(X_ref, X_full):.3e} "
+          f"(mean-sub {ref.rel_frobenius(Xc, Fc):.3e}) corr={ref.correlation(X_ref, X_full):.5f} "
+          f"(mean-sub {ref.correlation(Xc, Fc):.5f}) mean f={f.mean():.4f} argmax agreement={agree:.4f}")
+
+
+def test_large_full_per_image_bench_configuration():
+    d = make_dataset("large", device="cuda")
+    M, T, Q, H = d.images.shape[0], d.templates.shape[0], d.Q, 24
+    w = to_np(d.w)
+    U, _ = api.build_basis(d.templates, w, H)
+    ib, tb = _blocks(d, U, H)
+    work = torch.empty(WORK // 4, dtype=torch.float32, device="cuda")
+    keys = api.winners_reset(torch.zeros(M, dtype=torch.int64, device="cuda"))
+    api.align_argmax(ib, M, tb, T, Q, H, api.PER_IMAGE, work, best_key=keys)
+    val, tw, kw = (to_np(x) for x in api.winners_unpack(keys, Q))
+    rng = np.random.default_rng(7)
+    ms = rng.choice(M, 6, replace=False)
+    tt = to_np(d.t_true)
+    # oracle on the reported winner pair and on the planted (true) template of each sampled image
+    ia = np.repeat(np.arange(len(ms)), 2)
+    A = _rows(d.images, ms)
+    tsel = np.stack([tw[ms], tt[ms]], 1).ravel()
+    ut, ib_ = np.unique(tsel, return_inverse=True)
+    B = _rows(d.templates, ut)
+    X = ref.landscape_rank(A, B, w, U, ia, ib_).real.reshape(len(ms), 2, Q)
+    scale = np.abs(X).max()
+    tol_abs = TOL_FP32 * scale
+    for i, m in enumerate(ms):
+        xw, xt = X[i, 0], X[i, 1]
+        assert abs(val[m] - xw[kw[m]]) <= tol_abs                   # value matches the oracle at (t, k)
+        assert xw[kw[m]] >= xw.max() - tol_abs                      # k is the argmax for that template
+        assert val[m] >= xt.max() - tol_abs                         # no worse than the planted template
+    # sub-block at full sizes: per-pair values and landscapes vs the oracle element by element
+    mb = rng.choice(M, 24, replace=False)
+    tb_ = rng.choice(T, 24, replace=False)
+    wd, Ud = d.w.contiguous(), cuda(U, torch.float64)
+    sA, sB = d.images[torch.as_tensor(mb, device="cuda")].contiguous(), d.templates[torch.as_tensor(tb_, device="cuda")].contiguous()
+    sib, stb = api.compress(sA, wd, Ud, api.SIDE_IMAGE), api.compress(sB, wd, Ud, api.SIDE_TEMPLATE)
+    Xg = to_np(api.align_landscape(sib, 24, stb, 24, Q, H, work))
+    ia, ib2 = np.meshgrid(np.arange(24), np.arange(24), indexing="ij")
+    Xr = ref.landscape_rank(sA.cpu().numpy(), sB.cpu().numpy(), w, U, ia.ravel(), ib2.ravel()).real.reshape(24, 24, Q)
+    assert_landscape_close(Xg, Xr)
+
+
+def test_translations_streamed_landscape_and_argmax():
+    d = make_dataset("translations", device="cuda")
+    M, T, Q, H = d.images.shape[0], d.templates.shape[0], d.Q, 16
+    w = to_np(d.w)
+    U, _ = api.build_basis(d.templates, w, H)
+    ib, tb = _blocks(d, U, H)
+    work = torch.empty(WORK // 4, dtype=torch.float32, device="cuda")
+    val, k = api.align_argmax(ib, M, tb, T, Q, H, api.PER_PAIR, work)
+    val, k = to_np(val), to_np(k)
+    m, t = sample_pairs("translations", M, T, 192, 64, to_np(d.t_true))
+    um, im_ = np.unique(m, return_inverse=True)
+    ut, it_ = np.unique(t, return_inverse=True)
+    X_ref = ref.landscape_rank(_rows(d.images, um), _rows(d.templates, ut), w, U, im_, it_).real
+    tol_abs = TOL_FP32 * np.abs(X_ref).max()
+    assert np.abs(val[m, t] - X_ref.max(-1)).max() <= tol_abs
+    assert_argmax_gated(k[m, t], X_ref, tol_abs)
+    # the full M x T x Q landscape, streamed to HBM in image blocks through the caller's strides
+    blk = 4608
+    X = torch.empty((blk, T, Q), dtype=torch.float32, device="cuda")
+    order = np.argsort(m)
+    for b0 in range(0, M, blk):
+        nb = min(blk, M - b0)
+        # blocks of image rows are compressed separately (rows are independent)
+        rows = d.images[b0:b0 + nb].contiguous()
+        bib = api.compress(rows, d.w.contiguous(), cuda(U, torch.float64), api.SIDE_IMAGE)
+        api.align_landscape(bib, nb, tb, T, Q, H, work, X=X, ld_m=T * Q, ld_t=Q)
+        sel = order[(m[order] >= b0) & (m[order] < b0 + nb)]
+        if len(sel):
+            got = X[torch.as_tensor(m[sel] - b0, device="cuda"), torch.as_tensor(t[sel], device="cuda")].cpu().numpy()
+            err = np.abs(got - X_ref[sel]).max()
+            assert err <= tol_abs, err / np.abs(X_ref).max()
+    torch.cuda.synchronize()
