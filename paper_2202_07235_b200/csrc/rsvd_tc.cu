@@ -110,16 +110,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ float tf32_rn(float x) {
-    uint32_t u = __float_as_uint(x);
-    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x0FFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;
+__device__ __forceinline__ float tf32_rna(float x) {       // hardware round-to-TF32 (one instruction)
+    uint32_t u;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
     return __uint_as_float(u);
 }
+// x = hi + lo exactly (hi TF32-rounded; lo = x - hi has <= 13 significant bits and is fed as fp32:
+// the tensor core keeps its top 11, an error <= 2^-22 |x|).
 __device__ __forceinline__ void split4(float4 v, float4 &hi, float4 &lo) {
-    hi.x = tf32_rn(v.x); lo.x = tf32_rn(v.x - hi.x);
-    hi.y = tf32_rn(v.y); lo.y = tf32_rn(v.y - hi.y);
-    hi.z = tf32_rn(v.z); lo.z = tf32_rn(v.z - hi.z);
-    hi.w = tf32_rn(v.w); lo.w = tf32_rn(v.w - hi.w);
+    hi.x = tf32_rna(v.x); lo.x = v.x - hi.x;
+    hi.y = tf32_rna(v.y); lo.y = v.y - hi.y;
+    hi.z = tf32_rna(v.z); lo.z = v.z - hi.z;
+    hi.w = tf32_rna(v.w); lo.w = v.w - hi.w;
 }
 
 // ------------------------------------------------------------------ contraction kernel
@@ -248,14 +250,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 const int idx = pt + 256 * i;               // image row idx/8, chunk position idx%8
-                const float4 v = ra[i];
                 float4 hi, lo;
-                split4(make_float4(v.x, -v.y, v.z, -v.w), hi, lo);     // A_re row
-                sAhi[idx] = hi;
-                sAlo[idx] = lo;
-                split4(make_float4(v.y, v.x, v.w, v.z), hi, lo);       // A_im row (row + 64, same chunk)
-                sAhi[512 + idx] = hi;
-                sAlo[512 + idx] = lo;
+                split4(ra[i], hi, lo);
+                sAhi[idx] = make_float4(hi.x, -hi.y, hi.z, -hi.w);     // A_re row: (Re a, -Im a)
+                sAlo[idx] = make_float4(lo.x, -lo.y, lo.z, -lo.w);
+                sAhi[512 + idx] = make_float4(hi.y, hi.x, hi.w, hi.z); // A_im row (row + 64, same chunk)
+                sAlo[512 + idx] = make_float4(lo.y, lo.x, lo.w, lo.z);
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -269,12 +269,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
             __syncwarp();
             if (lane == 0) mbar_arrive(full + s);
         };
+        // L2 prefetch of the compact sub-tiles PF stages ahead (one bulk prefetch per operand), so the
+        // ping-pong loads hit L2 instead of DRAM.
+        constexpr int PF = 4;
+        auto prefetch = [&](int it) {
+            if (pt != 0 || it >= total) return;
+            const int q = q_begin + it / KB, kb = it % KB;
+            const float *gA = Acmp + (((int64_t)q * MT + mt) * KB + kb) * (int64_t)(TC_MT * 32);
+            const float *gB = Bcmp + (((int64_t)q * NT + nt) * KB + kb) * (int64_t)(TC_TT * 32);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gA), "r"((uint32_t)(TC_MT * 128)) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gB), "r"((uint32_t)(TC_TT * 128)) : "memory");
+        };
+        for (int it = 1; it < PF; ++it) prefetch(it);
         float4 ra0[2], rb0[8], ra1[2], rb1[8];
         if (total > 0) load(0, ra0, rb0);
         for (int it = 0; it < total; it += 2) {
+            prefetch(it + PF);
             if (it + 1 < total) load(it + 1, ra1, rb1);
             expand(it, ra0, rb0);
             if (it + 1 >= total) break;
+            prefetch(it + 1 + PF);
             if (it + 2 < total) load(it + 2, ra0, rb0);
             expand(it + 1, ra1, rb1);
         }
