@@ -136,15 +136,26 @@ struct AlignArgs {
     int64_t ld_m, ld_t;
 };
 
-static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const float *Upk, int64_t Mc, int64_t Tc,
+static cudaError_t make_tmap_any(int LOGN, CUtensorMap *tm, const float *Upk, int64_t Mc, int64_t Tc) {
+    switch (LOGN) {
+        case 4: return make_spectrum_tmap<4>(tm, Upk, Mc, Tc);
+        case 5: return make_spectrum_tmap<5>(tm, Upk, Mc, Tc);
+        case 6: return make_spectrum_tmap<6>(tm, Upk, Mc, Tc);
+        case 7: return make_spectrum_tmap<7>(tm, Upk, Mc, Tc);
+        case 8: return make_spectrum_tmap<8>(tm, Upk, Mc, Tc);
+        default: return make_spectrum_tmap<9>(tm, Upk, Mc, Tc);
+    }
+}
+
+static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const CUtensorMap &tm, int64_t Mc, int64_t Tc,
                                   int64_t m0, int64_t t0, int64_t mcv, int64_t tcv, const FftOut &o) {
     switch (LOGN) {
-        case 4: return launch_fft<4>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
-        case 5: return launch_fft<5>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
-        case 6: return launch_fft<6>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
-        case 7: return launch_fft<7>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
-        case 8: return launch_fft<8>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
-        default: return launch_fft<9>(mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
+        case 4: return launch_fft<4>(mode, s, tm, Mc, Tc, m0, t0, mcv, tcv, o);
+        case 5: return launch_fft<5>(mode, s, tm, Mc, Tc, m0, t0, mcv, tcv, o);
+        case 6: return launch_fft<6>(mode, s, tm, Mc, Tc, m0, t0, mcv, tcv, o);
+        case 7: return launch_fft<7>(mode, s, tm, Mc, Tc, m0, t0, mcv, tcv, o);
+        case 8: return launch_fft<8>(mode, s, tm, Mc, Tc, m0, t0, mcv, tcv, o);
+        default: return launch_fft<9>(mode, s, tm, Mc, Tc, m0, t0, mcv, tcv, o);
     }
 }
 
@@ -170,6 +181,8 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const FftOut o{a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t, a.T, a.t_offset};
     cudaError_t e;
     const int LOGN = ilog2(N);
+    CUtensorMap tmap;
+    if ((e = make_tmap_any(LOGN, &tmap, Upk, Mc, Tc)) != cudaSuccess) return cuda_check(e, "spectrum tensor map");
     const bool timed = timing_enabled();
     for (int64_t t0 = 0; t0 < Tpad; t0 += Tc) {
         const int64_t tc_ = std::min(Tc, Tpad - t0);
@@ -188,7 +201,7 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
                 if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "contract launch");
             }
             cudaEvent_t ev1 = timed ? timing_event(s) : nullptr;
-            e = launch_fft_any(LOGN, a.mode, s, Upk, Mc, Tc, m0, t0, mcv, tcv, o);
+            e = launch_fft_any(LOGN, a.mode, s, tmap, Mc, Tc, m0, t0, mcv, tcv, o);
             if (e != cudaSuccess) return cuda_check(e, "fft_reduce launch");
             count_launches(2);
             if (timed) {
