@@ -55,7 +55,7 @@ typedef enum { RSVD_PER_PAIR = 0, RSVD_PER_IMAGE = 1 } rsvd_reduce;
 
 /* Thread-local message describing the last non-OK status returned on this thread. */
 const char *rsvd_last_error(void);
-/* ABI version of this header (bumped when a signature or the block layout changes): 2. */
+/* ABI version of this header (bumped when a signature or the block layout changes): 3. */
 int32_t rsvd_abi_version(void);
 
 /* ------------------------------------------------------------------ sizes */
@@ -63,8 +63,9 @@ int32_t rsvd_abi_version(void);
  * TEMPLATE) at (Q, H).  The layout is opaque (it depends on the contraction path, see
  * rsvd_path_for); read it back only through rsvd_blocks_unpack. */
 int64_t rsvd_block_bytes(int64_t rows, int32_t Q, int32_t H, rsvd_side side);
-/* Contraction path used for (Q, H): 1 = FP32 SIMT, 2 = tcgen05 tensor cores with 3xTF32 error
- * compensation (~fp32 accuracy).  Default (AUTO): tensor cores whenever a row's H x Q coefficient
+/* Contraction path used for (Q, H): 1 = FP32 SIMT, 2 = tcgen05 tensor cores on CTA pairs with an
+ * fp16 hi/lo split of both (power-of-two row-scaled) operands, 3 MMAs per product, fp32
+ * accumulation (~fp32 accuracy, same 1e-5 gate as the SIMT path).  Default (AUTO): tensor cores whenever a row's H x Q coefficient
  * block fits in shared memory (H * Q <= 24576), else SIMT.  rsvd_set_path(0 auto | 1 simt | 2 tc)
  * overrides it process-wide (also env RSVD_PATH=auto|simt|tc); blocks must be produced and consumed
  * under the same path. */

@@ -3,9 +3,10 @@
 //
 // Data flow per chunk of (Mc x Tc) pairs, all on `stream`:
 //   contract_kernel   U_q[m,t] = sum_j alpha[q][j][m] beta[q][j][t] = S_q + conj(S_{Q-q}), q = 0..N
-//                     (N = Q/2; S_q = sum_h conj(A_q[m,h]) B_q[t,h]) -> workspace Upk[n][m][t] (q-major,
+//                     (N = Q/2; S_q = sum_h conj(A_q[m,h]) B_q[t,h]) -> workspace Upk[n][t][m] (q-major,
 //                     coalesced stores; Upk[0] packs the two real values (U_0, U_N)).  FP32 SIMT,
 //                     register tiled, cp.async double-buffered operand tiles.
+//   contract_tc_kernel (rsvd_tc.cu) the same U_q on tcgen05 CTA pairs (fp16 hi/lo split, TMA-fed).
 //   fft_reduce_kernel (rsvd_fft.cuh) Re X_k = 2 pi Re sum_q e^{-2 pi i qk/Q} S_q, fused with the
 //                     per-pair argmax (smallest k on ties), the per-image packed-key max, or the
 //                     landscape store.  The M x T x Q landscape never leaves the chip unless asked.
@@ -163,8 +164,8 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const int N = a.Q / 2;
     const int Kpad = (int)kpad_of(a.H);
     const bool tc = resolve_path(a.Q, a.H) == PATH_TC;
-    // pair tiles: SIMT 64 x 64; TC 64 images x 256 templates (one tcgen05 CTA tile)
-    const int64_t TM = 64, TT = tc ? 256 : CT_TILE;
+    // pair tiles: SIMT 64 x 64; TC 128 images x 256 templates (one tcgen05 CTA-pair tile)
+    const int64_t TM = tc ? 128 : 64, TT = tc ? 256 : CT_TILE;
     const int64_t Mpad = tc ? tc_rows_pad_side(a.M, RSVD_SIDE_IMAGE) : rows_pad_of(a.M);
     const int64_t Tpad = tc ? tc_rows_pad_side(a.T, RSVD_SIDE_TEMPLATE) : rows_pad_of(a.T);
     // chunk: Mc x Tc pairs (multiples of the tile) with Mc * Tc * N * 8 <= work_bytes.  Chunks are
@@ -177,9 +178,18 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     int64_t mct = std::min(mmax, std::max<int64_t>(1, ntiles / tct));
     tct = std::min(tmax, std::max(tct, ntiles / mct));      // widen t when rows run out
     const int64_t Mc = mct * TM, Tc = tct * TT;
-    float *Upk = reinterpret_cast<float *>(a.work);
-    const FftOut o{a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t, a.T, a.t_offset};
+    CUtensorMap tmA, tmB;
     cudaError_t e;
+    if (tc) {
+        if ((e = make_tc_operand_tmap(&tmA, a.alpha, a.M, a.Q, a.H, RSVD_SIDE_IMAGE)) != cudaSuccess)
+            return cuda_check(e, "image operand tensor map");
+        if ((e = make_tc_operand_tmap(&tmB, a.beta, a.T, a.Q, a.H, RSVD_SIDE_TEMPLATE)) != cudaSuccess)
+            return cuda_check(e, "template operand tensor map");
+    }
+    float *Upk = reinterpret_cast<float *>(a.work);
+    const FftOut o{a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t, a.T, a.t_offset,
+                   tc ? tc_scales(a.alpha, a.M, a.Q, a.H, RSVD_SIDE_IMAGE) : nullptr,
+                   tc ? tc_scales(a.beta, a.T, a.Q, a.H, RSVD_SIDE_TEMPLATE) : nullptr};
     const int LOGN = ilog2(N);
     CUtensorMap tmap;
     if ((e = make_tmap_any(LOGN, &tmap, Upk, Mc, Tc)) != cudaSuccess) return cuda_check(e, "spectrum tensor map");
@@ -192,8 +202,7 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
             const int64_t mcv = std::min(mc, a.M - m0);
             cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
             if (tc) {
-                e = launch_contract_tc(reinterpret_cast<const float *>(a.alpha), reinterpret_cast<const float *>(a.beta),
-                                       a.H, N, Mpad, Tpad, m0, t0, mc, tc_, Mc, Tc, Upk, s);
+                e = launch_contract_tc(tmA, tmB, a.H, N, m0, t0, mc, tc_, Mc, Tc, Upk, num_sms(), s);
                 if (e != cudaSuccess) return cuda_check(e, "contract (tcgen05) launch");
             } else {
                 dim3 g1((unsigned)(tc_ / CT_TILE), (unsigned)(mc / CT_TILE), (unsigned)((N + 1 + CT_QB - 1) / CT_QB));
@@ -257,7 +266,7 @@ using namespace rsvd;
 
 extern "C" int64_t rsvd_align_min_workspace_bytes(int32_t Q) {
     if (Q < 2) return -1;
-    return (int64_t)128 * 128 * (Q / 2) * (int64_t)sizeof(float2);     // one 128 x 128 pair tile (either path)
+    return (int64_t)128 * 256 * (Q / 2) * (int64_t)sizeof(float2);     // one 128 x 256 pair tile (either path)
 }
 
 extern "C" int64_t rsvd_align_workspace_bytes(int64_t M, int64_t T, int32_t Q, int32_t H) {

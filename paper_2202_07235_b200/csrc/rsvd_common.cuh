@@ -12,6 +12,7 @@
 // brev_E(k1) holds X[k1 + E * brev_L(l)].
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -33,7 +34,7 @@ cudaEvent_t timing_event(cudaStream_t s);
 void timing_span(cudaEvent_t a, cudaEvent_t b, int kind);
 enum { TK_CONTRACT = 0, TK_FFT = 1, TK_COMPRESS = 2, TK_BASIS = 3 };
 
-// contraction path: FP32 SIMT (block layout "simt") or tcgen05 3xTF32 (block layout "tc").
+// contraction path: FP32 SIMT (block layout "simt") or tcgen05 fp16 hi/lo split on CTA pairs (layout "tc").
 // resolve_path(Q, H) is the single source of truth used by block sizing, compress and align.
 enum { PATH_AUTO = 0, PATH_SIMT = 1, PATH_TC = 2 };
 int resolve_path(int Q, int H);
@@ -45,9 +46,10 @@ int64_t tc_block_bytes(int64_t rows, int Q, int H, int side);
 cudaError_t launch_compress_tc(const float2 *rings, int64_t n, int R, int Q, const double *w, const double *U, int H,
                                int side, float *blocks, cudaStream_t s);
 cudaError_t launch_unpack_tc(const float *blocks, int64_t n, int Q, int H, int side, float2 *coeffs, cudaStream_t s);
-cudaError_t launch_contract_tc(const float *Atc, const float *Btc, int H, int N, int64_t Mpad, int64_t Tpad,
-                               int64_t m0, int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk,
-                               cudaStream_t s);
+cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t rows, int Q, int H, int side);
+const float *tc_scales(const void *blocks, int64_t rows, int Q, int H, int side);
+cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int64_t m0, int64_t t0,
+                               int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms, cudaStream_t s);
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }

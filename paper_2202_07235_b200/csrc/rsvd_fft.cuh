@@ -71,6 +71,7 @@ struct FftOut {
     unsigned long long *best_key;
     float *X;
     int64_t ld_m, ld_t, T, t_offset;
+    const float *sc_m, *sc_t;      // TC path: exact power-of-two row scales of the operands (NULL = 1)
 };
 
 __device__ __forceinline__ uint32_t fr_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(FR_THREADS, 2) fft_reduce_kernel(const __grid_
         const int slot = kk & 1;
         const int tl = item / nmb, mb0 = (item - tl * nmb) * TB;
         const int64_t t = t0 + tl;
+        const float st = out.sc_t ? __ldg(out.sc_t + t) : 1.f;
         fr_mbar_wait(full + slot, (uint32_t)(kk >> 1) & 1u);
 
         // ---- stage: task q = tid + 256 i -> (row pair r = q / C4, column c4 = q % C4)
@@ -234,13 +236,15 @@ __global__ void __launch_bounds__(FR_THREADS, 2) fft_reduce_kernel(const __grid_
             const int64_t ml = mb0 + p;
             const bool valid = ml < mcv;
             const int64_t m = m0 + ml;
+            // PI / (s_m s_t): exact power-of-two rescale of the TC path's scaled operands
+            const float mul = PI / (((valid && out.sc_m) ? __ldg(out.sc_m + m) : 1.f) * st);
             if constexpr (MODE == MODE_LANDSCAPE) {
                 if (valid) {
                     float2 *dst = reinterpret_cast<float2 *>(out.X + m * out.ld_m + t * out.ld_t);
 #pragma unroll
                     for (int k2 = 0; k2 < N1; ++k2) {
                         const float2 z = w[j][brev(k2, clog2(N1))];
-                        dst[k1 + N2 * k2] = make_float2(PI * z.x, PI * z.y);
+                        dst[k1 + N2 * k2] = make_float2(mul * z.x, mul * z.y);
                     }
                 }
             } else {
@@ -251,7 +255,7 @@ __global__ void __launch_bounds__(FR_THREADS, 2) fft_reduce_kernel(const __grid_
                 for (int k2 = 0; k2 < N1; ++k2) mx = fmaxf(mx, fmaxf(w[j][k2].x, w[j][k2].y));
 #pragma unroll
                 for (int off = N2 / 2; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, off));
-                const float bv = PI * mx;
+                const float bv = mul * mx;
                 bool go = valid;
                 if constexpr (MODE == MODE_IMAGE) {
                     // filter against a possibly stale copy of the image's key: keys only grow, so a

@@ -1,32 +1,35 @@
 // rsvd_tc.cu -- tensor-core path of Step 2 (the q-batched complex contraction) on
-// sm_100a: tcgen05.mma kind::tf32 with 3xTF32 error compensation, plus the compact block layout it
-// consumes (written by compress) and the path selection.
+// sm_100a: tcgen05.mma kind::f16 on CTA pairs (cta_group::2, M = 256) with an fp16 hi/lo split of
+// both operands (error-compensated, ~fp32 accuracy), TMA-fed from operand rows that Step 1 (compress)
+// writes pre-expanded, plus the path selection.
 //
 // Real embedding of U_q[m,t] = sum_j alpha[q][j][m] beta[q][j][t] (alpha/beta: rsvd_compress.cu):
-// two A rows per image and one B row per template,
+// two A rows per image and one B row per template (K = 4H reals, j-interleaved),
 //   A_re[m] = (Re a_j, -Im a_j)_j ,  A_im[m] = (Im a_j, Re a_j)_j ,  B[t] = (Re b_j, Im b_j)_j
-//   D[m][t] = A_re . B = Re U ,  D[64 + m][t] = A_im . B = Im U.
-// Each fp32 operand x = hi + lo (both TF32-rounded); D = Ahi Bhi + Ahi Blo + Alo Bhi recovers ~fp32
-// accuracy (the dropped Alo Blo term is ~2^-22 relative).
+//   D[m][t] = A_re . B = Re U ,  D[64 + m][t] = A_im . B = Im U      (per CTA: 64 images).
+// Each row is scaled by an exact power of two s (row max in [2^13, 2^14)) and split
+// x s = hi + lo, hi = fp16(x s), lo = fp16(x s - hi); D = Ahi Bhi + Ahi Blo + Alo Bhi (fp32
+// accumulation in TMEM) carries ~2^-22 relative error per term.  The Step-3 kernel multiplies each
+// pair's result by 1 / (s_m s_t) (exact).
 //
-// Block layout (compact TC layout; same bytes as the SIMT layout): K-major rows of interleaved
-// complex fp32, 16 complex (128 B) per k-block row, pre-swizzled the way UMMA SWIZZLE_128B expects
-// (16-byte chunk c of row r stored at chunk c ^ (r & 7)):
-//   images    A[q][mtile][kb][64 rows][32 floats]    (mtile = 64 images, 8 KB per sub-tile)
-//   templates B[q][ttile][kb][256 rows][32 floats]   (ttile = 256 templates, 32 KB per sub-tile)
-// q = 0..N (N = Q/2), kb < KB = ceil(2H/16).  The in-shared-memory expansion to (Re, Im) rows and
-// hi/lo parts preserves the position of every 16-byte chunk (64 + r = r mod 8), so producers copy
-// chunk i of global to chunk i of shared memory with arithmetic only.
+// Operand layout (opaque; written by compress_tc_kernel), per side, fp16:
+//   op[q][kb][part][row][32],  q = 0..N (N = Q/2), kb < KB = ceil(4H/32), part 0 = hi, 1 = lo,
+//   image rows: image m -> rows (m/64)*128 + m%64 (A_re) and + 64 (A_im); 2 * round_up(M,128) rows;
+//   template rows: t; round_up(T,256) rows.  Then float scale[rows_pad] (s per image / template).
+// A 5-D tensor map (32 x rows x 2 x KB x (N+1)) with SWIZZLE_64B loads one (q, kb) box of 128 rows
+// x 32 fp16 x {hi,lo} (16 KB) straight into the UMMA K-major SW64 layout.
 //
-// contract_tc_kernel: one CTA per (64-image x 256-template tile, group of q), 13 warps:
-//   warp 0      TMEM allocator + MMA issuer: per stage 4 k-steps x 3 tcgen05.mma (M=128, N=256, K=8)
-//               into one of two 256-column TMEM accumulators; tcgen05.commit frees the smem stage /
-//               signals the epilogue;
-//   warps 1-4   epilogue: tcgen05.ld 32x32b of their 32 TMEM lanes; lanes 0-63 hold Re U, 64-127 Im U;
-//               stores to the planar spectrum workspace (re plane | im plane), releases the accumulator;
-//   warps 5-12  producers: LDG the compact (q, kb) sub-tiles (40 KB), expand to A hi/lo (2 x 16 KB) and
-//               B hi/lo (2 x 32 KB) in a 2-deep shared-memory ring, fence.proxy.async, arrive.
+// contract_tc_kernel: one CTA pair per (128-image x 256-template tile, group of q), 6 warps per CTA:
+//   warp 0    TMA producer (both CTAs: own 128 A rows + own half of the 256 B rows; completion on the
+//             leader's full barrier, expect_tx posted by the leader);
+//   warp 1    TMEM allocator (both) + MMA issuer (leader): per stage 3 x (1 or 2) tcgen05.mma
+//             256x256x16 into one of two 256-column accumulators, commits multicast to both CTAs;
+//   warps 2-5 epilogue (both): tcgen05.ld 32x32b of their lane quadrant (lanes 0-63 Re U, 64-127
+//             Im U), coalesced stores to the planar spectrum workspace, remote arrive on the
+//             leader's accumulator-empty barrier.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -36,36 +39,63 @@
 
 namespace rsvd {
 
-constexpr int TC_THREADS = 13 * 32;
-constexpr int TC_PROD_WARPS = 8;
-constexpr int TC_STAGES = 2;
-constexpr int TC_MT = 64;                           // images per tile
-constexpr int TC_TT = 256;                          // templates per tile
-constexpr uint32_t TC_A_BYTES = 128u * 128u;        // one of hi / lo: 128 rows x 128 B
-constexpr uint32_t TC_B_BYTES = 256u * 128u;
-constexpr uint32_t TC_STAGE_BYTES = 2 * TC_A_BYTES + 2 * TC_B_BYTES;    // 96 KB
+constexpr int TC_THREADS = 6 * 32;
+constexpr int TC_STAGES = 6;
+constexpr int TC_PIMG = 128;                        // images per CTA pair (64 per CTA)
+constexpr int TC_TT = 256;                          // templates per CTA pair (128 per CTA)
+constexpr uint32_t TC_PART_BYTES = 128u * 64u;      // 128 rows x 32 fp16
+constexpr uint32_t TC_OPND_BYTES = 2 * TC_PART_BYTES;
+constexpr uint32_t TC_STAGE_BYTES = 2 * TC_OPND_BYTES;    // A + B: 32 KB
 constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_BYTES + 1024 + 256;
 
-int tc_kb(int H) { return (int)((2 * (int64_t)H + 15) / 16); }
-int64_t tc_rows_pad_side(int64_t rows, int side) { return round_up(rows, side == RSVD_SIDE_TEMPLATE ? TC_TT : TC_MT); }
+int tc_kb(int H) { return (H + 7) / 8; }                    // 32-element k-blocks of K = 4H
+static int tc_steps(int H) { return (4 * H + 15) / 16; }    // K = 16 MMA steps
+int64_t tc_rows_pad_side(int64_t rows, int side) { return round_up(rows, side == RSVD_SIDE_TEMPLATE ? TC_TT : TC_PIMG); }
 int64_t tc_rows_pad(int64_t rows) { return round_up(rows, 256); }
+static int64_t tc_op_rows(int64_t rows, int side) {
+    return side == RSVD_SIDE_TEMPLATE ? round_up(rows, TC_TT) : 2 * round_up(rows, TC_PIMG);
+}
+static int64_t tc_op_bytes(int64_t rows, int Q, int H, int side) {
+    return (int64_t)(Q / 2 + 1) * tc_kb(H) * 2 * tc_op_rows(rows, side) * 64;
+}
 int64_t tc_block_bytes(int64_t rows, int Q, int H, int side) {
-    return (int64_t)(Q / 2 + 1) * tc_kb(H) * tc_rows_pad_side(rows, side) * 128;
+    return tc_op_bytes(rows, Q, H, side) + round_up(tc_rows_pad_side(rows, side) * 4, 256);
+}
+const float *tc_scales(const void *blocks, int64_t rows, int Q, int H, int side) {
+    return reinterpret_cast<const float *>(reinterpret_cast<const char *>(blocks) + tc_op_bytes(rows, Q, H, side));
 }
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+// UMMA shared-memory descriptor, K-major, SWIZZLE_64B: 8-row atoms of 64-byte rows, 512 B apart.
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr & 0x3FFFF) >> 4);          // start address
     d |= (uint64_t)1 << 16;                           // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;                 // SBO: 8-row atoms 1024 B apart
+    d |= (uint64_t)(512 >> 4) << 32;                  // SBO: 8-row atoms 512 B apart
     d |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
+    d |= (uint64_t)4 << 61;                           // SWIZZLE_64B
     return d;
 }
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// teardown rendezvous: only execution order matters (TMEM dealloc after the peer's last use)
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
 __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
 }
@@ -81,23 +111,43 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
             : "memory");
     }
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
-    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b)) : "memory");
+// Relaxed arrive: the accumulator-empty signal only orders the preceding tcgen05.ld's (via
+// tcgen05.fence::before_thread_sync), not the epilogue's global stores -- a release here would wait
+// for every outstanding store of the q before the MMA may reuse the accumulator.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_5d_pair(uint32_t dst, const CUtensorMap *tm, int c0, int c1, int c2, int c3,
+                                                 int c4, uint32_t mbar_cluster) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(mbar_cluster)
+        : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_mma_tf32(uint32_t dtmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void tc_mma_f16_pair(uint32_t dtmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dtmem),
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dtmem),
         "l"(da), "l"(db), "r"(idesc), "r"(acc)
         : "memory");
 }
-__device__ __forceinline__ void tc_commit(uint64_t *bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
+// arrive (once per CTA) on the barrier at this smem offset in both CTAs of the pair when all
+// previously issued MMAs have completed
+__device__ __forceinline__ void tc_commit_pair(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
 }
+// tcgen05.ld of 32 consecutive columns of this warp's 32 lanes (asynchronous: tmem_wait_ld before use)
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -107,29 +157,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
           "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
           "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-
-__device__ __forceinline__ float tf32_rna(float x) {       // hardware round-to-TF32 (one instruction)
-    uint32_t u;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
-    return __uint_as_float(u);
-}
-// x = hi + lo exactly (hi TF32-rounded; lo = x - hi has <= 13 significant bits and is fed as fp32:
-// the tensor core keeps its top 11, an error <= 2^-22 |x|).
-__device__ __forceinline__ void split4(float4 v, float4 &hi, float4 &lo) {
-    hi.x = tf32_rna(v.x); lo.x = v.x - hi.x;
-    hi.y = tf32_rna(v.y); lo.y = v.y - hi.y;
-    hi.z = tf32_rna(v.z); lo.z = v.z - hi.z;
-    hi.w = tf32_rna(v.w); lo.w = v.w - hi.w;
-}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ------------------------------------------------------------------ contraction kernel
-// grid: ntiles_chunk * nqg; chunk tiles (Mc/64) x (Tc/256); item -> (tile, q-group).
-// Upk planar: re plane [(n*Mc + ml)*Tc + tl], im plane at + N*Mc*Tc (floats).
-__global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
-    const float *__restrict__ Acmp, const float *__restrict__ Bcmp, int KB, int N, int64_t MT, int64_t NT,
-    int64_t mt0, int64_t nt0, int ntl, int qg, int nqg, int64_t Mc, int64_t Tc, float *__restrict__ Upk) {
+// Items (tile, q-group) of one chunk, tile = (128-image tile mt_l < mtl, 256-template tile nt_l < ntl);
+// cluster c processes items c, c + nclusters, ...  Upk planar: re plane [(n*Tc + tl)*Mc + ml], im
+// plane at + N*Mc*Tc (floats); slot n = 0 packs (U_0, U_N).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
+    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int steps, int KB, int N,
+    int mtl, int ntl, int mt0, int nt0, int qg, int nqg, int nitems, int64_t Mc, int64_t Tc,
+    float *__restrict__ Upk) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint64_t *bars = reinterpret_cast<uint64_t *>(base + TC_STAGES * TC_STAGE_BYTES);
@@ -137,190 +175,186 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * TC_STAGES + 4);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int item = blockIdx.x;
-    const int tile = item / nqg, qgi = item % nqg;
-    const int mt_l = tile / ntl, nt_l = tile % ntl;
-    const int64_t mt = mt0 + mt_l, nt = nt0 + nt_l;
-    const int q_begin = qgi * qg;
-    const int q_end = min(N + 1, q_begin + qg);
-    const int nqi = max(0, q_end - q_begin);
+    const uint32_t rank = cluster_rank();
+    const int cl = (int)(blockIdx.x >> 1), ncl = (int)(gridDim.x >> 1);
 
-    if (warp == 0) {
-        if (lane == 0) {
-            for (int s = 0; s < TC_STAGES; ++s) { mbar_init(full + s, TC_PROD_WARPS); mbar_init(empty + s, 1); }
-            for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 4); }
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncwarp();
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 8); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- MMA issuer
+        // ---------------- TMA producer (both CTAs)
         if (lane == 0) {
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
-                                   ((uint32_t)(128 >> 4) << 24);
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
             int it = 0;
-            for (int qi = 0; qi < nqi; ++qi) {
-                const int acc = qi & 1;
-                mbar_wait(tempty + acc, (((uint32_t)qi >> 1) & 1u) ^ 1u);
-                tc_fence_after();
-                const uint32_t dt = tmem + (uint32_t)(acc * 256);
-                for (int kb = 0; kb < KB; ++kb, ++it) {
-                    const int s = it % TC_STAGES;
-                    mbar_wait(full + s, (uint32_t)(it / TC_STAGES) & 1u);
-                    tc_fence_after();
-                    const uint32_t sa = smem_u32(base + s * TC_STAGE_BYTES);
-                    const uint64_t a_hi = sw128_desc(sa), a_lo = sw128_desc(sa + TC_A_BYTES);
-                    const uint64_t b_hi = sw128_desc(sa + 2 * TC_A_BYTES), b_lo = sw128_desc(sa + 2 * TC_A_BYTES + TC_B_BYTES);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint64_t o = (uint64_t)(2 * k);          // +32 B per K=8 tf32 step
-                        tc_mma_tf32(dt, a_hi + o, b_hi + o, idesc, (kb | k) ? 1u : 0u);
-                        tc_mma_tf32(dt, a_hi + o, b_lo + o, idesc, 1u);
-                        tc_mma_tf32(dt, a_lo + o, b_hi + o, idesc, 1u);
+            for (int item = cl; item < nitems; item += ncl) {
+                const int tile = item / nqg, qgi = item - tile * nqg;
+                const int mt_l = tile / ntl, nt_l = tile - mt_l * ntl;
+                const int q_begin = qgi * qg, q_end = min(N + 1, q_begin + qg);
+                const int rowA = (mt0 + mt_l) * 2 * TC_PIMG + (int)rank * 128;
+                const int rowB = (nt0 + nt_l) * TC_TT + (int)rank * 128;
+                for (int q = q_begin; q < q_end; ++q) {
+                    for (int kb = 0; kb < KB; ++kb, ++it) {
+                        const int s = it % TC_STAGES;
+                        mbar_wait(empty + s, ((uint32_t)(it / TC_STAGES) & 1u) ^ 1u);
+                        const uint32_t fb = smem_u32(full + s);
+                        if (rank == 0) mbar_expect_tx(full + s, 2 * TC_STAGE_BYTES);
+                        const uint32_t fbl = rank == 0 ? fb : mapa_rank(fb, 0);
+                        const uint32_t dst = smem_u32(base + s * TC_STAGE_BYTES);
+                        tma_load_5d_pair(dst, &tmA, 0, rowA, 0, kb, q, fbl);
+                        tma_load_5d_pair(dst + TC_OPND_BYTES, &tmB, 0, rowB, 0, kb, q, fbl);
                     }
-                    tc_commit(empty + s);          // stage free once these MMAs complete
                 }
-                tc_commit(tfull + acc);            // accumulator ready for the epilogue
+            }
+            // drain: the last MMA commit of every stage has arrived here before the CTA may exit
+            for (int k = 0; k < TC_STAGES && k < it; ++k) {
+                const int j = it - 1 - k;
+                mbar_wait(empty + (j % TC_STAGES), (uint32_t)(j / TC_STAGES) & 1u);
             }
         }
-    } else if (warp <= 4) {
-        // ---------------- epilogue
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (leader CTA)
+        if (rank == 0 && lane == 0) {
+            const uint32_t idesc = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+            int it = 0, qi = 0;
+            for (int item = cl; item < nitems; item += ncl) {
+                const int qgi = item % nqg;
+                const int q_begin = qgi * qg, q_end = min(N + 1, q_begin + qg);
+                for (int q = q_begin; q < q_end; ++q, ++qi) {
+                    const int acc = qi & 1;
+                    mbar_wait(tempty + acc, (((uint32_t)qi >> 1) & 1u) ^ 1u);
+                    tc_fence_after();
+                    const uint32_t dt = tmem + (uint32_t)(acc * 256);
+                    for (int kb = 0; kb < KB; ++kb, ++it) {
+                        const int s = it % TC_STAGES;
+                        mbar_wait(full + s, (uint32_t)(it / TC_STAGES) & 1u);
+                        tc_fence_after();
+                        const uint32_t sa = smem_u32(base + s * TC_STAGE_BYTES);
+                        const uint64_t a_hi = sw64_desc(sa), a_lo = sw64_desc(sa + TC_PART_BYTES);
+                        const uint64_t b_hi = sw64_desc(sa + TC_OPND_BYTES), b_lo = sw64_desc(sa + TC_OPND_BYTES + TC_PART_BYTES);
+                        const int nst = min(2, steps - 2 * kb);
+                        for (int k = 0; k < nst; ++k) {
+                            const uint64_t o = (uint64_t)(2 * k);          // +32 B per K=16 fp16 step
+                            tc_mma_f16_pair(dt, a_hi + o, b_hi + o, idesc, (kb | k) ? 1u : 0u);
+                            tc_mma_f16_pair(dt, a_hi + o, b_lo + o, idesc, 1u);
+                            tc_mma_f16_pair(dt, a_lo + o, b_hi + o, idesc, 1u);
+                        }
+                        tc_commit_pair(empty + s);       // both CTAs' stage s free once these complete
+                    }
+                    tc_commit_pair(tfull + acc);          // accumulator ready in both CTAs
+                }
+            }
+        }
+    } else {
+        // ---------------- epilogue (both CTAs)
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
         const int row = quad * 32 + lane;
         const bool re_rows = row < 64;
-        const int64_t ml = (int64_t)mt_l * TC_MT + (row & 63);
         float *const plane_re = Upk, *const plane_im = Upk + (int64_t)N * Mc * Tc;
-        for (int qi = 0; qi < nqi; ++qi) {
-            const int acc = qi & 1;
-            mbar_wait(tfull + acc, ((uint32_t)qi >> 1) & 1u);
-            tc_fence_after();
-            const int q = q_begin + qi;
-            // q = 0: Re U_0 -> re plane slot 0; q = N: Re U_N -> im plane slot 0; Im rows of both dropped
-            const bool store = (q != 0 && q != N) || re_rows;
-            float *plane = (q == N) ? plane_im : ((q == 0 || re_rows) ? plane_re : plane_im);
-            const int n = (q == N) ? 0 : q;
-            // workspace [n][t][m]: the 32 lanes hold 32 consecutive images -> each store is one 128-B line
-            float *dst = plane + ((int64_t)n * Tc + (int64_t)nt_l * TC_TT) * Mc + ml;
-            const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256);
-#pragma unroll 1
-            for (int c0 = 0; c0 < 256; c0 += 32) {
-                uint32_t v[32];
-                tmem_ld32(tbase + (uint32_t)c0, v);
-                if (store) {
+        const uint32_t te0 = rank == 0 ? smem_u32(tempty) : mapa_rank(smem_u32(tempty), 0);
+        int qi = 0;
+        for (int item = cl; item < nitems; item += ncl) {
+            const int tile = item / nqg, qgi = item - tile * nqg;
+            const int mt_l = tile / ntl, nt_l = tile - mt_l * ntl;
+            const int q_begin = qgi * qg, q_end = min(N + 1, q_begin + qg);
+            const int64_t ml = (int64_t)mt_l * TC_PIMG + rank * 64 + (row & 63);
+            for (int q = q_begin; q < q_end; ++q, ++qi) {
+                const int acc = qi & 1;
+                mbar_wait(tfull + acc, ((uint32_t)qi >> 1) & 1u);
+                tc_fence_after();
+                // q = 0: Re U_0 -> re plane slot 0; q = N: Re U_N -> im plane slot 0; Im rows of both dropped
+                const bool store = (q != 0 && q != N) || re_rows;
+                float *plane = (q == N) ? plane_im : ((q == 0 || re_rows) ? plane_re : plane_im);
+                const int n = (q == N) ? 0 : q;
+                // workspace [n][t][m]: the 32 lanes hold 32 consecutive images -> each store is one 128-B line
+                float *dst = plane + ((int64_t)n * Tc + (int64_t)nt_l * TC_TT) * Mc + ml;
+                const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256);
+                // 64-column batches, the next batch's TMEM loads in flight while this one is stored
+                uint32_t v[2][2][32];
+                tmem_ld32(tbase, v[0][0]);
+                tmem_ld32(tbase + 32, v[0][1]);
+                tmem_wait_ld();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) dst[(int64_t)(c0 + i) * Mc] = __uint_as_float(v[i]);
+                for (int b = 0; b < 4; ++b) {
+                    const int cur = b & 1;
+                    if (b < 3) {
+                        tmem_ld32(tbase + (uint32_t)(64 * b + 64), v[cur ^ 1][0]);
+                        tmem_ld32(tbase + (uint32_t)(64 * b + 96), v[cur ^ 1][1]);
+                    }
+                    if (store) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                dst[(int64_t)(64 * b + 32 * h + i) * Mc] = __uint_as_float(v[cur][h][i]);
+                    }
+                    tmem_wait_ld();
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(te0 + (uint32_t)(acc * 8));
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty + acc);
-        }
-    } else {
-        // ---------------- producers: global compact tiles -> expanded hi/lo operand stages
-        // Register ping-pong: the loads of stage it+1 are in flight while stage it waits for its smem
-        // slot and is expanded, so one global-load latency is hidden per stage.
-        const int pt = tid - 5 * 32;               // 0..255
-        const int total = nqi * KB;
-        auto load = [&](int it, float4 (&ra)[2], float4 (&rb)[8]) {
-            const int q = q_begin + it / KB, kb = it % KB;
-            const float4 *gA = reinterpret_cast<const float4 *>(
-                Acmp + (((int64_t)q * MT + mt) * KB + kb) * (int64_t)(TC_MT * 32));
-            const float4 *gB = reinterpret_cast<const float4 *>(
-                Bcmp + (((int64_t)q * NT + nt) * KB + kb) * (int64_t)(TC_TT * 32));
-#pragma unroll
-            for (int i = 0; i < 2; ++i) ra[i] = __ldg(gA + pt + 256 * i);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) rb[i] = __ldg(gB + pt + 256 * i);
-        };
-        auto expand = [&](int it, const float4 (&ra)[2], const float4 (&rb)[8]) {
-            const int s = it % TC_STAGES;
-            mbar_wait(empty + s, ((uint32_t)(it / TC_STAGES) & 1u) ^ 1u);
-            float4 *sAhi = reinterpret_cast<float4 *>(base + s * TC_STAGE_BYTES);
-            float4 *sAlo = sAhi + TC_A_BYTES / 16;
-            float4 *sBhi = sAlo + TC_A_BYTES / 16;
-            float4 *sBlo = sBhi + TC_B_BYTES / 16;
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const int idx = pt + 256 * i;               // image row idx/8, chunk position idx%8
-                float4 hi, lo;
-                split4(ra[i], hi, lo);
-                sAhi[idx] = make_float4(hi.x, -hi.y, hi.z, -hi.w);     // A_re row: (Re a, -Im a)
-                sAlo[idx] = make_float4(lo.x, -lo.y, lo.z, -lo.w);
-                sAhi[512 + idx] = make_float4(hi.y, hi.x, hi.w, hi.z); // A_im row (row + 64, same chunk)
-                sAlo[512 + idx] = make_float4(lo.y, lo.x, lo.w, lo.z);
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int idx = pt + 256 * i;
-                float4 hi, lo;
-                split4(rb[i], hi, lo);
-                sBhi[idx] = hi;
-                sBlo[idx] = lo;
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(full + s);
-        };
-        // L2 prefetch of the compact sub-tiles PF stages ahead (one bulk prefetch per operand), so the
-        // ping-pong loads hit L2 instead of DRAM.
-        constexpr int PF = 4;
-        auto prefetch = [&](int it) {
-            if (pt != 0 || it >= total) return;
-            const int q = q_begin + it / KB, kb = it % KB;
-            const float *gA = Acmp + (((int64_t)q * MT + mt) * KB + kb) * (int64_t)(TC_MT * 32);
-            const float *gB = Bcmp + (((int64_t)q * NT + nt) * KB + kb) * (int64_t)(TC_TT * 32);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gA), "r"((uint32_t)(TC_MT * 128)) : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gB), "r"((uint32_t)(TC_TT * 128)) : "memory");
-        };
-        for (int it = 1; it < PF; ++it) prefetch(it);
-        float4 ra0[2], rb0[8], ra1[2], rb1[8];
-        if (total > 0) load(0, ra0, rb0);
-        for (int it = 0; it < total; it += 2) {
-            prefetch(it + PF);
-            if (it + 1 < total) load(it + 1, ra1, rb1);
-            expand(it, ra0, rb0);
-            if (it + 1 >= total) break;
-            prefetch(it + 1 + PF);
-            if (it + 2 < total) load(it + 2, ra0, rb0);
-            expand(it + 1, ra1, rb1);
         }
     }
     tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
+    cluster_sync_relaxed();
+    if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
 }
 
-// ------------------------------------------------------------------ compact TC block emission (Step 1 tail)
-// Emits the compact TC rows of one row (image or template) from its coefficients at[h][q] (smem,
-// [H][Q]); 8 lanes write one 128-byte swizzled row (one 16-byte chunk each).
-__device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, int64_t row, int64_t ntiles,
-                             float *__restrict__ blocks) {
-    const int N = Q / 2;
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    const int ch = tid & 7;
-    const int rows_tile = side == RSVD_SIDE_TEMPLATE ? TC_TT : TC_MT;
-    const int64_t tile = row / rows_tile;
-    const int r = (int)(row % rows_tile);
-    const int total = (N + 1) * KB;
-    for (int idx = tid >> 3; idx < total; idx += nthr >> 3) {
-        const int kb = idx % KB;
-        const int q = idx / KB;
-        float4 v;
-        float2 c2[2];
+// ------------------------------------------------------------------ TC operand emission (Step 1 tail)
+// From the coefficients at[h][q] (smem, [H][Q]) of one row: the exact power-of-two row scale s
+// (max |Re|,|Im| of the stored values times s in [2^13, 2^14)), then the hi/lo fp16 operand rows.
+__device__ float row_scale(const float2 *at, int count, float *red) {
+    float mx = 0.f;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) mx = fmaxf(mx, fmaxf(fabsf(at[i].x), fabsf(at[i].y)));
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-            const int j = kb * 16 + ch * 2 + jj;              // complex index of alpha/beta
+    for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+        if (threadIdx.x == 0) red[32] = v;
+    }
+    __syncthreads();
+    const float m = red[32];
+    if (!(m > 0.f) || !isfinite(m)) return 1.f;
+    return ldexpf(1.f, 13 - ilogbf(m));
+}
+
+__device__ __forceinline__ void split_h(float x, __half &hi, __half &lo) {
+    hi = __float2half_rn(x);
+    lo = __float2half_rn(x - __half2float(hi));
+}
+
+__device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, int64_t row, int64_t op_rows,
+                             float s, __half *__restrict__ ops) {
+    const int N = Q / 2;
+    const int total = (N + 1) * KB * 4;                 // (q, kb, quarter of the 32-element k-block)
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const int qu = idx & 3;
+        const int kb = (idx >> 2) % KB;
+        const int q = (idx >> 2) / KB;
+        float2 c[4];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int j = kb * 16 + qu * 4 + jj;          // complex index of alpha/beta
             float2 a = make_float2(0.f, 0.f);
             if (j < H) {
                 a = at[j * Q + q];
@@ -329,19 +363,38 @@ __device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, i
                 a = at[(j - H) * Q + ((Q - q) & (Q - 1))];
                 if (side == RSVD_SIDE_TEMPLATE) a = c_conj(a);
             }
-            c2[jj] = a;
+            c[jj] = make_float2(a.x * s, a.y * s);
         }
-        v = make_float4(c2[0].x, c2[0].y, c2[1].x, c2[1].y);
-        const int64_t sub = ((int64_t)q * ntiles + tile) * KB + kb;
-        *reinterpret_cast<float4 *>(blocks + (sub * rows_tile + r) * 32 + ((ch ^ (r & 7)) * 4)) = v;
+        const int64_t sub = ((int64_t)q * KB + kb) * 2;   // (q, kb, part 0)
+        if (side == RSVD_SIDE_TEMPLATE) {
+            __align__(16) __half hi[8], lo[8];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) { split_h(c[jj].x, hi[2 * jj], lo[2 * jj]); split_h(c[jj].y, hi[2 * jj + 1], lo[2 * jj + 1]); }
+            *reinterpret_cast<uint4 *>(ops + ((sub + 0) * op_rows + row) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(hi);
+            *reinterpret_cast<uint4 *>(ops + ((sub + 1) * op_rows + row) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(lo);
+        } else {
+            const int64_t rre = (row / 64) * 128 + row % 64, rim = rre + 64;
+            __align__(16) __half rh[8], rl[8], ih[8], il[8];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                split_h(c[jj].x, rh[2 * jj], rl[2 * jj]);            // A_re = (Re a, -Im a)
+                split_h(-c[jj].y, rh[2 * jj + 1], rl[2 * jj + 1]);
+                split_h(c[jj].y, ih[2 * jj], il[2 * jj]);            // A_im = (Im a, Re a)
+                split_h(c[jj].x, ih[2 * jj + 1], il[2 * jj + 1]);
+            }
+            *reinterpret_cast<uint4 *>(ops + ((sub + 0) * op_rows + rre) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(rh);
+            *reinterpret_cast<uint4 *>(ops + ((sub + 1) * op_rows + rre) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(rl);
+            *reinterpret_cast<uint4 *>(ops + ((sub + 0) * op_rows + rim) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(ih);
+            *reinterpret_cast<uint4 *>(ops + ((sub + 1) * op_rows + rim) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(il);
+        }
     }
 }
 
 template <int LOGQ>
 __global__ void __launch_bounds__(256) compress_tc_kernel(const float2 *__restrict__ rings, int64_t n, int R,
                                                           const double *__restrict__ w, const double *__restrict__ U,
-                                                          int H, int side, int KB, int64_t ntiles,
-                                                          float *__restrict__ blocks) {
+                                                          int H, int side, int KB, int64_t op_rows,
+                                                          __half *__restrict__ ops, float *__restrict__ scales) {
     constexpr int Q = 1 << LOGQ;
     constexpr int L = 32;
     constexpr int E = Q / L;
@@ -350,6 +403,7 @@ __global__ void __launch_bounds__(256) compress_tc_kernel(const float2 *__restri
     float2 *tw = reinterpret_cast<float2 *>(smem_raw);       // [E][L]
     float2 *at = tw + E * L;                                 // [H][Q]
     float *up = reinterpret_cast<float *>(at + (size_t)H * Q);   // [R][HC]
+    float *red = up + (size_t)R * HC;                        // [33]
     const int64_t row = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < E * L; i += 256) tw[i] = twiddle_N(i % L, i / L, Q);
@@ -399,11 +453,13 @@ __global__ void __launch_bounds__(256) compress_tc_kernel(const float2 *__restri
         for (int k1 = 0; k1 < E; ++k1) at[h * Q + k1 + E * b] = v[brev(k1, clog2(E))];
     }
     __syncthreads();
-    emit_tc_rows(at, H, Q, KB, side, row, ntiles, blocks);
+    const float s = row_scale(at, H * Q, red);
+    if (tid == 0) scales[row] = s;
+    emit_tc_rows(at, H, Q, KB, side, row, op_rows, s, ops);
 }
 
 size_t compress_tc_smem(int Q, int H, int R) {
-    return (size_t)Q * sizeof(float2) + (size_t)H * Q * sizeof(float2) + (size_t)R * 16 * sizeof(float);
+    return (size_t)Q * sizeof(float2) + (size_t)H * Q * sizeof(float2) + (size_t)R * 16 * sizeof(float) + 33 * 4;
 }
 
 // TC layout needs the whole [H][Q] coefficient block of a row in shared memory (R <= 256).
@@ -424,12 +480,14 @@ void set_path(int p) { g_path = (p == PATH_SIMT || p == PATH_TC) ? p : PATH_AUTO
 
 template <int LOGQ>
 static cudaError_t launch_compress_tc_q(const float2 *rings, int64_t n, int R, const double *w, const double *U, int H,
-                                        int side, float *blocks, cudaStream_t s) {
+                                        int side, void *blocks, cudaStream_t s) {
     const size_t smem = compress_tc_smem(1 << LOGQ, H, R);
     cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel<LOGQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int64_t ntiles = tc_rows_pad_side(n, side) / (side == RSVD_SIDE_TEMPLATE ? TC_TT : TC_MT);
-    compress_tc_kernel<LOGQ><<<(unsigned)n, 256, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H), ntiles, blocks);
+    const int Q = 1 << LOGQ;
+    float *scales = const_cast<float *>(tc_scales(blocks, n, Q, H, side));
+    compress_tc_kernel<LOGQ><<<(unsigned)n, 256, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H), tc_op_rows(n, side),
+                                                            reinterpret_cast<__half *>(blocks), scales);
     return cudaGetLastError();
 }
 
@@ -445,9 +503,9 @@ cudaError_t launch_compress_tc(const float2 *rings, int64_t n, int R, int Q, con
     }
 }
 
-// canonical coefficients from compact TC blocks, test / debug path
-__global__ void unpack_tc_kernel(const float *__restrict__ blocks, int64_t n, int Q, int H, int side, int KB,
-                                 int64_t ntiles, float2 *__restrict__ coeffs) {
+// canonical coefficients from the TC operand rows (hi + lo) / s, test / debug path
+__global__ void unpack_tc_kernel(const __half *__restrict__ ops, const float *__restrict__ scales, int64_t n, int Q,
+                                 int H, int side, int KB, int64_t op_rows, float2 *__restrict__ coeffs) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * (int64_t)Q * H) return;
     const int h = (int)(idx % H);
@@ -456,12 +514,15 @@ __global__ void unpack_tc_kernel(const float *__restrict__ blocks, int64_t n, in
     const int N = Q / 2;
     const int qq = q <= N ? q : Q - q;
     const int j = q <= N ? h : H + h;
-    const int kb = j / 16, ch = (j % 16) / 2, jj = j % 2;
-    const int rows_tile = side == RSVD_SIDE_TEMPLATE ? TC_TT : TC_MT;
-    const int r = (int)(row % rows_tile);
-    const int64_t sub = ((int64_t)qq * ntiles + row / rows_tile) * KB + kb;
-    const int64_t off = (sub * rows_tile + r) * 32 + (int64_t)((ch ^ (r & 7)) * 4) + 2 * jj;
-    float2 v = make_float2(blocks[off], blocks[off + 1]);          // alpha_j / beta_j
+    const int kb = j / 16, e = 2 * (j % 16);
+    const int64_t r = side == RSVD_SIDE_TEMPLATE ? row : (row / 64) * 128 + row % 64;
+    const int64_t sub = ((int64_t)qq * KB + kb) * 2;
+    const __half *hi = ops + (sub * op_rows + r) * 32 + e;
+    const __half *lo = ops + ((sub + 1) * op_rows + r) * 32 + e;
+    const float inv = 1.f / scales[row];
+    float x = (__half2float(hi[0]) + __half2float(lo[0])) * inv;
+    float y = (__half2float(hi[1]) + __half2float(lo[1])) * inv;
+    float2 v = side == RSVD_SIDE_TEMPLATE ? make_float2(x, y) : make_float2(x, -y);   // alpha / beta_j
     if (q <= N) { if (side == RSVD_SIDE_IMAGE) v = c_conj(v); }
     else { if (side == RSVD_SIDE_TEMPLATE) v = c_conj(v); }
     coeffs[idx] = v;
@@ -469,31 +530,66 @@ __global__ void unpack_tc_kernel(const float *__restrict__ blocks, int64_t n, in
 
 cudaError_t launch_unpack_tc(const float *blocks, int64_t n, int Q, int H, int side, float2 *coeffs, cudaStream_t s) {
     const int64_t total = n * (int64_t)Q * H;
-    const int64_t ntiles = tc_rows_pad_side(n, side) / (side == RSVD_SIDE_TEMPLATE ? TC_TT : TC_MT);
-    unpack_tc_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(blocks, n, Q, H, side, tc_kb(H), ntiles, coeffs);
+    unpack_tc_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<const __half *>(blocks), tc_scales(blocks, n, Q, H, side), n, Q, H, side, tc_kb(H),
+        tc_op_rows(n, side), coeffs);
     return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ contraction launch (one chunk)
-cudaError_t launch_contract_tc(const float *Acmp, const float *Bcmp, int H, int N, int64_t Mpad, int64_t Tpad,
-                               int64_t m0, int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk,
-                               cudaStream_t s) {
+// ------------------------------------------------------------------ tensor maps + launch
+typedef CUresult (*PFN_encodeTiled_tc)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                       const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled_tc encode_fn() {
+    static PFN_encodeTiled_tc fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled_tc>(p);
+    }
+    return fn;
+}
+
+// 5-D map of one side's operand rows: (k 32, row, part 2, kb, q), box (32, 128, 2, 1, 1), SWIZZLE_64B.
+cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t rows, int Q, int H, int side) {
+    PFN_encodeTiled_tc enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    const int64_t op_rows = tc_op_rows(rows, side);
+    const int KB = tc_kb(H);
+    const cuuint64_t dims[5] = {32, (cuuint64_t)op_rows, 2, (cuuint64_t)KB, (cuuint64_t)(Q / 2 + 1)};
+    const cuuint64_t strides[4] = {64, (cuuint64_t)op_rows * 64, (cuuint64_t)op_rows * 128,
+                                   (cuuint64_t)op_rows * 128 * KB};
+    const cuuint32_t box[5] = {32, 128, 2, 1, 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void *>(blocks), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// One chunk: images [m0, m0 + mc) (multiples of 128), templates [t0, t0 + tc) (multiples of 256).
+cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int64_t m0, int64_t t0,
+                               int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(contract_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const int KB = tc_kb(H);
-    const int mtl = (int)(mc / TC_MT), ntl = (int)(tc / TC_TT);
+    const int mtl = (int)(mc / TC_PIMG), ntl = (int)(tc / TC_TT);
     const int ntiles = mtl * ntl;
-    const int target = 148;
+    const int target = std::max(1, nsms / 2);
     int nqg = std::max(1, (target + ntiles - 1) / ntiles);
     nqg = std::min(nqg, N + 1);
     const int qg = (N + 1 + nqg - 1) / nqg;
     nqg = (N + 1 + qg - 1) / qg;
-    contract_tc_kernel<<<(unsigned)(ntiles * nqg), TC_THREADS, TC_SMEM, s>>>(
-        Acmp, Bcmp, KB, N, Mpad / TC_MT, Tpad / TC_TT, m0 / TC_MT, t0 / TC_TT, ntl, qg, nqg, Mc, Tc, Upk);
+    const int nitems = ntiles * nqg;
+    const int ncl = std::min(nitems, target);
+    contract_tc_kernel<<<(unsigned)(2 * ncl), TC_THREADS, TC_SMEM, s>>>(
+        tmA, tmB, tc_steps(H), tc_kb(H), N, mtl, ntl, (int)(m0 / TC_PIMG), (int)(t0 / TC_TT), qg, nqg, nitems, Mc, Tc,
+        Upk);
     return cudaGetLastError();
 }
 

@@ -43,19 +43,21 @@ def test_sizes(lib):
         assert api.block_bytes(1, 32, 1) == 17 * 16 * 64 * 8
         api.set_path(api.PATH_TC)
         assert api.path_for(512, 24) == api.PATH_TC
-        # compact TC layout: (N+1) q x KB = ceil(2H/16) k-block rows of 128 B; images padded to 64,
-        # templates to 256 rows
-        assert api.block_bytes(16384, 512, 24, api.SIDE_IMAGE) == 257 * 3 * 16384 * 128
-        assert api.block_bytes(8192, 512, 24, api.SIDE_TEMPLATE) == 257 * 3 * 8192 * 128
-        assert api.block_bytes(10, 64, 4, api.SIDE_TEMPLATE) == 33 * 1 * 256 * 128
+        # TC layout: (N+1) q x KB = ceil(4H/32) k-blocks x {hi, lo} x operand rows of 32 fp16 (64 B);
+        # images: 2 rows (Re, Im embedding) per image, padded to 128 images; templates padded to 256;
+        # then one float scale per padded row, rounded up to 256 B
+        assert api.block_bytes(16384, 512, 24, api.SIDE_IMAGE) == 257 * 3 * 2 * 32768 * 64 + 16384 * 4
+        assert api.block_bytes(8192, 512, 24, api.SIDE_TEMPLATE) == 257 * 3 * 2 * 8192 * 64 + 8192 * 4
+        assert api.block_bytes(10, 64, 4, api.SIDE_TEMPLATE) == 33 * 1 * 2 * 256 * 64 + 1024
+        assert api.block_bytes(10, 64, 4, api.SIDE_IMAGE) == 33 * 1 * 2 * 256 * 64 + 512
         assert api.path_for(1024, 256) == api.PATH_SIMT        # H x Q block too large for the TC compress
     finally:
         api.set_path(api.PATH_AUTO)
     assert api.path_for(512, 24) == api.PATH_TC
     assert api.kernel_chunk() == 32
     assert api.kernel_partials_bytes(8192, 128) == 256 * 128 * 128 * 8
-    assert api.align_min_workspace_bytes(512) == 128 * 128 * 256 * 8
-    assert lib.rsvd_abi_version() == 2
+    assert api.align_min_workspace_bytes(512) == 128 * 256 * 256 * 8
+    assert lib.rsvd_abi_version() == 3
 
 
 def test_eigen_solver_matches_lapack(lib):
