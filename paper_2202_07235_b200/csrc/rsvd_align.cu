@@ -18,6 +18,7 @@
 
 #include "rsvd_common.cuh"
 #include "rsvd_fft.cuh"
+#include "rsvd_fft2.cuh"
 
 namespace rsvd {
 
@@ -137,7 +138,23 @@ struct AlignArgs {
     int64_t ld_m, ld_t;
 };
 
+// Steps 3-4 kernel: fft2 (rsvd_fft2.cuh) for N = Q/2 <= 256, the original schedule (rsvd_fft.cuh)
+// for N = 512 or when RSVD_FFT_V1=1 (kept for comparison).
+static bool use_fft2(int LOGN) {
+    static const int v1 = [] { const char *e = getenv("RSVD_FFT_V1"); return e ? atoi(e) : 0; }();
+    return LOGN <= 8 && !v1;
+}
+
 static cudaError_t make_tmap_any(int LOGN, CUtensorMap *tm, const float *Upk, int64_t Mc, int64_t Tc) {
+    if (use_fft2(LOGN)) {
+        switch (LOGN) {
+            case 4: return make_spectrum_tmap2<4>(tm, Upk, Mc, Tc);
+            case 5: return make_spectrum_tmap2<5>(tm, Upk, Mc, Tc);
+            case 6: return make_spectrum_tmap2<6>(tm, Upk, Mc, Tc);
+            case 7: return make_spectrum_tmap2<7>(tm, Upk, Mc, Tc);
+            default: return make_spectrum_tmap2<8>(tm, Upk, Mc, Tc);
+        }
+    }
     switch (LOGN) {
         case 4: return make_spectrum_tmap<4>(tm, Upk, Mc, Tc);
         case 5: return make_spectrum_tmap<5>(tm, Upk, Mc, Tc);
@@ -150,6 +167,15 @@ static cudaError_t make_tmap_any(int LOGN, CUtensorMap *tm, const float *Upk, in
 
 static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const CUtensorMap &tm, int64_t Mc, int64_t Tc,
                                   int64_t m0, int64_t t0, int64_t mcv, int64_t tcv, const FftOut &o) {
+    if (use_fft2(LOGN)) {
+        switch (LOGN) {
+            case 4: return launch_fft2<4>(mode, s, tm, m0, t0, mcv, tcv, o);
+            case 5: return launch_fft2<5>(mode, s, tm, m0, t0, mcv, tcv, o);
+            case 6: return launch_fft2<6>(mode, s, tm, m0, t0, mcv, tcv, o);
+            case 7: return launch_fft2<7>(mode, s, tm, m0, t0, mcv, tcv, o);
+            default: return launch_fft2<8>(mode, s, tm, m0, t0, mcv, tcv, o);
+        }
+    }
     switch (LOGN) {
         case 4: return launch_fft<4>(mode, s, tm, Mc, Tc, m0, t0, mcv, tcv, o);
         case 5: return launch_fft<5>(mode, s, tm, Mc, Tc, m0, t0, mcv, tcv, o);

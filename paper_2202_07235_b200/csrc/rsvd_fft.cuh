@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(FR_THREADS, 2) fft_reduce_kernel(const __grid_
     constexpr int N = C::N, Q = C::Q, NH = C::NH, N1 = C::N1, N2 = C::N2, TB = C::TB, C4 = C::C4, SZ = C::SZ;
     constexpr int SP = C::ST_PER;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    // pointer arithmetic on the __shared__ array (not an integer round trip) keeps LDS/STS addressing
+    unsigned char *base = smem_raw + ((1024u - (fr_smem(smem_raw) & 1023u)) & 1023u);
     float *Ur = reinterpret_cast<float *>(base);                             // [NST][ROWS][TB]
     float2 *ZY = reinterpret_cast<float2 *>(base + C::NST * C::UBYTES);      // [TB][SZ]
     float2 *Wq = ZY + TB * SZ;                                               // [NH]  W_Q^r

@@ -1,0 +1,291 @@
+// rsvd_fft2.cuh -- Steps 3-4 of the align path (PAPER.md:673 transform, forward sign per DESIGN.md
+// G3; PAPER.md:504-517 argmax), restructured for N = Q/2 <= 256: same mathematics as rsvd_fft.cuh
+// (one complex length-N FFT of Z_n = (Y_n + conj Y_{N-n}) + i W_Q^n (Y_n - conj Y_{N-n}) per pair,
+// z_k = x_{2k} + i x_{2k+1}, Re X_k = 2 pi x_k; Z is formed from U = 2Y, so results are scaled by pi).
+//
+// Four-step N = N1 x N2 (N1 = 2^floor(log2 N / 2) columns, N2 >= N1 rows), lane = image:
+//   work item  one template x 32 images; a CTA holds G independent warp groups of N1/2 warps, each
+//              owning one shared-memory slot (its own TMA target and, in place, its transpose buffer)
+//              and one mbarrier; groups synchronise with named barriers only;
+//   TMA        the group's 2N spectrum rows x 32 images land in its slot (3-D tensor-map boxes);
+//   pass 1     warp c of a group owns the mirror column pair {c, N1 - c} (warp 0: the self-mirror
+//              columns 0 and N1/2), so Z_n and Z_{N-n} are formed in registers from the two values
+//              they share (no staging pass), then two in-register DIF DFTs of length N2 over n2,
+//              twiddles W_N^{n1 k1}, and stores over the slot as ZY[image][k1 N1 + (n1 ^ sw(k1))]
+//              (row stride N + 1: conflict-free for both passes);
+//   pass 2     one thread per (image, k1): in-register DIF DFT of length N1 over n1 -> z[k1 + N2 k2];
+//              landscape store, or max then first argmax over the N2 lanes of the pair; the next
+//              item's TMA is issued as soon as the slot has been read.
+#pragma once
+
+#include "rsvd_fft.cuh"
+
+namespace rsvd {
+
+template <int LOGN>
+struct Fft2Cfg {
+    static constexpr int N = 1 << LOGN;
+    static constexpr int Q = 2 * N;
+    static constexpr int N1 = 1 << (LOGN / 2);        // columns (pass-2 length)
+    static constexpr int N2 = N / N1;                 // rows (pass-1 length), N2 in {N1, 2 N1}
+    static constexpr int TASKS = N1 / 2;              // warps per group
+    static constexpr int GT = 32 * TASKS;             // threads per group
+    static constexpr int G = 16 / TASKS;              // groups per CTA (512 threads)
+    static constexpr int THREADS = G * GT;
+    static constexpr int TB = 32;                     // images per item (lane = image)
+    static constexpr int ROWS = 2 * N;                // re plane rows, then im plane rows
+    static constexpr int BOXR = ROWS < 256 ? ROWS : 256;
+    static constexpr int NBOX = ROWS / BOXR;
+    static constexpr int UBYTES = ROWS * TB * 4;
+    static constexpr int SZ = N + 1;                  // ZY row stride (float2)
+    static constexpr int ZBYTES = TB * SZ * 8;
+    static constexpr int SLOT = ((UBYTES > ZBYTES ? UBYTES : ZBYTES) + 1023) / 1024 * 1024;
+    static constexpr int SWD = N1 >= 16 ? 1 : 16 / N1;
+    static constexpr int P2_PER = TB * N2 / GT;       // pass-2 tasks per thread
+    static constexpr size_t smem_bytes() { return 1024 + (size_t)G * SLOT + (size_t)N * 8 + (size_t)(N / 2) * 8 + G * 8 + 64; }
+};
+
+// Z_r and Z_{N-r} from a = U_r, b = U_{N-r} (0 < r < N/2), w = W_Q^r.
+__device__ __forceinline__ void z_pair(float2 a, float2 b, float2 w, float2 &zr, float2 &zm) {
+    const float sx = a.x + b.x, sy = a.y - b.y;            // s = U_r + conj U_{N-r}
+    const float dx = a.x - b.x, dy = a.y + b.y;            // d = U_r - conj U_{N-r}
+    const float px = w.x * dx - w.y * dy, py = w.x * dy + w.y * dx;
+    zr = make_float2(sx - py, sy + px);                    // s + i p
+    zm = make_float2(sx + py, px - sy);                    // conj(s) + i conj(p)
+}
+
+template <int LOGN, int MODE>
+__global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                               int64_t m0, int64_t t0, int64_t mcv,
+                                                                               int64_t tcv, FftOut out) {
+    using C = Fft2Cfg<LOGN>;
+    constexpr int N = C::N, Q = C::Q, N1 = C::N1, N2 = C::N2, TB = C::TB, SZ = C::SZ, G = C::G, GT = C::GT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // pointer arithmetic on the __shared__ array (not an integer round trip) keeps LDS/STS addressing
+    unsigned char *base = smem_raw + ((1024u - (fr_smem(smem_raw) & 1023u)) & 1023u);
+    float2 *Wn = reinterpret_cast<float2 *>(base + G * C::SLOT);     // [N1][N2] W_N^{c k1}
+    float2 *Wq = Wn + N;                                             // [N/2]  W_Q^r
+    uint64_t *full = reinterpret_cast<uint64_t *>(Wq + N / 2);       // [G]
+
+    const int tid = threadIdx.x;
+    const int g = tid / GT, gt = tid - g * GT;
+    const int warp = gt >> 5, lane = tid & 31;
+    float *U = reinterpret_cast<float *>(base + g * C::SLOT);       // [ROWS][TB]
+    float2 *ZY = reinterpret_cast<float2 *>(U);                      // [TB][SZ], in place after pass-1 reads
+    const int nmb = (int)((mcv + TB - 1) / TB);
+    const int nitems = (int)tcv * nmb;
+    const int stride = (int)gridDim.x * G;
+    const int first = (int)blockIdx.x * G + g;
+
+    auto issue = [&](int it) {                                   // group thread 0 only
+        const int tl = it / nmb, mb0 = (it - tl * nmb) * TB;
+        const uint32_t bar = fr_smem(full + g);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((uint32_t)C::UBYTES)
+                     : "memory");
+#pragma unroll
+        for (int bx = 0; bx < C::NBOX; ++bx) {
+            const uint32_t dst = fr_smem(U + (size_t)bx * C::BOXR * TB);
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                ::"r"(dst), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(mb0), "r"(tl), "r"(bx * C::BOXR), "r"(bar)
+                : "memory");
+        }
+    };
+    auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(GT) : "memory"); };
+
+    if (gt == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fr_smem(full + g)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (first < nitems) issue(first);
+    }
+    for (int i = tid; i < N; i += C::THREADS) Wn[i] = twiddle_N(i / N2, i % N2, N);
+    for (int i = tid; i < N / 2; i += C::THREADS) {
+        float sn, cs;
+        sincospif(2.0f * (float)i / (float)Q, &sn, &cs);
+        Wq[i] = make_float2(cs, -sn);
+    }
+    __syncthreads();
+
+    const float PI = 3.14159265358979323846f;
+    // pass-1 columns of this warp
+    const int ca = warp == 0 ? 0 : warp;
+    const int cb = warp == 0 ? N1 / 2 : N1 - warp;
+    int kk = 0;
+    for (int item = first; item < nitems; item += stride, ++kk) {
+        const int tl = item / nmb, mb0 = (item - tl * nmb) * TB;
+        const int64_t t = t0 + tl;
+        const float st = out.sc_t ? __ldg(out.sc_t + t) : 1.f;
+        fr_mbar_wait(full + g, (uint32_t)kk & 1u);
+
+        // ---- pass 1: Z from the ring, two DFTs of length N2
+        float2 za[N2], zb[N2];
+        auto ld = [&](int n) { return make_float2(U[n * TB + lane], U[(N + n) * TB + lane]); };
+        if (warp == 0) {
+            // column 0: rows N1*n2; pairs (n2, N2 - n2); n2 = 0 -> Z_0, n2 = N2/2 -> Z_{N/2}
+            {
+                const float2 u0 = ld(0);                                  // (U_0, U_N) packed
+                za[0] = make_float2(u0.x + u0.y, u0.x - u0.y);
+                const float2 uh = ld(N / 2);
+                za[N2 / 2] = make_float2(2.f * uh.x, 2.f * uh.y);
+#pragma unroll
+                for (int n2 = 1; n2 < N2 / 2; ++n2) z_pair(ld(N1 * n2), ld(N1 * (N2 - n2)), Wq[N1 * n2], za[n2], za[N2 - n2]);
+            }
+            // column N1/2: rows N1/2 + N1 n2; pairs (n2, N2 - 1 - n2)
+#pragma unroll
+            for (int n2 = 0; n2 < N2 / 2; ++n2) {
+                const int r = N1 / 2 + N1 * n2;
+                z_pair(ld(r), ld(N - r), Wq[r], zb[n2], zb[N2 - 1 - n2]);
+            }
+        } else {
+            // columns c and N1 - c: (c, n2) <-> (N1 - c, N2 - 1 - n2)
+#pragma unroll
+            for (int n2 = 0; n2 < N2 / 2; ++n2) {
+                const int ra = ca + N1 * n2, rb = cb + N1 * n2;
+                z_pair(ld(ra), ld(N - ra), Wq[ra], za[n2], zb[N2 - 1 - n2]);
+                z_pair(ld(rb), ld(N - rb), Wq[rb], zb[n2], za[N2 - 1 - n2]);
+            }
+        }
+        gbar();                                                // (A) every U read: slot becomes ZY
+        dif_reg<N2>(za);
+        dif_reg<N2>(zb);
+        {
+            float2 *yw = ZY + lane * SZ;
+            const float2 *twa = Wn + ca * N2, *twb = Wn + cb * N2;
+#pragma unroll
+            for (int k1 = 0; k1 < N2; ++k1) {
+                float2 xa = za[brev(k1, clog2(N2))], xb = zb[brev(k1, clog2(N2))];
+                if (k1) {
+                    xa = c_mul(xa, twa[k1]);
+                    xb = c_mul(xb, twb[k1]);
+                }
+                const int sw = (k1 / C::SWD) % N1;
+                yw[k1 * N1 + (ca ^ sw)] = xa;
+                yw[k1 * N1 + (cb ^ sw)] = xb;
+            }
+        }
+        gbar();                                                // (B) ZY complete
+
+        // ---- pass 2
+        float2 w[C::P2_PER][N1];
+#pragma unroll
+        for (int j = 0; j < C::P2_PER; ++j) {
+            const int task = gt + GT * j;
+            const int p = task / N2, k1 = task % N2;
+            const float2 *yr = ZY + p * SZ + k1 * N1;
+            const int sw = (k1 / C::SWD) % N1;
+#pragma unroll
+            for (int i = 0; i < N1; ++i) w[j][i] = yr[i ^ sw];
+        }
+        gbar();                                                // (C) slot free: next item's TMA
+        if (gt == 0 && item + stride < nitems) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(item + stride);
+        }
+        uint32_t stale[C::P2_PER];                             // MODE_IMAGE: image keys
+        if constexpr (MODE == MODE_IMAGE) {
+#pragma unroll
+            for (int j = 0; j < C::P2_PER; ++j) {
+                const int ml = mb0 + (gt + GT * j) / N2;
+                stale[j] = ml < mcv ? (uint32_t)(__ldcg(out.best_key + m0 + ml) >> 32) : 0u;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < C::P2_PER; ++j) {
+            const int task = gt + GT * j;
+            const int p = task / N2, k1 = task % N2;
+            dif_reg<N1>(w[j]);                                 // w[brev(k2)] = z[k1 + N2 k2]
+            const int64_t ml = mb0 + p;
+            const bool valid = ml < mcv;
+            const int64_t m = m0 + ml;
+            const float mul = PI / (((valid && out.sc_m) ? __ldg(out.sc_m + m) : 1.f) * st);
+            if constexpr (MODE == MODE_LANDSCAPE) {
+                if (valid) {
+                    float2 *dst = reinterpret_cast<float2 *>(out.X + m * out.ld_m + t * out.ld_t);
+#pragma unroll
+                    for (int k2 = 0; k2 < N1; ++k2) {
+                        const float2 z = w[j][brev(k2, clog2(N1))];
+                        dst[k1 + N2 * k2] = make_float2(mul * z.x, mul * z.y);
+                    }
+                }
+            } else {
+                const unsigned gmask = N2 >= 32 ? 0xffffffffu
+                                                : (((1u << (N2 & 31)) - 1u) << ((threadIdx.x & 31) & ~(N2 - 1)));
+                float mx = -INFINITY;
+#pragma unroll
+                for (int k2 = 0; k2 < N1; ++k2) mx = fmaxf(mx, fmaxf(w[j][k2].x, w[j][k2].y));
+#pragma unroll
+                for (int off = N2 / 2; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, off));
+                const float bv = mul * mx;
+                bool go = valid;
+                if constexpr (MODE == MODE_IMAGE) go = valid && ord_f32(bv) >= stale[j];
+                if (go) {                                      // uniform over the pair's lanes
+                    int bk = 0x7fffffff;
+#pragma unroll
+                    for (int k2 = N1 - 1; k2 >= 0; --k2) {     // descending: the smallest index wins
+                        const float2 z = w[j][brev(k2, clog2(N1))];
+                        const int kx = 2 * (k1 + N2 * k2);
+                        if (z.y == mx) bk = kx + 1;
+                        if (z.x == mx) bk = kx;
+                    }
+#pragma unroll
+                    for (int off = N2 / 2; off >= 1; off >>= 1) bk = min(bk, __shfl_xor_sync(gmask, bk, off));
+                    if (k1 == 0) {
+                        if constexpr (MODE == MODE_PAIR) {
+                            out.best_val[m * out.T + t] = bv;
+                            out.best_k[m * out.T + t] = bk;
+                        } else {
+                            const uint32_t idx = (uint32_t)((out.t_offset + t) * Q + bk);
+                            const unsigned long long key =
+                                ((unsigned long long)ord_f32(bv) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
+                            atomicMax(out.best_key + m, key);
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// 3-D view of the planar workspace with 32-image boxes (the fft2 work item).
+template <int LOGN>
+static cudaError_t make_spectrum_tmap2(CUtensorMap *tm, const float *Upk, int64_t Mc, int64_t Tc) {
+    using C = Fft2Cfg<LOGN>;
+    PFN_encodeTiled_fr enc = encode_tiled_fn();
+    if (!enc) return cudaErrorNotSupported;
+    const cuuint64_t dims[3] = {(cuuint64_t)Mc, (cuuint64_t)Tc, (cuuint64_t)C::ROWS};
+    const cuuint64_t strides[2] = {(cuuint64_t)Mc * 4, (cuuint64_t)Mc * Tc * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)C::TB, 1u, (cuuint32_t)C::BOXR};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(Upk), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int LOGN, int MODE>
+static cudaError_t launch_fft2_mode(cudaStream_t s, const CUtensorMap &tm, int64_t m0, int64_t t0, int64_t mcv,
+                                    int64_t tcv, const FftOut &out) {
+    using C = Fft2Cfg<LOGN>;
+    const size_t smem = C::smem_bytes();
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(fft2_reduce_kernel<LOGN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int64_t nitems = tcv * ((mcv + C::TB - 1) / C::TB);
+    const int64_t grid = std::min<int64_t>((nitems + C::G - 1) / C::G, (int64_t)num_sms());
+    fft2_reduce_kernel<LOGN, MODE><<<(unsigned)grid, C::THREADS, smem, s>>>(tm, m0, t0, mcv, tcv, out);
+    return cudaGetLastError();
+}
+
+template <int LOGN>
+static cudaError_t launch_fft2(int mode, cudaStream_t s, const CUtensorMap &tm, int64_t m0, int64_t t0, int64_t mcv,
+                               int64_t tcv, const FftOut &out) {
+    if (mode == MODE_PAIR) return launch_fft2_mode<LOGN, MODE_PAIR>(s, tm, m0, t0, mcv, tcv, out);
+    if (mode == MODE_IMAGE) return launch_fft2_mode<LOGN, MODE_IMAGE>(s, tm, m0, t0, mcv, tcv, out);
+    return launch_fft2_mode<LOGN, MODE_LANDSCAPE>(s, tm, m0, t0, mcv, tcv, out);
+}
+
+}  // namespace rsvd
