@@ -4,9 +4,10 @@
 // z_k = x_{2k} + i x_{2k+1}, Re X_k = 2 pi x_k; Z is formed from U = 2Y, so results are scaled by pi).
 //
 // Four-step N = N1 x N2 (N1 = 2^floor(log2 N / 2) columns, N2 >= N1 rows), lane = image:
-//   work item  one template x 32 images; a CTA holds G independent warp groups of N1/2 warps, each
-//              owning one shared-memory slot (its own TMA target and, in place, its transpose buffer)
-//              and one mbarrier; groups synchronise with named barriers only;
+//   work item  one template x 32 images; a CTA holds G independent warp groups of N1/2 warps that
+//              take its items in turn from a ring of G + 1 shared-memory slots (each the TMA target of
+//              one item and, in place, its transpose buffer; one mbarrier each); groups synchronise
+//              with named barriers only, and a slot is refilled G + 1 items ahead once read;
 //   TMA        the group's 2N spectrum rows x 32 images land in its slot (3-D tensor-map boxes);
 //   pass 1     warp c of a group owns the mirror column pair {c, N1 - c} (warp 0: the self-mirror
 //              columns 0 and N1/2), so Z_n and Z_{N-n} are formed in registers from the two values
@@ -42,7 +43,8 @@ struct Fft2Cfg {
     static constexpr int SLOT = ((UBYTES > ZBYTES ? UBYTES : ZBYTES) + 1023) / 1024 * 1024;
     static constexpr int SWD = N1 >= 16 ? 1 : 16 / N1;
     static constexpr int P2_PER = TB * N2 / GT;       // pass-2 tasks per thread
-    static constexpr size_t smem_bytes() { return 1024 + (size_t)G * SLOT + (size_t)N * 8 + (size_t)(N / 2) * 8 + G * 8 + 64; }
+    static constexpr int NSLOT = G + 1;               // one slot in flight beyond the G being processed
+    static constexpr size_t smem_bytes() { return 1024 + (size_t)NSLOT * SLOT + (size_t)N * 8 + (size_t)(N / 2) * 8 + NSLOT * 8 + 64; }
 };
 
 // Z_r and Z_{N-r} from a = U_r, b = U_{N-r} (0 < r < N/2), w = W_Q^r.
@@ -63,28 +65,28 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // pointer arithmetic on the __shared__ array (not an integer round trip) keeps LDS/STS addressing
     unsigned char *base = smem_raw + ((1024u - (fr_smem(smem_raw) & 1023u)) & 1023u);
-    float2 *Wn = reinterpret_cast<float2 *>(base + G * C::SLOT);     // [N1][N2] W_N^{c k1}
+    float2 *Wn = reinterpret_cast<float2 *>(base + C::NSLOT * C::SLOT);   // [N1][N2] W_N^{c k1}
     float2 *Wq = Wn + N;                                             // [N/2]  W_Q^r
-    uint64_t *full = reinterpret_cast<uint64_t *>(Wq + N / 2);       // [G]
+    uint64_t *full = reinterpret_cast<uint64_t *>(Wq + N / 2);       // [NSLOT]
 
     const int tid = threadIdx.x;
     const int g = tid / GT, gt = tid - g * GT;
     const int warp = gt >> 5, lane = tid & 31;
-    float *U = reinterpret_cast<float *>(base + g * C::SLOT);       // [ROWS][TB]
-    float2 *ZY = reinterpret_cast<float2 *>(U);                      // [TB][SZ], in place after pass-1 reads
     const int nmb = (int)((mcv + TB - 1) / TB);
     const int nitems = (int)tcv * nmb;
-    const int stride = (int)gridDim.x * G;
-    const int first = (int)blockIdx.x * G + g;
+    const int grid = (int)gridDim.x;
+    // local index i -> item blockIdx.x + grid * i, processed by group i % G in slot i % NSLOT
+    auto item_of = [&](int i) { return (int)blockIdx.x + grid * i; };
 
-    auto issue = [&](int it) {                                   // group thread 0 only
+    auto issue = [&](int i) {                                    // one thread
+        const int it = item_of(i), sl = i % C::NSLOT;
         const int tl = it / nmb, mb0 = (it - tl * nmb) * TB;
-        const uint32_t bar = fr_smem(full + g);
+        const uint32_t bar = fr_smem(full + sl);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((uint32_t)C::UBYTES)
                      : "memory");
 #pragma unroll
         for (int bx = 0; bx < C::NBOX; ++bx) {
-            const uint32_t dst = fr_smem(U + (size_t)bx * C::BOXR * TB);
+            const uint32_t dst = fr_smem(base + (size_t)sl * C::SLOT + (size_t)bx * C::BOXR * TB * 4);
             asm volatile(
                 "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                 ::"r"(dst), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(mb0), "r"(tl), "r"(bx * C::BOXR), "r"(bar)
@@ -93,10 +95,11 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
     };
     auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(GT) : "memory"); };
 
-    if (gt == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fr_smem(full + g)));
+    if (tid == 0) {
+        for (int sl = 0; sl < C::NSLOT; ++sl) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fr_smem(full + sl)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (first < nitems) issue(first);
+        for (int i = 0; i < C::NSLOT; ++i)
+            if (item_of(i) < nitems) issue(i);
     }
     for (int i = tid; i < N; i += C::THREADS) Wn[i] = twiddle_N(i / N2, i % N2, N);
     for (int i = tid; i < N / 2; i += C::THREADS) {
@@ -110,12 +113,14 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
     // pass-1 columns of this warp
     const int ca = warp == 0 ? 0 : warp;
     const int cb = warp == 0 ? N1 / 2 : N1 - warp;
-    int kk = 0;
-    for (int item = first; item < nitems; item += stride, ++kk) {
+    for (int i = g; item_of(i) < nitems; i += G) {
+        const int item = item_of(i), sl = i % C::NSLOT;
+        float *U = reinterpret_cast<float *>(base + (size_t)sl * C::SLOT);    // [ROWS][TB]
+        float2 *ZY = reinterpret_cast<float2 *>(U);                           // [TB][SZ], in place after pass-1 reads
         const int tl = item / nmb, mb0 = (item - tl * nmb) * TB;
         const int64_t t = t0 + tl;
         const float st = out.sc_t ? __ldg(out.sc_t + t) : 1.f;
-        fr_mbar_wait(full + g, (uint32_t)kk & 1u);
+        fr_mbar_wait(full + sl, (uint32_t)(i / C::NSLOT) & 1u);
 
         // ---- pass 1: Z from the ring, two DFTs of length N2
         float2 za[N2], zb[N2];
@@ -176,10 +181,10 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
 #pragma unroll
             for (int i = 0; i < N1; ++i) w[j][i] = yr[i ^ sw];
         }
-        gbar();                                                // (C) slot free: next item's TMA
-        if (gt == 0 && item + stride < nitems) {
+        gbar();                                                // (C) slot free: refill it NSLOT items ahead
+        if (gt == 0 && item_of(i + C::NSLOT) < nitems) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(item + stride);
+            issue(i + C::NSLOT);
         }
         uint32_t stale[C::P2_PER];                             // MODE_IMAGE: image keys
         if constexpr (MODE == MODE_IMAGE) {
