@@ -12,8 +12,8 @@
 //   pass 1     warp c of a group owns the mirror column pair {c, N1 - c} (warp 0: the self-mirror
 //              columns 0 and N1/2), so Z_n and Z_{N-n} are formed in registers from the two values
 //              they share (no staging pass), then two in-register DIF DFTs of length N2 over n2,
-//              twiddles W_N^{n1 k1}, and stores over the slot as ZY[image][k1 N1 + (n1 ^ sw(k1))]
-//              (row stride N + 1: conflict-free for both passes);
+//              twiddles W_N^{n1 k1}, and stores over the slot as ZY[image][k1][n1] with padded strides
+//              (N1 + 1 per k1 block, odd per image: conflict-free for both passes, no index swizzle);
 //   pass 2     one thread per (image, k1): in-register DIF DFT of length N1 over n1 -> z[k1 + N2 k2];
 //              landscape store, or max then first argmax over the N2 lanes of the pair; the next
 //              item's TMA is issued as soon as the slot has been read.
@@ -38,10 +38,10 @@ struct Fft2Cfg {
     static constexpr int BOXR = ROWS < 256 ? ROWS : 256;
     static constexpr int NBOX = ROWS / BOXR;
     static constexpr int UBYTES = ROWS * TB * 4;
-    static constexpr int SZ = N + 1;                  // ZY row stride (float2)
+    static constexpr int SK = N1 + 1;                 // ZY stride of one k1 block (float2)
+    static constexpr int SZ = N2 * SK + 1;            // ZY stride of one image (odd)
     static constexpr int ZBYTES = TB * SZ * 8;
     static constexpr int SLOT = ((UBYTES > ZBYTES ? UBYTES : ZBYTES) + 1023) / 1024 * 1024;
-    static constexpr int SWD = N1 >= 16 ? 1 : 16 / N1;
     static constexpr int P2_PER = TB * N2 / GT;       // pass-2 tasks per thread
     static constexpr int NSLOT = G + 1;               // one slot in flight beyond the G being processed
     static constexpr size_t smem_bytes() { return 1024 + (size_t)NSLOT * SLOT + (size_t)N * 8 + (size_t)(N / 2) * 8 + NSLOT * 8 + 64; }
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
         dif_reg<N2>(za);
         dif_reg<N2>(zb);
         {
-            float2 *yw = ZY + lane * SZ;
+            float2 *ywa = ZY + lane * SZ + ca, *ywb = ZY + lane * SZ + cb;
             const float2 *twa = Wn + ca * N2, *twb = Wn + cb * N2;
 #pragma unroll
             for (int k1 = 0; k1 < N2; ++k1) {
@@ -163,9 +163,8 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
                     xa = c_mul(xa, twa[k1]);
                     xb = c_mul(xb, twb[k1]);
                 }
-                const int sw = (k1 / C::SWD) % N1;
-                yw[k1 * N1 + (ca ^ sw)] = xa;
-                yw[k1 * N1 + (cb ^ sw)] = xb;
+                ywa[k1 * C::SK] = xa;
+                ywb[k1 * C::SK] = xb;
             }
         }
         gbar();                                                // (B) ZY complete
@@ -176,10 +175,9 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
         for (int j = 0; j < C::P2_PER; ++j) {
             const int task = gt + GT * j;
             const int p = task / N2, k1 = task % N2;
-            const float2 *yr = ZY + p * SZ + k1 * N1;
-            const int sw = (k1 / C::SWD) % N1;
+            const float2 *yr = ZY + p * SZ + k1 * C::SK;
 #pragma unroll
-            for (int i = 0; i < N1; ++i) w[j][i] = yr[i ^ sw];
+            for (int i = 0; i < N1; ++i) w[j][i] = yr[i];
         }
         gbar();                                                // (C) slot free: refill it NSLOT items ahead
         if (gt == 0 && item_of(i + C::NSLOT) < nitems) {
