@@ -23,7 +23,9 @@ constexpr int JB = 32;         // angular samples per smem slab
 constexpr int NTHR = 256;
 
 // grid: (ntile, ntile, nchunks), only tiles with ti >= tj.  Thread (ty, tx) owns rows
-// r_a = ti*64 + ty + 16a and r'_b = tj*64 + tx + 16b, a, b < 4.
+// r_a = ti*64 + ty + 16a and r'_b = tj*64 + tx + 16b, a, b < 4.  Samples are widened to fp64 once,
+// when staged in shared memory, so the inner loop is pure DFMA (products of fp32 values are exact in
+// fp64; accumulation order is fixed).
 __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__restrict__ tmpl,
                                                                int64_t T, int R, int Q,
                                                                double *__restrict__ partials) {
@@ -31,8 +33,9 @@ __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__r
     if (ti < tj) return;
     const int64_t c = blockIdx.z;
     const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-    __shared__ float2 xi[BT][JB + 1];
-    __shared__ float2 xj[BT][JB + 1];
+    extern __shared__ __align__(16) double2 kp_smem[];
+    double2 (*xi)[JB + 1] = reinterpret_cast<double2 (*)[JB + 1]>(kp_smem);
+    double2 (*xj)[JB + 1] = reinterpret_cast<double2 (*)[JB + 1]>(kp_smem + BT * (JB + 1));
     __shared__ double si[BT][2], sj[BT][2];       // per-template row sums (re, im)
 
     double acc[4][4];
@@ -48,43 +51,40 @@ __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__r
         if (tid < BT) { si[tid][0] = si[tid][1] = 0.0; sj[tid][0] = sj[tid][1] = 0.0; }
         for (int j0 = 0; j0 < Q; j0 += JB) {
             __syncthreads();
-            // load 64 rows x JB samples for both row tiles
+            // load 64 rows x JB samples for both row tiles, widened to fp64
             for (int idx = tid; idx < BT * JB; idx += NTHR) {
                 const int rr = idx / JB, jj = idx % JB;
                 const int r1 = ti * BT + rr, r2 = tj * BT + rr;
                 const int j = j0 + jj;
-                float2 z = make_float2(0.f, 0.f);
-                xi[rr][jj] = (r1 < R && j < Q) ? bt[(int64_t)r1 * Q + j] : z;
-                xj[rr][jj] = (r2 < R && j < Q) ? bt[(int64_t)r2 * Q + j] : z;
+                const float2 z = make_float2(0.f, 0.f);
+                const float2 u = (r1 < R && j < Q) ? __ldg(bt + (int64_t)r1 * Q + j) : z;
+                const float2 v = (r2 < R && j < Q) ? __ldg(bt + (int64_t)r2 * Q + j) : z;
+                xi[rr][jj] = make_double2((double)u.x, (double)u.y);
+                xj[rr][jj] = make_double2((double)v.x, (double)v.y);
             }
             __syncthreads();
             // row sums (fp64, fixed order)
             if (tid < BT) {
                 double sr = 0, sim = 0, tr = 0, tim = 0;
                 for (int jj = 0; jj < JB; ++jj) {
-                    sr += (double)xi[tid][jj].x; sim += (double)xi[tid][jj].y;
-                    tr += (double)xj[tid][jj].x; tim += (double)xj[tid][jj].y;
+                    sr += xi[tid][jj].x; sim += xi[tid][jj].y;
+                    tr += xj[tid][jj].x; tim += xj[tid][jj].y;
                 }
                 si[tid][0] += sr; si[tid][1] += sim;
                 sj[tid][0] += tr; sj[tid][1] += tim;
             }
             // Gram: Re(x_r conj(x_r')) = xr xr' + xi xi'
+#pragma unroll 4
             for (int jj = 0; jj < JB; ++jj) {
-                double ar[4], ai[4], br[4], bi[4];
+                double2 av[4], bv[4];
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    const float2 u = xi[ty + 16 * a][jj];
-                    ar[a] = u.x; ai[a] = u.y;
-                }
+                for (int a = 0; a < 4; ++a) av[a] = xi[ty + 16 * a][jj];
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const float2 u = xj[tx + 16 * b][jj];
-                    br[b] = u.x; bi[b] = u.y;
-                }
+                for (int b = 0; b < 4; ++b) bv[b] = xj[tx + 16 * b][jj];
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) acc[a][b] = fma(ar[a], br[b], fma(ai[a], bi[b], acc[a][b]));
+                    for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a].x, bv[b].x, fma(av[a].y, bv[b].y, acc[a][b]));
             }
         }
         __syncthreads();
@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__r
             if (r1 < R && r2 < R) out[(int64_t)r1 * R + r2] = acc[a][b];
         }
 }
+constexpr size_t KP_SMEM = 2 * (size_t)BT * (JB + 1) * sizeof(double2);
 
 // C[r][r'] = sqrt(w_r w_r') / (T Q) * sum_c P_c[max(r,r')][min(r,r')] (lower triangle is the
 // computed one; reading it for both halves makes C exactly symmetric).
@@ -157,7 +158,13 @@ extern "C" rsvd_status rsvd_kernel_partials(const void *templates, int64_t T, in
     dim3 grid(nt, nt, (unsigned)nchunks);
     const bool timed = timing_enabled();
     cudaEvent_t ev0 = timed ? timing_event((cudaStream_t)stream) : nullptr;
-    kernel_partials_kernel<<<grid, NTHR, 0, (cudaStream_t)stream>>>(
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kernel_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KP_SMEM);
+        if (e != cudaSuccess) return cuda_check(e, "kernel_partials attribute");
+        attr = true;
+    }
+    kernel_partials_kernel<<<grid, NTHR, KP_SMEM, (cudaStream_t)stream>>>(
         reinterpret_cast<const float2 *>(templates), T, R, Q, partials);
     count_launches(1);
     if (timed) timing_span(ev0, timing_event((cudaStream_t)stream), TK_BASIS);

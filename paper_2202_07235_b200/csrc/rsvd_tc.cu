@@ -390,7 +390,7 @@ __device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, i
     }
 }
 
-template <int LOGQ>
+template <int LOGQ, int HC>
 __global__ void __launch_bounds__(256) compress_tc_kernel(const float2 *__restrict__ rings, int64_t n, int R,
                                                           const double *__restrict__ w, const double *__restrict__ U,
                                                           int H, int side, int KB, int64_t op_rows,
@@ -398,7 +398,6 @@ __global__ void __launch_bounds__(256) compress_tc_kernel(const float2 *__restri
     constexpr int Q = 1 << LOGQ;
     constexpr int L = 32;
     constexpr int E = Q / L;
-    constexpr int HC = 16;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2 *tw = reinterpret_cast<float2 *>(smem_raw);       // [E][L]
     float2 *at = tw + E * L;                                 // [H][Q]
@@ -423,6 +422,7 @@ __global__ void __launch_bounds__(256) compress_tc_kernel(const float2 *__restri
             float2 acc[HC];
 #pragma unroll
             for (int hh = 0; hh < HC; ++hh) acc[hh] = make_float2(0.f, 0.f);
+#pragma unroll 4
             for (int r = 0; r < R; ++r) {
                 const float2 a = __ldg(ring + (int64_t)r * Q + j);
                 const float4 *u4 = reinterpret_cast<const float4 *>(up + r * HC);
@@ -458,8 +458,11 @@ __global__ void __launch_bounds__(256) compress_tc_kernel(const float2 *__restri
     emit_tc_rows(at, H, Q, KB, side, row, op_rows, s, ops);
 }
 
+// principal rings per projection pass: the whole H in one pass up to 32 (one read of the rings)
+static int compress_hc(int H) { return H <= 8 ? 8 : (H <= 16 ? 16 : (H <= 24 ? 24 : 32)); }
+
 size_t compress_tc_smem(int Q, int H, int R) {
-    return (size_t)Q * sizeof(float2) + (size_t)H * Q * sizeof(float2) + (size_t)R * 16 * sizeof(float) + 33 * 4;
+    return (size_t)Q * sizeof(float2) + (size_t)H * Q * sizeof(float2) + (size_t)R * compress_hc(H) * sizeof(float) + 33 * 4;
 }
 
 // TC layout needs the whole [H][Q] coefficient block of a row in shared memory (R <= 256).
@@ -478,17 +481,27 @@ int resolve_path(int Q, int H) {
 }
 void set_path(int p) { g_path = (p == PATH_SIMT || p == PATH_TC) ? p : PATH_AUTO; }
 
-template <int LOGQ>
-static cudaError_t launch_compress_tc_q(const float2 *rings, int64_t n, int R, const double *w, const double *U, int H,
-                                        int side, void *blocks, cudaStream_t s) {
+template <int LOGQ, int HC>
+static cudaError_t launch_compress_tc_qh(const float2 *rings, int64_t n, int R, const double *w, const double *U, int H,
+                                         int side, void *blocks, cudaStream_t s) {
     const size_t smem = compress_tc_smem(1 << LOGQ, H, R);
-    cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel<LOGQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel<LOGQ, HC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int Q = 1 << LOGQ;
     float *scales = const_cast<float *>(tc_scales(blocks, n, Q, H, side));
-    compress_tc_kernel<LOGQ><<<(unsigned)n, 256, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H), tc_op_rows(n, side),
-                                                            reinterpret_cast<__half *>(blocks), scales);
+    compress_tc_kernel<LOGQ, HC><<<(unsigned)n, 256, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H), tc_op_rows(n, side),
+                                                                reinterpret_cast<__half *>(blocks), scales);
     return cudaGetLastError();
+}
+template <int LOGQ>
+static cudaError_t launch_compress_tc_q(const float2 *rings, int64_t n, int R, const double *w, const double *U, int H,
+                                        int side, void *blocks, cudaStream_t s) {
+    switch (compress_hc(H)) {
+        case 8: return launch_compress_tc_qh<LOGQ, 8>(rings, n, R, w, U, H, side, blocks, s);
+        case 16: return launch_compress_tc_qh<LOGQ, 16>(rings, n, R, w, U, H, side, blocks, s);
+        case 24: return launch_compress_tc_qh<LOGQ, 24>(rings, n, R, w, U, H, side, blocks, s);
+        default: return launch_compress_tc_qh<LOGQ, 32>(rings, n, R, w, U, H, side, blocks, s);
+    }
 }
 
 cudaError_t launch_compress_tc(const float2 *rings, int64_t n, int R, int Q, const double *w, const double *U, int H,
