@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__r
                 const double re = si[ty + 16 * a][0] * sj[tx + 16 * b][0] + si[ty + 16 * a][1] * sj[tx + 16 * b][1];
                 acc[a][b] -= re * invQ;
             }
+        __syncthreads();           // every thread has read si/sj before the next template zeroes them
     }
     double *out = partials + c * (int64_t)R * R;
 #pragma unroll
