@@ -95,11 +95,12 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
     };
     auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(GT) : "memory"); };
 
+    // PDL: the next chunk's contraction may be scheduled as SMs free up (it waits for us before
+    // writing the workspace); our own input is the previous kernel's output, so wait for it first.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (tid == 0) {
         for (int sl = 0; sl < C::NSLOT; ++sl) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fr_smem(full + sl)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int i = 0; i < C::NSLOT; ++i)
-            if (item_of(i) < nitems) issue(i);
     }
     for (int i = tid; i < N; i += C::THREADS) Wn[i] = twiddle_N(i / N2, i % N2, N);
     for (int i = tid; i < N / 2; i += C::THREADS) {
@@ -107,6 +108,10 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
         sincospif(2.0f * (float)i / (float)Q, &sn, &cs);
         Wq[i] = make_float2(cs, -sn);
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid == 0)
+        for (int i = 0; i < C::NSLOT; ++i)
+            if (item_of(i) < nitems) issue(i);
     __syncthreads();
 
     const float PI = 3.14159265358979323846f;
@@ -279,8 +284,17 @@ static cudaError_t launch_fft2_mode(cudaStream_t s, const CUtensorMap &tm, int64
     }
     const int64_t nitems = tcv * ((mcv + C::TB - 1) / C::TB);
     const int64_t grid = std::min<int64_t>((nitems + C::G - 1) / C::G, (int64_t)num_sms());
-    fft2_reduce_kernel<LOGN, MODE><<<(unsigned)grid, C::THREADS, smem, s>>>(tm, m0, t0, mcv, tcv, out);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fft2_reduce_kernel<LOGN, MODE>, tm, m0, t0, mcv, tcv, out);
 }
 
 template <int LOGN>

@@ -177,6 +177,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = cluster_rank();
     const int cl = (int)(blockIdx.x >> 1), ncl = (int)(gridDim.x >> 1);
+    // PDL: the next kernel (Step 3 on this chunk) may be scheduled as SMs free up; it waits for us.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < TC_STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
@@ -264,6 +266,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
         const bool re_rows = row < 64;
         float *const plane_re = Upk, *const plane_im = Upk + (int64_t)N * Mc * Tc;
         const uint32_t te0 = rank == 0 ? smem_u32(tempty) : mapa_rank(smem_u32(tempty), 0);
+        // PDL: operands are read-only, so TMA + MMA above may overlap the previous kernel's tail; the
+        // workspace is only written after that kernel (Step 3 of the previous chunk) has finished.
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         int qi = 0;
         for (int item = cl; item < nitems; item += ncl) {
             const int tile = item / nqg, qgi = item - tile * nqg;
@@ -600,9 +605,19 @@ cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, i
     nqg = (N + 1 + qg - 1) / qg;
     const int nitems = ntiles * nqg;
     const int ncl = std::min(nitems, target);
-    contract_tc_kernel<<<(unsigned)(2 * ncl), TC_THREADS, TC_SMEM, s>>>(
-        tmA, tmB, tc_steps(H), tc_kb(H), N, mtl, ntl, (int)(m0 / TC_PIMG), (int)(t0 / TC_TT), qg, nqg, nitems, Mc, Tc,
-        Upk);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * ncl));
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = TC_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, contract_tc_kernel, tmA, tmB, tc_steps(H), tc_kb(H), N, mtl, ntl,
+                                       (int)(m0 / TC_PIMG), (int)(t0 / TC_TT), qg, nqg, nitems, Mc, Tc, Upk);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
