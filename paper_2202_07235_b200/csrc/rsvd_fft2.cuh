@@ -44,7 +44,7 @@ struct Fft2Cfg {
     static constexpr int SLOT = ((UBYTES > ZBYTES ? UBYTES : ZBYTES) + 1023) / 1024 * 1024;
     static constexpr int P2_PER = TB * N2 / GT;       // pass-2 tasks per thread
     static constexpr int NSLOT = G + 1;               // one slot in flight beyond the G being processed
-    static constexpr size_t smem_bytes() { return 1024 + (size_t)NSLOT * SLOT + (size_t)N * 8 + (size_t)(N / 2) * 8 + NSLOT * 8 + 64; }
+    static constexpr size_t smem_bytes() { return 1024 + (size_t)NSLOT * SLOT + (size_t)N * 8 + (size_t)(N / 2) * 8 + NSLOT * 12 + 64; }
 };
 
 // Z_r and Z_{N-r} from a = U_r, b = U_{N-r} (0 < r < N/2), w = W_Q^r.
@@ -68,6 +68,10 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
     float2 *Wn = reinterpret_cast<float2 *>(base + C::NSLOT * C::SLOT);   // [N1][N2] W_N^{c k1}
     float2 *Wq = Wn + N;                                             // [N/2]  W_Q^r
     uint64_t *full = reinterpret_cast<uint64_t *>(Wq + N / 2);       // [NSLOT]
+    // tag[s] = local index of the item whose load was last issued into slot s.  A group may reach
+    // its wait for item i while slot i % NSLOT still holds (or is loading) item i - NSLOT: the parity
+    // wait alone would then pass one phase early, so it first waits for the tag.
+    volatile int *tag = reinterpret_cast<volatile int *>(full + C::NSLOT);   // [NSLOT]
 
     const int tid = threadIdx.x;
     const int g = tid / GT, gt = tid - g * GT;
@@ -80,6 +84,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
 
     auto issue = [&](int i) {                                    // one thread
         const int it = item_of(i), sl = i % C::NSLOT;
+        tag[sl] = i;
         const int tl = it / nmb, mb0 = (it - tl * nmb) * TB;
         const uint32_t bar = fr_smem(full + sl);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((uint32_t)C::UBYTES)
@@ -99,7 +104,10 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
     // writing the workspace); our own input is the previous kernel's output, so wait for it first.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (tid == 0) {
-        for (int sl = 0; sl < C::NSLOT; ++sl) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fr_smem(full + sl)));
+        for (int sl = 0; sl < C::NSLOT; ++sl) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fr_smem(full + sl)));
+            tag[sl] = -1;
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = tid; i < N; i += C::THREADS) Wn[i] = twiddle_N(i / N2, i % N2, N);
@@ -125,6 +133,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
         const int tl = item / nmb, mb0 = (item - tl * nmb) * TB;
         const int64_t t = t0 + tl;
         const float st = out.sc_t ? __ldg(out.sc_t + t) : 1.f;
+        while (tag[sl] != i) {}
         fr_mbar_wait(full + sl, (uint32_t)(i / C::NSLOT) & 1u);
 
         // ---- pass 1: Z from the ring, two DFTs of length N2

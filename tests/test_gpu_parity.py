@@ -159,6 +159,35 @@ def test_edge_shapes_random_rings(M, T, R, Q, H):
     _check_all(_gpu_path(A, B, w, U, H), X_ref)
 
 
+@pytest.mark.parametrize("Q", [32, 64, 128, 256, 512, 1024])
+def test_many_items_per_cta_all_modes(Q):
+    """Tens of FFT work items per CTA (so every slot of the Step-3 TMA ring is reused many times and
+    warp groups drift apart): sampled landscapes against the oracle, and the per-pair / per-image
+    argmax outputs against the landscape the same launch configuration produced."""
+    M, T, R, H = 600, 300, 16, 4
+    rng = np.random.default_rng(Q)
+    A = (rng.standard_normal((M, R, Q)) + 1j * rng.standard_normal((M, R, Q))).astype(np.complex64)
+    B = (rng.standard_normal((T, R, Q)) + 1j * rng.standard_normal((T, R, Q))).astype(np.complex64)
+    k, w = radial_grid(R)
+    U, _ = api.build_basis(cuda(B), w, H)
+    out = _gpu_path(A, B, w, U, H)
+    m = rng.integers(0, M, 160)
+    t = rng.integers(0, T, 160)
+    X_ref = ref.landscape_rank(A, B, w, U, m, t).real
+    tol_abs = TOL_FP32 * np.abs(X_ref).max()
+    assert np.abs(out["X"][m, t] - X_ref).max() <= tol_abs
+    assert np.abs(out["val"][m, t] - X_ref.max(-1)).max() <= tol_abs
+    assert_argmax_gated(out["k"][m, t], X_ref, tol_abs)
+    # every pair: argmax outputs agree with the landscape kernel's own values
+    X = out["X"]
+    assert np.abs(out["val"] - X.max(-1)).max() <= 1e-6 * np.abs(X).max()
+    kk = out["k"]
+    assert np.all(X[np.arange(M)[:, None], np.arange(T)[None, :], kk] >= X.max(-1) - 1e-6 * np.abs(X).max())
+    v, ti, ki = out["img"]
+    assert np.abs(v - out["val"].max(1)).max() <= 1e-6 * np.abs(X).max()
+    assert np.all(out["val"][np.arange(M), ti] == v)
+
+
 def test_small_workspace_many_chunks():
     """Minimum workspace forces many small chunks: results identical to one big chunk."""
     d = make_dataset("small", M=200, T=150)
