@@ -166,14 +166,16 @@ static cudaError_t make_tmap_any(int LOGN, CUtensorMap *tm, const float *Upk, in
 }
 
 static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const CUtensorMap &tm, int64_t Mc, int64_t Tc,
-                                  int64_t m0, int64_t t0, int64_t mcv, int64_t tcv, const FftOut &o) {
+                                  int64_t m0, int64_t t0, int64_t mcv, int64_t tcv, const FftOut &o, float *Upk) {
+    static const bool discard = [] { const char *e = getenv("RSVD_NO_DISCARD"); return !(e && atoi(e)); }();
+    float *dU = discard ? Upk : nullptr;
     if (use_fft2(LOGN)) {
         switch (LOGN) {
-            case 4: return launch_fft2<4>(mode, s, tm, m0, t0, mcv, tcv, o);
-            case 5: return launch_fft2<5>(mode, s, tm, m0, t0, mcv, tcv, o);
-            case 6: return launch_fft2<6>(mode, s, tm, m0, t0, mcv, tcv, o);
-            case 7: return launch_fft2<7>(mode, s, tm, m0, t0, mcv, tcv, o);
-            default: return launch_fft2<8>(mode, s, tm, m0, t0, mcv, tcv, o);
+            case 4: return launch_fft2<4>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
+            case 5: return launch_fft2<5>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
+            case 6: return launch_fft2<6>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
+            case 7: return launch_fft2<7>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
+            default: return launch_fft2<8>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
         }
     }
     switch (LOGN) {
@@ -236,7 +238,7 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
                 if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "contract launch");
             }
             cudaEvent_t ev1 = timed ? timing_event(s) : nullptr;
-            e = launch_fft_any(LOGN, a.mode, s, tmap, Mc, Tc, m0, t0, mcv, tcv, o);
+            e = launch_fft_any(LOGN, a.mode, s, tmap, Mc, Tc, m0, t0, mcv, tcv, o, Upk);
             if (e != cudaSuccess) return cuda_check(e, "fft_reduce launch");
             count_launches(2);
             if (timed) {

@@ -59,7 +59,9 @@ __device__ __forceinline__ void z_pair(float2 a, float2 b, float2 w, float2 &zr,
 template <int LOGN, int MODE>
 __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                                int64_t m0, int64_t t0, int64_t mcv,
-                                                                               int64_t tcv, FftOut out) {
+                                                                               int64_t tcv, FftOut out,
+                                                                               float *__restrict__ Upk, int64_t Mc,
+                                                                               int64_t Tc) {
     using C = Fft2Cfg<LOGN>;
     constexpr int N = C::N, Q = C::Q, N1 = C::N1, N2 = C::N2, TB = C::TB, SZ = C::SZ, G = C::G, GT = C::GT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -135,6 +137,13 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
         const float st = out.sc_t ? __ldg(out.sc_t + t) : 1.f;
         while (tag[sl] != i) {}
         fr_mbar_wait(full + sl, (uint32_t)(i / C::NSLOT) & 1u);
+        // the item's 2N spectrum rows (one 128-B line each: 32 images x fp32) are now in shared memory
+        // and dead in HBM terms: drop them from L2 without write-back (the next chunk's contraction
+        // rewrites every line before it is read again)
+        if (Upk) {
+            for (int r = gt; r < C::ROWS; r += GT)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(Upk + ((int64_t)r * Tc + tl) * Mc + mb0) : "memory");
+        }
 
         // ---- pass 1: Z from the ring, two DFTs of length N2
         float2 za[N2], zb[N2];
@@ -281,7 +290,7 @@ static cudaError_t make_spectrum_tmap2(CUtensorMap *tm, const float *Upk, int64_
 
 template <int LOGN, int MODE>
 static cudaError_t launch_fft2_mode(cudaStream_t s, const CUtensorMap &tm, int64_t m0, int64_t t0, int64_t mcv,
-                                    int64_t tcv, const FftOut &out) {
+                                    int64_t tcv, const FftOut &out, float *Upk, int64_t Mc, int64_t Tc) {
     using C = Fft2Cfg<LOGN>;
     const size_t smem = C::smem_bytes();
     static bool attr = false;
@@ -303,15 +312,15 @@ static cudaError_t launch_fft2_mode(cudaStream_t s, const CUtensorMap &tm, int64
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, fft2_reduce_kernel<LOGN, MODE>, tm, m0, t0, mcv, tcv, out);
+    return cudaLaunchKernelEx(&cfg, fft2_reduce_kernel<LOGN, MODE>, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
 }
 
 template <int LOGN>
 static cudaError_t launch_fft2(int mode, cudaStream_t s, const CUtensorMap &tm, int64_t m0, int64_t t0, int64_t mcv,
-                               int64_t tcv, const FftOut &out) {
-    if (mode == MODE_PAIR) return launch_fft2_mode<LOGN, MODE_PAIR>(s, tm, m0, t0, mcv, tcv, out);
-    if (mode == MODE_IMAGE) return launch_fft2_mode<LOGN, MODE_IMAGE>(s, tm, m0, t0, mcv, tcv, out);
-    return launch_fft2_mode<LOGN, MODE_LANDSCAPE>(s, tm, m0, t0, mcv, tcv, out);
+                               int64_t tcv, const FftOut &out, float *Upk, int64_t Mc, int64_t Tc) {
+    if (mode == MODE_PAIR) return launch_fft2_mode<LOGN, MODE_PAIR>(s, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
+    if (mode == MODE_IMAGE) return launch_fft2_mode<LOGN, MODE_IMAGE>(s, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
+    return launch_fft2_mode<LOGN, MODE_LANDSCAPE>(s, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
 }
 
 }  // namespace rsvd
