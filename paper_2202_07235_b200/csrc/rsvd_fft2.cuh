@@ -135,6 +135,17 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
         const int tl = item / nmb, mb0 = (item - tl * nmb) * TB;
         const int64_t t = t0 + tl;
         const float st = out.sc_t ? __ldg(out.sc_t + t) : 1.f;
+        // per-image side data of this item's pass-2 tasks, fetched now so its latency hides behind pass 1
+        uint32_t stale[C::P2_PER];                             // MODE_IMAGE: the image's current key
+        float smv[C::P2_PER];                                  // image operand scale (TC path)
+#pragma unroll
+        for (int j = 0; j < C::P2_PER; ++j) {
+            const int ml = mb0 + (gt + GT * j) / N2;
+            const bool ok = ml < mcv;
+            smv[j] = (ok && out.sc_m) ? __ldg(out.sc_m + m0 + ml) : 1.f;
+            stale[j] = 0u;
+            if constexpr (MODE == MODE_IMAGE) stale[j] = ok ? (uint32_t)(__ldcg(out.best_key + m0 + ml) >> 32) : 0u;
+        }
         while (tag[sl] != i) {}
         fr_mbar_wait(full + sl, (uint32_t)(i / C::NSLOT) & 1u);
         // the item's 2N spectrum rows (one 128-B line each: 32 images x fp32) are now in shared memory
@@ -207,14 +218,6 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(i + C::NSLOT);
         }
-        uint32_t stale[C::P2_PER];                             // MODE_IMAGE: image keys
-        if constexpr (MODE == MODE_IMAGE) {
-#pragma unroll
-            for (int j = 0; j < C::P2_PER; ++j) {
-                const int ml = mb0 + (gt + GT * j) / N2;
-                stale[j] = ml < mcv ? (uint32_t)(__ldcg(out.best_key + m0 + ml) >> 32) : 0u;
-            }
-        }
 #pragma unroll
         for (int j = 0; j < C::P2_PER; ++j) {
             const int task = gt + GT * j;
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
             const int64_t ml = mb0 + p;
             const bool valid = ml < mcv;
             const int64_t m = m0 + ml;
-            const float mul = PI / (((valid && out.sc_m) ? __ldg(out.sc_m + m) : 1.f) * st);
+            const float mul = PI / (smv[j] * st);
             if constexpr (MODE == MODE_LANDSCAPE) {
                 if (valid) {
                     float2 *dst = reinterpret_cast<float2 *>(out.X + m * out.ld_m + t * out.ld_t);

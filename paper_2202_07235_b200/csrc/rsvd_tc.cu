@@ -395,59 +395,124 @@ __device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, i
     }
 }
 
+// Step 1 for the TC layout, one CTA per row: rings -> principal rings (psi-space projection with the
+// fp64 basis rounded to fp32) -> length-Q DFT -> row scale -> fp16 hi/lo operand rows.  The row's R
+// rings stream through shared memory in slabs of whole rings with double-buffered bulk copies
+// (cp.async.bulk + mbarrier), so loads run ahead of the projection FMAs.
+constexpr int CPT_THREADS = 256;
+
 template <int LOGQ, int HC>
-__global__ void __launch_bounds__(256) compress_tc_kernel(const float2 *__restrict__ rings, int64_t n, int R,
-                                                          const double *__restrict__ w, const double *__restrict__ U,
-                                                          int H, int side, int KB, int64_t op_rows,
-                                                          __half *__restrict__ ops, float *__restrict__ scales) {
+__global__ void __launch_bounds__(CPT_THREADS, 1) compress_tc_kernel(const float2 *__restrict__ rings, int64_t n, int R,
+                                                                     const double *__restrict__ w,
+                                                                     const double *__restrict__ U, int H, int side,
+                                                                     int KB, int64_t op_rows, int slab_rings,
+                                                                     __half *__restrict__ ops, float *__restrict__ scales) {
     constexpr int Q = 1 << LOGQ;
     constexpr int L = 32;
     constexpr int E = Q / L;
+    constexpr int JPT = Q >= CPT_THREADS ? Q / CPT_THREADS : 1;      // angular samples per thread
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2 *tw = reinterpret_cast<float2 *>(smem_raw);       // [E][L]
-    float2 *at = tw + E * L;                                 // [H][Q]
-    float *up = reinterpret_cast<float *>(at + (size_t)H * Q);   // [R][HC]
-    float *red = up + (size_t)R * HC;                        // [33]
+    const int slab_f2 = slab_rings * Q;
+    float2 *slab = reinterpret_cast<float2 *>(smem_raw);              // [2][slab_rings][Q]
+    float2 *tw = slab + 2 * slab_f2;                                  // [E][L]
+    float2 *at = tw + E * L;                                          // [H][Q]
+    float *up = reinterpret_cast<float *>(at + (size_t)H * Q);        // [R][HC]
+    float *red = up + (size_t)R * HC;                                 // [33]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(red + 34);           // [2] (8-byte aligned: 34 floats)
     const int64_t row = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < E * L; i += 256) tw[i] = twiddle_N(i % L, i / L, Q);
+    const float2 *ring = rings + row * (int64_t)R * Q;
+    const int nslab = (R + slab_rings - 1) / slab_rings;
+    auto issue = [&](int s, int buf) {                                // thread 0
+        const int r0 = s * slab_rings, nr = min(slab_rings, R - r0);
+        const uint32_t bytes = (uint32_t)nr * Q * 8u;
+        const uint32_t b = smem_u32(bar + buf);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(slab + (size_t)buf * slab_f2)),
+                     "l"(ring + (int64_t)r0 * Q), "r"(bytes), "r"(b)
+                     : "memory");
+    };
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar + 1)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < E * L; i += CPT_THREADS) tw[i] = twiddle_N(i % L, i / L, Q);
     float2 stw[clog2(L)];
     lane_stage_twiddles<L>(lane, stw);
-    const float2 *ring = rings + row * (int64_t)R * Q;
     const double invQ = 1.0 / (double)Q;
+    int ks = 0;                                                       // slabs consumed so far (all passes)
     for (int h0 = 0; h0 < H; h0 += HC) {
         const int hc = min(HC, H - h0);
         __syncthreads();
-        for (int i = tid; i < R * HC; i += 256) {
+        for (int i = tid; i < R * HC; i += CPT_THREADS) {
             const int r = i / HC, hh = i % HC;
             up[i] = (hh < hc) ? (float)(U[(int64_t)r * H + h0 + hh] * sqrt(w[r]) * invQ) : 0.f;
         }
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(0, ks & 1);
+            if (nslab > 1) issue(1, (ks + 1) & 1);
+        }
         __syncthreads();
-        for (int j = tid; j < Q; j += 256) {
-            float2 acc[HC];
+        float2 acc[JPT][HC];
 #pragma unroll
-            for (int hh = 0; hh < HC; ++hh) acc[hh] = make_float2(0.f, 0.f);
-#pragma unroll 4
-            for (int r = 0; r < R; ++r) {
-                const float2 a = __ldg(ring + (int64_t)r * Q + j);
-                const float4 *u4 = reinterpret_cast<const float4 *>(up + r * HC);
+        for (int jj = 0; jj < JPT; ++jj)
 #pragma unroll
-                for (int g = 0; g < HC / 4; ++g) {
-                    const float4 u = u4[g];
-                    acc[4 * g + 0].x = fmaf(u.x, a.x, acc[4 * g + 0].x); acc[4 * g + 0].y = fmaf(u.x, a.y, acc[4 * g + 0].y);
-                    acc[4 * g + 1].x = fmaf(u.y, a.x, acc[4 * g + 1].x); acc[4 * g + 1].y = fmaf(u.y, a.y, acc[4 * g + 1].y);
-                    acc[4 * g + 2].x = fmaf(u.z, a.x, acc[4 * g + 2].x); acc[4 * g + 2].y = fmaf(u.z, a.y, acc[4 * g + 2].y);
-                    acc[4 * g + 3].x = fmaf(u.w, a.x, acc[4 * g + 3].x); acc[4 * g + 3].y = fmaf(u.w, a.y, acc[4 * g + 3].y);
+            for (int hh = 0; hh < HC; ++hh) acc[jj][hh] = make_float2(0.f, 0.f);
+        for (int s = 0; s < nslab; ++s, ++ks) {
+            const int buf = ks & 1;
+            asm volatile(
+                "{\n\t.reg .pred p;\n"
+                "CPT_WAIT:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                "@!p bra CPT_WAIT;\n\t}" ::"r"(smem_u32(bar + buf)),
+                "r"((uint32_t)(ks >> 1) & 1u)
+                : "memory");
+            const float2 *sl = slab + (size_t)buf * slab_f2;
+            const int r0 = s * slab_rings, nr = min(slab_rings, R - r0);
+            if (tid < Q) {
+#pragma unroll 2
+                for (int rr = 0; rr < nr; ++rr) {
+                    const float4 *u4 = reinterpret_cast<const float4 *>(up + (r0 + rr) * HC);
+                    float2 a[JPT];
+#pragma unroll
+                    for (int jj = 0; jj < JPT; ++jj) a[jj] = sl[rr * Q + tid + CPT_THREADS * jj];
+#pragma unroll
+                    for (int g = 0; g < HC / 4; ++g) {
+                        const float4 u = u4[g];
+#pragma unroll
+                        for (int jj = 0; jj < JPT; ++jj) {
+                            acc[jj][4 * g + 0].x = fmaf(u.x, a[jj].x, acc[jj][4 * g + 0].x);
+                            acc[jj][4 * g + 0].y = fmaf(u.x, a[jj].y, acc[jj][4 * g + 0].y);
+                            acc[jj][4 * g + 1].x = fmaf(u.y, a[jj].x, acc[jj][4 * g + 1].x);
+                            acc[jj][4 * g + 1].y = fmaf(u.y, a[jj].y, acc[jj][4 * g + 1].y);
+                            acc[jj][4 * g + 2].x = fmaf(u.z, a[jj].x, acc[jj][4 * g + 2].x);
+                            acc[jj][4 * g + 2].y = fmaf(u.z, a[jj].y, acc[jj][4 * g + 2].y);
+                            acc[jj][4 * g + 3].x = fmaf(u.w, a[jj].x, acc[jj][4 * g + 3].x);
+                            acc[jj][4 * g + 3].y = fmaf(u.w, a[jj].y, acc[jj][4 * g + 3].y);
+                        }
+                    }
                 }
             }
+            __syncthreads();                                          // slab buffer free
+            if (tid == 0 && s + 2 < nslab) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(s + 2, buf);
+            }
+        }
+        if (tid < Q) {
 #pragma unroll
-            for (int hh = 0; hh < HC; ++hh)
-                if (hh < hc) at[(h0 + hh) * Q + j] = acc[hh];
+            for (int jj = 0; jj < JPT; ++jj)
+#pragma unroll
+                for (int hh = 0; hh < HC; ++hh)
+                    if (hh < hc) at[(h0 + hh) * Q + tid + CPT_THREADS * jj] = acc[jj][hh];
         }
     }
     __syncthreads();
     // in-place length-Q forward DFT of each principal ring, natural order
-    for (int h = warp; h < H; h += 8) {
+    for (int h = warp; h < H; h += CPT_THREADS / 32) {
         float2 v[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = at[h * Q + lane + L * e];
@@ -465,13 +530,27 @@ __global__ void __launch_bounds__(256) compress_tc_kernel(const float2 *__restri
 
 // principal rings per projection pass: the whole H in one pass up to 32 (one read of the rings)
 static int compress_hc(int H) { return H <= 8 ? 8 : (H <= 16 ? 16 : (H <= 24 ? 24 : 32)); }
-
+static size_t compress_fixed_smem(int Q, int H, int R) {
+    return (size_t)Q * sizeof(float2) + (size_t)H * Q * sizeof(float2) + (size_t)R * compress_hc(H) * sizeof(float) +
+           34 * 4 + 16;
+}
+constexpr size_t CPT_SMEM_BUDGET = 200 * 1024;
+// rings per slab: the largest of 32 / 16 / 8 KB slabs (at least one ring) that fits the budget
+static int compress_slab_rings(int Q, int H, int R) {
+    const size_t ring = (size_t)Q * sizeof(float2);
+    for (size_t slab : {32768u, 16384u, 8192u}) {
+        const size_t sb = std::max(slab, ring);
+        if (compress_fixed_smem(Q, H, R) + 2 * sb <= CPT_SMEM_BUDGET) return (int)std::min<size_t>(sb / ring, (size_t)R);
+    }
+    return 0;
+}
 size_t compress_tc_smem(int Q, int H, int R) {
-    return (size_t)Q * sizeof(float2) + (size_t)H * Q * sizeof(float2) + (size_t)R * compress_hc(H) * sizeof(float) + 33 * 4;
+    const int sr = compress_slab_rings(Q, H, R);
+    return compress_fixed_smem(Q, H, R) + 2 * (size_t)std::max(sr, 1) * Q * sizeof(float2);
 }
 
 // TC layout needs the whole [H][Q] coefficient block of a row in shared memory (R <= 256).
-bool tc_supported(int Q, int H) { return compress_tc_smem(Q, H, 256) <= 200 * 1024; }
+bool tc_supported(int Q, int H) { return compress_slab_rings(Q, H, 256) > 0; }
 
 static int g_path = -1;
 int resolve_path(int Q, int H) {
@@ -489,13 +568,16 @@ void set_path(int p) { g_path = (p == PATH_SIMT || p == PATH_TC) ? p : PATH_AUTO
 template <int LOGQ, int HC>
 static cudaError_t launch_compress_tc_qh(const float2 *rings, int64_t n, int R, const double *w, const double *U, int H,
                                          int side, void *blocks, cudaStream_t s) {
-    const size_t smem = compress_tc_smem(1 << LOGQ, H, R);
+    const int Q = 1 << LOGQ;
+    const int sr = compress_slab_rings(Q, H, R);
+    if (sr < 1) return cudaErrorInvalidValue;
+    const size_t smem = compress_tc_smem(Q, H, R);
     cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel<LOGQ, HC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int Q = 1 << LOGQ;
     float *scales = const_cast<float *>(tc_scales(blocks, n, Q, H, side));
-    compress_tc_kernel<LOGQ, HC><<<(unsigned)n, 256, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H), tc_op_rows(n, side),
-                                                                reinterpret_cast<__half *>(blocks), scales);
+    compress_tc_kernel<LOGQ, HC><<<(unsigned)n, CPT_THREADS, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H),
+                                                                        tc_op_rows(n, side), sr,
+                                                                        reinterpret_cast<__half *>(blocks), scales);
     return cudaGetLastError();
 }
 template <int LOGQ>
