@@ -13,11 +13,13 @@
 // pair's result by 1 / (s_m s_t) (exact).
 //
 // Operand layout (opaque; written by compress_tc_kernel), per side, fp16:
-//   op[q][kb][part][row][32],  q = 0..N (N = Q/2), kb < KB = ceil(4H/32), part 0 = hi, 1 = lo,
+//   op[q][kb][row][64],  q = 0..N (N = Q/2), kb < KB = ceil(4H/32); elements 0-31 of a row are the
+//   hi parts of the k-block's 32 reals, 32-63 the lo parts (one 128-B line per row and k-block),
 //   image rows: image m -> rows (m/64)*128 + m%64 (A_re) and + 64 (A_im); 2 * round_up(M,128) rows;
 //   template rows: t; round_up(T,256) rows.  Then float scale[rows_pad] (s per image / template).
-// A 5-D tensor map (32 x rows x 2 x KB x (N+1)) with SWIZZLE_64B loads one (q, kb) box of 128 rows
-// x 32 fp16 x {hi,lo} (16 KB) straight into the UMMA K-major SW64 layout.
+// A 4-D tensor map (64 x rows x KB x (N+1)) with SWIZZLE_128B loads one (q, kb) box of 128 rows x
+// 128 B (16 KB, full-line TMA requests) straight into the UMMA K-major SW128 layout, where hi and lo
+// are the two 32-element K halves of the same tile (descriptor start +0 / +64 B).
 //
 // contract_tc_kernel: one CTA pair per (128-image x 256-template tile, group of q), 6 warps per CTA:
 //   warp 0    TMA producer (both CTAs: own 128 A rows + own half of the 256 B rows; completion on the
@@ -43,8 +45,7 @@ constexpr int TC_THREADS = 6 * 32;
 constexpr int TC_STAGES = 6;
 constexpr int TC_PIMG = 128;                        // images per CTA pair (64 per CTA)
 constexpr int TC_TT = 256;                          // templates per CTA pair (128 per CTA)
-constexpr uint32_t TC_PART_BYTES = 128u * 64u;      // 128 rows x 32 fp16
-constexpr uint32_t TC_OPND_BYTES = 2 * TC_PART_BYTES;
+constexpr uint32_t TC_OPND_BYTES = 128u * 128u;     // 128 rows x (32 hi + 32 lo) fp16
 constexpr uint32_t TC_STAGE_BYTES = 2 * TC_OPND_BYTES;    // A + B: 32 KB
 constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_BYTES + 1024 + 256;
 
@@ -68,14 +69,14 @@ const float *tc_scales(const void *blocks, int64_t rows, int Q, int H, int side)
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// UMMA shared-memory descriptor, K-major, SWIZZLE_64B: 8-row atoms of 64-byte rows, 512 B apart.
-__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: 8-row atoms of 128-byte rows, 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr & 0x3FFFF) >> 4);          // start address
     d |= (uint64_t)1 << 16;                           // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(512 >> 4) << 32;                  // SBO: 8-row atoms 512 B apart
+    d |= (uint64_t)(1024 >> 4) << 32;                 // SBO: 8-row atoms 1024 B apart
     d |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
-    d |= (uint64_t)4 << 61;                           // SWIZZLE_64B
+    d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
     return d;
 }
 
@@ -120,12 +121,12 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void tma_load_5d_pair(uint32_t dst, const CUtensorMap *tm, int c0, int c1, int c2, int c3,
-                                                 int c4, uint32_t mbar_cluster) {
+__device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap *tm, int c0, int c1, int c2, int c3,
+                                                 uint32_t mbar_cluster) {
     asm volatile(
-        "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(mbar_cluster)
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar_cluster)
         : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -215,8 +216,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
                         if (rank == 0) mbar_expect_tx(full + s, 2 * TC_STAGE_BYTES);
                         const uint32_t fbl = rank == 0 ? fb : mapa_rank(fb, 0);
                         const uint32_t dst = smem_u32(base + s * TC_STAGE_BYTES);
-                        tma_load_5d_pair(dst, &tmA, 0, rowA, 0, kb, q, fbl);
-                        tma_load_5d_pair(dst + TC_OPND_BYTES, &tmB, 0, rowB, 0, kb, q, fbl);
+                        tma_load_4d_pair(dst, &tmA, 0, rowA, kb, q, fbl);
+                        tma_load_4d_pair(dst + TC_OPND_BYTES, &tmB, 0, rowB, kb, q, fbl);
                     }
                 }
             }
@@ -244,8 +245,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
                         mbar_wait(full + s, (uint32_t)(it / TC_STAGES) & 1u);
                         tc_fence_after();
                         const uint32_t sa = smem_u32(base + s * TC_STAGE_BYTES);
-                        const uint64_t a_hi = sw64_desc(sa), a_lo = sw64_desc(sa + TC_PART_BYTES);
-                        const uint64_t b_hi = sw64_desc(sa + TC_OPND_BYTES), b_lo = sw64_desc(sa + TC_OPND_BYTES + TC_PART_BYTES);
+                        const uint64_t a_hi = sw128_desc(sa), a_lo = a_hi + 4;          // lo: K half at +64 B
+                        const uint64_t b_hi = sw128_desc(sa + TC_OPND_BYTES), b_lo = b_hi + 4;
                         const int nst = min(2, steps - 2 * kb);
                         for (int k = 0; k < nst; ++k) {
                             const uint64_t o = (uint64_t)(2 * k);          // +32 B per K=16 fp16 step
@@ -370,13 +371,13 @@ __device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, i
             }
             c[jj] = make_float2(a.x * s, a.y * s);
         }
-        const int64_t sub = ((int64_t)q * KB + kb) * 2;   // (q, kb, part 0)
+        const int64_t sub = (int64_t)q * KB + kb;         // (q, kb): rows of 64 fp16 (hi | lo)
         if (side == RSVD_SIDE_TEMPLATE) {
             __align__(16) __half hi[8], lo[8];
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) { split_h(c[jj].x, hi[2 * jj], lo[2 * jj]); split_h(c[jj].y, hi[2 * jj + 1], lo[2 * jj + 1]); }
-            *reinterpret_cast<uint4 *>(ops + ((sub + 0) * op_rows + row) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(hi);
-            *reinterpret_cast<uint4 *>(ops + ((sub + 1) * op_rows + row) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(lo);
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + row) * 64 + qu * 8) = *reinterpret_cast<uint4 *>(hi);
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + row) * 64 + 32 + qu * 8) = *reinterpret_cast<uint4 *>(lo);
         } else {
             const int64_t rre = (row / 64) * 128 + row % 64, rim = rre + 64;
             __align__(16) __half rh[8], rl[8], ih[8], il[8];
@@ -387,10 +388,10 @@ __device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, i
                 split_h(c[jj].y, ih[2 * jj], il[2 * jj]);            // A_im = (Im a, Re a)
                 split_h(c[jj].x, ih[2 * jj + 1], il[2 * jj + 1]);
             }
-            *reinterpret_cast<uint4 *>(ops + ((sub + 0) * op_rows + rre) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(rh);
-            *reinterpret_cast<uint4 *>(ops + ((sub + 1) * op_rows + rre) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(rl);
-            *reinterpret_cast<uint4 *>(ops + ((sub + 0) * op_rows + rim) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(ih);
-            *reinterpret_cast<uint4 *>(ops + ((sub + 1) * op_rows + rim) * 32 + qu * 8) = *reinterpret_cast<uint4 *>(il);
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rre) * 64 + qu * 8) = *reinterpret_cast<uint4 *>(rh);
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rre) * 64 + 32 + qu * 8) = *reinterpret_cast<uint4 *>(rl);
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rim) * 64 + qu * 8) = *reinterpret_cast<uint4 *>(ih);
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rim) * 64 + 32 + qu * 8) = *reinterpret_cast<uint4 *>(il);
         }
     }
 }
@@ -616,9 +617,9 @@ __global__ void unpack_tc_kernel(const __half *__restrict__ ops, const float *__
     const int j = q <= N ? h : H + h;
     const int kb = j / 16, e = 2 * (j % 16);
     const int64_t r = side == RSVD_SIDE_TEMPLATE ? row : (row / 64) * 128 + row % 64;
-    const int64_t sub = ((int64_t)qq * KB + kb) * 2;
-    const __half *hi = ops + (sub * op_rows + r) * 32 + e;
-    const __half *lo = ops + ((sub + 1) * op_rows + r) * 32 + e;
+    const int64_t sub = (int64_t)qq * KB + kb;
+    const __half *hi = ops + (sub * op_rows + r) * 64 + e;
+    const __half *lo = hi + 32;
     const float inv = 1.f / scales[row];
     float x = (__half2float(hi[0]) + __half2float(lo[0])) * inv;
     float y = (__half2float(hi[1]) + __half2float(lo[1])) * inv;
@@ -652,19 +653,18 @@ static PFN_encodeTiled_tc encode_fn() {
     return fn;
 }
 
-// 5-D map of one side's operand rows: (k 32, row, part 2, kb, q), box (32, 128, 2, 1, 1), SWIZZLE_64B.
+// 4-D map of one side's operand rows: (64 fp16 = hi | lo, row, kb, q), box (64, 128, 1, 1), SWIZZLE_128B.
 cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t rows, int Q, int H, int side) {
     PFN_encodeTiled_tc enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
     const int64_t op_rows = tc_op_rows(rows, side);
     const int KB = tc_kb(H);
-    const cuuint64_t dims[5] = {32, (cuuint64_t)op_rows, 2, (cuuint64_t)KB, (cuuint64_t)(Q / 2 + 1)};
-    const cuuint64_t strides[4] = {64, (cuuint64_t)op_rows * 64, (cuuint64_t)op_rows * 128,
-                                   (cuuint64_t)op_rows * 128 * KB};
-    const cuuint32_t box[5] = {32, 128, 2, 1, 1};
-    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<void *>(blocks), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+    const cuuint64_t dims[4] = {64, (cuuint64_t)op_rows, (cuuint64_t)KB, (cuuint64_t)(Q / 2 + 1)};
+    const cuuint64_t strides[3] = {128, (cuuint64_t)op_rows * 128, (cuuint64_t)op_rows * 128 * KB};
+    const cuuint32_t box[4] = {64, 128, 1, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void *>(blocks), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
