@@ -122,11 +122,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap *tm, int c0, int c1, int c2, int c3,
-                                                 uint32_t mbar_cluster) {
+                                                 uint32_t mbar_cluster, uint64_t policy) {
     asm volatile(
-        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar_cluster)
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar_cluster), "l"(policy)
         : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -201,6 +201,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+            // chunks run template-tile outer / image inner: a chunk's template operands are re-read by
+            // every following chunk of the same template tile, image operands by none of them
+            uint64_t pol_stream, pol_keep;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
             int it = 0;
             for (int item = cl; item < nitems; item += ncl) {
                 const int tile = item / nqg, qgi = item - tile * nqg;
@@ -216,8 +221,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
                         if (rank == 0) mbar_expect_tx(full + s, 2 * TC_STAGE_BYTES);
                         const uint32_t fbl = rank == 0 ? fb : mapa_rank(fb, 0);
                         const uint32_t dst = smem_u32(base + s * TC_STAGE_BYTES);
-                        tma_load_4d_pair(dst, &tmA, 0, rowA, kb, q, fbl);
-                        tma_load_4d_pair(dst + TC_OPND_BYTES, &tmB, 0, rowB, kb, q, fbl);
+                        tma_load_4d_pair(dst, &tmA, 0, rowA, kb, q, fbl, pol_stream);
+                        tma_load_4d_pair(dst + TC_OPND_BYTES, &tmB, 0, rowB, kb, q, fbl, pol_keep);
                     }
                 }
             }
