@@ -80,8 +80,9 @@ void householder_tridiag(int n, std::vector<double> &A, std::vector<double> &Z,
     for (int i = 0; i + 1 < n; ++i) e[i] = A[(size_t)(i + 1) * n + i];
 }
 
-// Implicit symmetric QR on the tridiagonal (d, e), accumulating rotations into Z's columns.
-bool tridiag_qr(int n, std::vector<double> &d, std::vector<double> &e, std::vector<double> &Z) {
+// Implicit symmetric QR on the tridiagonal (d, e), accumulating rotations into the columns of Z,
+// held transposed (Zt[col][row]) so that each rotation updates two contiguous vectors.
+bool tridiag_qr(int n, std::vector<double> &d, std::vector<double> &e, std::vector<double> &Zt) {
     if (n <= 1) return true;
     const double eps = 2.220446049250313e-16;
     double anorm = 0.0;
@@ -121,11 +122,12 @@ bool tridiag_qr(int n, std::vector<double> &d, std::vector<double> &e, std::vect
                 bulge = -s * e[k + 1];
                 e[k + 1] = c * e[k + 1];
             }
+            double *__restrict__ zk = &Zt[(size_t)k * n];
+            double *__restrict__ zk1 = &Zt[(size_t)(k + 1) * n];
             for (int row = 0; row < n; ++row) {
-                double *zr = &Z[(size_t)row * n];
-                const double zk = zr[k], zk1 = zr[k + 1];
-                zr[k] = c * zk - s * zk1;
-                zr[k + 1] = s * zk + c * zk1;
+                const double a = zk[row], b = zk1[row];
+                zk[row] = c * a - s * b;
+                zk1[row] = s * a + c * b;
             }
         }
     }
@@ -149,7 +151,10 @@ extern "C" rsvd_status rsvd_eigen_basis(const double *C, int32_t R, int32_t H, d
         }
     std::vector<double> Z, d, e;
     householder_tridiag(n, A, Z, d, e);
-    if (!tridiag_qr(n, d, e, Z)) return fail(RSVD_ERR_NUMERIC, "eigen-solver did not converge");
+    std::vector<double> Zt((size_t)n * n);
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c < n; ++c) Zt[(size_t)c * n + r] = Z[(size_t)r * n + c];
+    if (!tridiag_qr(n, d, e, Zt)) return fail(RSVD_ERR_NUMERIC, "eigen-solver did not converge");
     std::vector<int> order(n);
     std::iota(order.begin(), order.end(), 0);
     // stable descending sort (insertion sort: n <= 256, deterministic)
@@ -165,13 +170,13 @@ extern "C" rsvd_status rsvd_eigen_basis(const double *C, int32_t R, int32_t H, d
         int imax = 0;
         double amax = -1.0;
         for (int r = 0; r < n; ++r) {
-            const double z = Z[(size_t)r * n + col];
+            const double z = Zt[(size_t)col * n + r];
             nrm += z * z;
             if (std::fabs(z) > amax) { amax = std::fabs(z); imax = r; }
         }
         nrm = std::sqrt(nrm);
-        const double sgn = (Z[(size_t)imax * n + col] < 0) ? -1.0 : 1.0;
-        for (int r = 0; r < n; ++r) U[(size_t)r * H + h] = sgn * Z[(size_t)r * n + col] / nrm;
+        const double sgn = (Zt[(size_t)col * n + imax] < 0) ? -1.0 : 1.0;
+        for (int r = 0; r < n; ++r) U[(size_t)r * H + h] = sgn * Zt[(size_t)col * n + r] / nrm;
     }
     if (lambda)
         for (int i = 0; i < n; ++i) lambda[i] = d[order[i]];
