@@ -405,10 +405,11 @@ __device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, i
 // fp64 basis rounded to fp32) -> length-Q DFT -> row scale -> fp16 hi/lo operand rows.  The row's R
 // rings stream through shared memory in slabs of whole rings with double-buffered bulk copies
 // (cp.async.bulk + mbarrier), so loads run ahead of the projection FMAs.
-constexpr int CPT_THREADS = 256;
+template <int Q>
+struct CptCfg { static constexpr int THREADS = Q >= 512 ? 512 : 256; };
 
 template <int LOGQ, int HC>
-__global__ void __launch_bounds__(CPT_THREADS, 1) compress_tc_kernel(const float2 *__restrict__ rings, int64_t n, int R,
+__global__ void __launch_bounds__(CptCfg<(1 << LOGQ)>::THREADS, 1) compress_tc_kernel(const float2 *__restrict__ rings, int64_t n, int R,
                                                                      const double *__restrict__ w,
                                                                      const double *__restrict__ U, int H, int side,
                                                                      int KB, int64_t op_rows, int slab_rings,
@@ -416,6 +417,7 @@ __global__ void __launch_bounds__(CPT_THREADS, 1) compress_tc_kernel(const float
     constexpr int Q = 1 << LOGQ;
     constexpr int L = 32;
     constexpr int E = Q / L;
+    constexpr int CPT_THREADS = CptCfg<Q>::THREADS;
     constexpr int JPT = Q >= CPT_THREADS ? Q / CPT_THREADS : 1;      // angular samples per thread
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int slab_f2 = slab_rings * Q;
@@ -581,7 +583,7 @@ static cudaError_t launch_compress_tc_qh(const float2 *rings, int64_t n, int R, 
     cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel<LOGQ, HC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     float *scales = const_cast<float *>(tc_scales(blocks, n, Q, H, side));
-    compress_tc_kernel<LOGQ, HC><<<(unsigned)n, CPT_THREADS, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H),
+    compress_tc_kernel<LOGQ, HC><<<(unsigned)n, CptCfg<(1 << LOGQ)>::THREADS, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H),
                                                                         tc_op_rows(n, side), sr,
                                                                         reinterpret_cast<__half *>(blocks), scales);
     return cudaGetLastError();
