@@ -367,20 +367,23 @@ def run_ours(args):
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for _ in range(args.e2e_steps):
-                d_img.copy_(h_img, non_blocking=True)
-                d_tmp.copy_(h_tmp, non_blocking=True)
-                (kk, val, tt, k), _ = step(d_img, d_tmp)
+                # public streamed path: copies of template / image blocks overlap partials, compress, align
+                (kk, val, tt, k), _ = pdist.align_from_host(h_img, h_tmp, T, t0, w_dev, H, d_img, d_tmp, work=work)
                 for h, d in zip(h_out, (val, tt, k)):
                     h.copy_(d, non_blocking=True)
             e1.record(stream)
             torch.cuda.synchronize()
             e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, world)
+            # the streamed result must equal the device-resident step's winners
+            same = bool(torch.equal(kk, out[0]))
             h2d = int(sum_over_ranks(h_img.numel() * 8 + h_tmp.numel() * 8, world))
             d2h = int(sum_over_ranks(M * 12, world))
             e2e = {"value": pairs / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": round(e2e_ms, 3),
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                   "path": "pinned host rings -> cudaMemcpyAsync -> basis/compress/align/combine -> "
-                           "winners (val,t,k) to pinned host"}
+                   "matches_device_step": same,
+                   "path": "pinned host rings -> paper_2202_07235_b200.dist.align_from_host (H2D of template / "
+                           "image blocks on a copy stream overlapped with partials, compress and per-block "
+                           "align) -> combine -> winners (val,t,k) to pinned host"}
             del h_img, h_tmp, d_img, d_tmp
         except Exception as exc:  # host memory etc.
             e2e = {"value": None, "unit": UNIT, "error": str(exc)[:200]}

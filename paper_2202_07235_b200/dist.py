@@ -76,6 +76,68 @@ def combine_keys(keys: torch.Tensor, Q: int, group=None):
     return api.combine_winners(keys.view(1, -1), Q)
 
 
+def align_from_host(h_images: torch.Tensor, h_tmpl_shard: torch.Tensor, T_total: int, t_offset: int, w_dev: torch.Tensor,
+                    H: int, d_images: torch.Tensor, d_tmpl: torch.Tensor, img_block: int = 2048,
+                    tmpl_block: int = 1024, work: torch.Tensor | None = None, group=None):
+    """The whole per-image path (rows a0-a4 + combine) from pinned HOST rings, with the host->device
+    copies overlapped with the computation instead of preceding it:
+
+      copy stream    template blocks, then image blocks, back to back (PCIe never idles);
+      compute stream kernel partials per template block as it lands -> (all-gather) -> reduce ->
+                     host eigen-solve -> compress the template shard -> for each image block as it
+                     lands: compress it and align it against the whole shard (per-image keys are
+                     independent, so blocks write disjoint key slices) -> (all-gather) -> combine.
+
+    h_images [M, R, Q] / h_tmpl_shard [T_loc, R, Q]: pinned complex64 host tensors; d_images /
+    d_tmpl: device buffers of the same shapes (caller-owned, reused across calls).  Returns
+    ((keys, val, t, k) on the device, U).  Same results as compressing/aligning everything at once."""
+    from . import api
+    dev = d_images.device
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    M, R, Q = h_images.shape
+    T_loc = h_tmpl_shard.shape[0]
+    chunk = api.kernel_chunk()
+    tmpl_block = max(chunk, (tmpl_block // chunk) * chunk)
+    img_block = max(128, (img_block // 128) * 128)
+    copy.wait_stream(comp)                                  # device buffers are free
+    t_ev, i_ev = [], []
+    with torch.cuda.stream(copy):
+        for b0 in range(0, T_loc, tmpl_block):
+            d_tmpl[b0:b0 + tmpl_block].copy_(h_tmpl_shard[b0:b0 + tmpl_block], non_blocking=True)
+            t_ev.append(torch.cuda.Event())
+            t_ev[-1].record(copy)
+        for b0 in range(0, M, img_block):
+            d_images[b0:b0 + img_block].copy_(h_images[b0:b0 + img_block], non_blocking=True)
+            i_ev.append(torch.cuda.Event())
+            i_ev[-1].record(copy)
+    # a0: partials per template block as it arrives (fixed global 32-template chunks)
+    nch = (T_loc + chunk - 1) // chunk
+    part = torch.empty((max(nch, 1), R, R), dtype=torch.float64, device=dev)
+    for i, b0 in enumerate(range(0, T_loc, tmpl_block)):
+        comp.wait_event(t_ev[i])
+        nb = min(tmpl_block, T_loc - b0)
+        api.kernel_partials(d_tmpl[b0:b0 + nb], out=part[b0 // chunk:(b0 + nb + chunk - 1) // chunk])
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        part = gather_chunk_partials(part[:nch], T_total, chunk, group)
+    C = api.kernel_reduce(part, T_total, Q, w_dev)
+    U, lam = api.eigen_basis(C.cpu().numpy(), H)           # host solve (syncs comp; copies keep going)
+    U_dev = torch.tensor(U, dtype=torch.float64, device=dev)
+    # a1 templates, then a1-a4 per image block
+    tb = api.compress(d_tmpl, w_dev, U_dev, api.SIDE_TEMPLATE) if T_loc else None
+    keys = torch.zeros(M, dtype=torch.int64, device=dev)
+    if work is None:
+        work = torch.empty(api.align_workspace_bytes(img_block, T_loc, Q, H) // 4, dtype=torch.float32, device=dev)
+    for i, b0 in enumerate(range(0, M, img_block)):
+        comp.wait_event(i_ev[i])
+        nb = min(img_block, M - b0)
+        ib = api.compress(d_images[b0:b0 + nb], w_dev, U_dev, api.SIDE_IMAGE)
+        if T_loc:
+            api.align_argmax(ib, nb, tb, T_loc, Q, H, api.PER_IMAGE, work, best_key=keys[b0:b0 + nb],
+                             t_offset=t_offset)
+    return combine_keys(keys, Q, group), U
+
+
 def pack_key_reference(val: np.ndarray, t: np.ndarray, k: np.ndarray, Q: int) -> np.ndarray:
     """Host mirror of the ABI's packed-key format (include/rsvd.h), for tests of the host logic:
     (ord(float32 val) << 32) | (0xFFFFFFFF - (t*Q + k)) as uint64."""

@@ -273,3 +273,25 @@ def test_error_paths():
                                  None) == 2
     assert lib.rsvd_align_argmax(b, 2, b, 2, 0, Q, H, 9, big.data_ptr(), big.numel() * 4, b, b, b, None) == 1
     assert len(lib.rsvd_last_error()) > 0
+
+
+def test_streamed_host_path_matches_device_path(contraction_path):
+    """dist.align_from_host (host->device copies of template / image blocks overlapped with the
+    compute) returns exactly the winners of the device-resident path, including ragged blocks."""
+    from paper_2202_07235_b200 import dist as pdist
+    d = make_dataset("small", M=700, T=300)
+    H, Q = 8, d.Q
+    w = d.w.contiguous()
+    h_img = d.images.cpu().pin_memory()
+    h_tmp = d.templates.cpu().pin_memory()
+    d_img, d_tmp = torch.empty_like(d.images), torch.empty_like(d.templates)
+    (keys, val, t, k), U = pdist.align_from_host(h_img, h_tmp, 300, 0, w, H, d_img, d_tmp, img_block=256,
+                                                   tmpl_block=64)
+    U2, _ = pdist.basis_from_shards(d.templates, 300, w, H)
+    assert np.array_equal(U, U2)
+    Ud = cuda(U2, torch.float64)
+    ib = api.compress(d.images, w, Ud, api.SIDE_IMAGE)
+    tb = api.compress(d.templates, w, Ud, api.SIDE_TEMPLATE)
+    work = torch.empty(api.align_workspace_bytes(700, 300, Q, H) // 4, dtype=torch.float32, device="cuda")
+    ref_keys = api.align_argmax(ib, 700, tb, 300, Q, H, api.PER_IMAGE, work)
+    assert torch.equal(keys, ref_keys)
