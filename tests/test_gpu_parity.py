@@ -279,7 +279,7 @@ def test_streamed_host_path_matches_device_path(contraction_path):
     """dist.align_from_host (host->device copies of template / image blocks overlapped with the
     compute) returns exactly the winners of the device-resident path, including ragged blocks."""
     from paper_2202_07235_b200 import dist as pdist
-    d = make_dataset("small", M=700, T=300)
+    d = make_dataset("small", M=700, T=300, device="cuda")
     H, Q = 8, d.Q
     w = d.w.contiguous()
     h_img = d.images.cpu().pin_memory()
