@@ -55,7 +55,7 @@ typedef enum { RSVD_PER_PAIR = 0, RSVD_PER_IMAGE = 1 } rsvd_reduce;
 
 /* Thread-local message describing the last non-OK status returned on this thread. */
 const char *rsvd_last_error(void);
-/* ABI version of this header (bumped when a signature or the block layout changes): 3. */
+/* ABI version of this header (bumped when a signature or the block layout changes): 4. */
 int32_t rsvd_abi_version(void);
 
 /* ------------------------------------------------------------------ sizes */
@@ -148,6 +148,29 @@ rsvd_status rsvd_align_argmax(const void *img_blocks, int64_t M, const void *tmp
 rsvd_status rsvd_align_landscape(const void *img_blocks, int64_t M, const void *tmpl_blocks,
                                  int64_t T, int32_t Q, int32_t H, void *work, int64_t work_bytes,
                                  float *X, int64_t ld_m, int64_t ld_t, rsvd_stream_t stream);
+
+/* ------------------------------------------------------------------ row f1: finer gamma (NEXT)
+ * "If a finer resolution in gamma is required then the array [of Fourier coefficients] can be
+ * zero-padded prior to the FFT".  Same as rsvd_align_argmax / rsvd_align_landscape
+ * but on the grid gamma_k = 2 pi k / Q_out, Q_out = Q * 2^p <= 1024 (Q_out == Q is the plain call):
+ *   Re X(gamma) = pi [ U_0 + 2 Re sum_{n=1}^{Q/2-1} e^{-i n gamma} U_n + U_{Q/2} cos(Q gamma / 2) ],
+ * U_n = S_n + conj(S_{Q-n}), i.e. the trigonometric interpolant with the Nyquist bin split
+ * symmetrically between +-Q/2 (reading G4); it equals the plain landscape at every
+ * gamma_{k 2^p}.  Indices k / packed keys / strides refer to the Q_out grid ((t_offset+T)*Q_out < 2^32
+ * for PER_IMAGE; ld_t >= Q_out).  work >= rsvd_align_min_workspace_bytes(Q_out).
+ * best_gamma (PER_PAIR only, device [M][T] float, may be NULL): 3-point parabolic refinement of the
+ *   first argmax k (SPEC.md argmax_refine): gamma = 2 pi (k + d) / Q_out, d = (y_{k-1} - y_{k+1}) /
+ *   (2 (y_{k-1} - 2 y_k + y_{k+1})) clamped to [-1/2, 1/2] (0 if the samples are not a strict peak),
+ *   neighbours cyclic, gamma in [0, 2 pi).  Non-PER_PAIR with best_gamma != NULL is RSVD_ERR_ARG. */
+rsvd_status rsvd_align_argmax_fine(const void *img_blocks, int64_t M, const void *tmpl_blocks,
+                                   int64_t T, int64_t t_offset, int32_t Q, int32_t H, int32_t Q_out,
+                                   rsvd_reduce mode, void *work, int64_t work_bytes, float *best_val,
+                                   int32_t *best_k, uint64_t *best_key, float *best_gamma,
+                                   rsvd_stream_t stream);
+rsvd_status rsvd_align_landscape_fine(const void *img_blocks, int64_t M, const void *tmpl_blocks,
+                                      int64_t T, int32_t Q, int32_t H, int32_t Q_out, void *work,
+                                      int64_t work_bytes, float *X, int64_t ld_m, int64_t ld_t,
+                                      rsvd_stream_t stream);
 
 /* ------------------------------------------------------------------ per-image winners
  * rsvd_winners_reset: keys[0..M) = 0 (below every real key).

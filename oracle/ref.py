@@ -25,6 +25,10 @@ O5 metrics             relative Frobenius error, Pearson correlation, backward-e
 P8 landscape_fb        2 pi sum_q e^{-2 pi i q k / Q} sum_r w_r conj(ahat[r,q]) bhat[r,q] with a
                        DIRECT (matrix) DFT -- Eq. image_innerproduct_0; used only
                        as a pin against O1.
+F1 landscape_rank_fine Re X at gamma_k = 2 pi k / Q_out from the rank-H coefficients, evaluated
+                       directly (no FFT): "zero-padded prior to the FFT" with the
+                       Nyquist bin split between +-Q/2 (reading G4).
+F1 argmax_refine       grid argmax + 3-point quadratic interpolation (SPEC.md argmax_refine).
 
 Parity pins for every function live in tests/test_oracle_pins.py.
 """
@@ -149,6 +153,50 @@ def landscape_fb(A, B, w, ia, ib) -> np.ndarray:
         S = (np.asarray(w)[:, None] * np.conj(ah) * bh).sum(axis=0)     # Step 1 (:358)
         out[p] = 2.0 * np.pi * (F @ S)                     # Step 2 (:359): sum_q e^{-i q gamma_k} S_q
     return out
+
+
+# ------------------------------------------------------------------------------------ F1
+def landscape_rank_fine(A, B, w, U, ia, ib, Q_out: int) -> np.ndarray:
+    """F1: Re X(gamma_k), gamma_k = 2 pi k / Q_out, of the rank-H landscape (real, [P, Q_out]).
+
+    Coefficients of the principal rings (eta_r = sqrt(w_r): G2) by a direct DFT,
+    Ahat[h, q] = (1/Q) sum_j at[h, j] e^{-2 pi i q j/Q} (G1); S_q = sum_h conj(Ahat[h,q]) Bhat[h,q]
+    (Step 1, :672); then the zero-padded transform (:363) evaluated term by term:
+      X(gamma) = 2 pi [ sum_{q=-Q/2+1}^{Q/2-1} e^{-i q gamma} S_q + cos(Q gamma / 2) S_{Q/2} ],
+    S_{-q} == S_{Q-q}; the unpaired bin Q/2 split symmetrically between +-Q/2 (reading G4)."""
+    ia, ib = _pairs(ia, ib)
+    AT = principal_rings(np.asarray(A)[ia], w, U)          # [P, H, Q]
+    BT = principal_rings(np.asarray(B)[ib], w, U)
+    Q = AT.shape[2]
+    j = np.arange(Q)
+    F = np.exp(-2j * np.pi * np.outer(j, j) / Q)           # F[q, j]
+    Ah = AT @ F.T / Q                                      # [P, H, q]
+    Bh = BT @ F.T / Q
+    S = (np.conj(Ah) * Bh).sum(axis=1)                     # [P, q]
+    N = Q // 2
+    gam = 2.0 * np.pi * np.arange(Q_out) / Q_out
+    qs = np.concatenate([np.arange(0, N), np.arange(-N + 1, 0)])       # signed frequencies, Nyquist apart
+    cols = np.concatenate([np.arange(0, N), np.arange(N + 1, Q)])
+    E = np.exp(-1j * np.outer(qs, gam))                    # [freq, gamma]
+    X = S[:, cols] @ E + S[:, N][:, None] * np.cos(N * gam)[None, :]
+    return (2.0 * np.pi * X).real
+
+
+def argmax_refine(x: np.ndarray) -> np.ndarray:
+    """SPEC.md argmax_refine along the last axis: gamma = 2 pi (k + d) / Q, k the first argmax,
+    d = (y[k-1] - y[k+1]) / (2 (y[k-1] - 2 y[k] + y[k+1])) (vertex of the parabola through the three
+    cyclic neighbours), d = 0 unless the curvature is negative, clamped to [-1/2, 1/2]; in [0, 2 pi)."""
+    x = np.asarray(x, dtype=np.float64)
+    Q = x.shape[-1]
+    k = argmax_first(x)
+    y0 = np.take_along_axis(x, k[..., None], -1)[..., 0]
+    ym = np.take_along_axis(x, ((k - 1) % Q)[..., None], -1)[..., 0]
+    yp = np.take_along_axis(x, ((k + 1) % Q)[..., None], -1)[..., 0]
+    den = ym - 2.0 * y0 + yp
+    with np.errstate(divide="ignore", invalid="ignore"):
+        d = np.where(den < 0, 0.5 * (ym - yp) / np.where(den < 0, den, 1.0), 0.0)
+    d = np.clip(d, -0.5, 0.5)
+    return np.mod(2.0 * np.pi * (k + d) / Q, 2.0 * np.pi)
 
 
 # ------------------------------------------------------------------------------------ O3

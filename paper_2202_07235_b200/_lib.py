@@ -36,6 +36,8 @@ SIGNATURES = [
     ("rsvd_blocks_unpack", _I32, [_P, _I64, _I32, _I32, _I32, _P, _P]),
     ("rsvd_align_argmax", _I32, [_P, _I64, _P, _I64, _I64, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P]),
     ("rsvd_align_landscape", _I32, [_P, _I64, _P, _I64, _I32, _I32, _P, _I64, _P, _I64, _I64, _P]),
+    ("rsvd_align_argmax_fine", _I32, [_P, _I64, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P, _P]),
+    ("rsvd_align_landscape_fine", _I32, [_P, _I64, _P, _I64, _I32, _I32, _I32, _P, _I64, _P, _I64, _I64, _P]),
     ("rsvd_winners_reset", _I32, [_P, _I64, _P]),
     ("rsvd_winners_unpack", _I32, [_P, _I64, _I32, _P, _P, _P, _P]),
     ("rsvd_combine_winners", _I32, [_P, _I32, _I64, _I32, _P, _P, _P, _P, _P]),

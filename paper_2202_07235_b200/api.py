@@ -17,7 +17,8 @@ from ._lib import PER_IMAGE, PER_PAIR, SIDE_IMAGE, SIDE_TEMPLATE, RsvdError, che
 
 __all__ = ["block_bytes", "path_for", "set_path", "PATH_AUTO", "PATH_SIMT", "PATH_TC", "kernel_chunk", "kernel_partials_bytes", "align_workspace_bytes",
            "align_min_workspace_bytes", "kernel_partials", "kernel_reduce", "eigen_basis", "build_basis",
-           "compress", "blocks_unpack", "align_argmax", "align_landscape", "winners_reset",
+           "compress", "blocks_unpack", "align_argmax", "align_landscape", "align_argmax_fine",
+           "align_landscape_fine", "winners_reset",
            "winners_unpack", "combine_winners", "launch_count", "timing_enable", "timing_read", "Aligner", "RsvdError", "PER_PAIR", "PER_IMAGE",
            "SIDE_IMAGE", "SIDE_TEMPLATE"]
 
@@ -148,6 +149,42 @@ def align_landscape(img_blocks, M: int, tmpl_blocks, T: int, Q: int, H: int, wor
     check(_lib.lib().rsvd_align_landscape(ptr(img_blocks), M, ptr(tmpl_blocks), T, Q, H, ptr(work),
                                           work.numel() * work.element_size(), ptr(X), ld_m, ld_t,
                                           stream_handle(stream)))
+    return X
+
+
+def align_argmax_fine(img_blocks, M: int, tmpl_blocks, T: int, Q: int, H: int, Q_out: int, mode: int, work,
+                      best_val=None, best_k=None, best_key=None, best_gamma=None, refine: bool = True,
+                      t_offset: int = 0, stream=None):
+    """rsvd_align_argmax_fine: argmax on the zero-padded grid gamma_k = 2 pi k / Q_out (PAPER.md:363);
+    PER_PAIR also returns the 3-point parabolic-refined angle when refine=True."""
+    require_cuda(img_blocks, tmpl_blocks, work)
+    dev = img_blocks.device
+    if mode == PER_PAIR:
+        if best_val is None:
+            best_val = torch.empty((M, T), dtype=torch.float32, device=dev)
+        if best_k is None:
+            best_k = torch.empty((M, T), dtype=torch.int32, device=dev)
+        if refine and best_gamma is None:
+            best_gamma = torch.empty((M, T), dtype=torch.float32, device=dev)
+    else:
+        if best_key is None:
+            best_key = torch.zeros(M, dtype=torch.int64, device=dev)
+    check(_lib.lib().rsvd_align_argmax_fine(ptr(img_blocks), M, ptr(tmpl_blocks), T, t_offset, Q, H, Q_out, mode,
+                                            ptr(work), work.numel() * work.element_size(), ptr(best_val),
+                                            ptr(best_k), ptr(best_key), ptr(best_gamma), stream_handle(stream)))
+    return (best_val, best_k, best_gamma) if mode == PER_PAIR else best_key
+
+
+def align_landscape_fine(img_blocks, M: int, tmpl_blocks, T: int, Q: int, H: int, Q_out: int, work, X=None,
+                         ld_m: int | None = None, ld_t: int | None = None, stream=None):
+    """rsvd_align_landscape_fine: Re X on the zero-padded grid gamma_k = 2 pi k / Q_out."""
+    require_cuda(img_blocks, tmpl_blocks, work)
+    if X is None:
+        X = torch.empty((M, T, Q_out), dtype=torch.float32, device=img_blocks.device)
+        ld_m, ld_t = T * Q_out, Q_out
+    check(_lib.lib().rsvd_align_landscape_fine(ptr(img_blocks), M, ptr(tmpl_blocks), T, Q, H, Q_out, ptr(work),
+                                               work.numel() * work.element_size(), ptr(X), ld_m, ld_t,
+                                               stream_handle(stream)))
     return X
 
 

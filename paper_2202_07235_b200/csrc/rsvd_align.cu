@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(CT_THREADS, 3) contract_kernel(const float2 *_
                                                                  const float2 *__restrict__ beta,
                                                                  int64_t Mpad, int64_t Tpad, int Kpad, int N,
                                                                  int64_t m0, int64_t t0, int64_t Mc, int64_t Tc,
-                                                                 float *__restrict__ Upk) {
+                                                                 float *__restrict__ Upk, int Nout) {
     __shared__ __align__(16) float2 As[2][CT_KC][CT_TILE];
     __shared__ __align__(16) float2 Bs[2][CT_KC][CT_TILE];
 
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(CT_THREADS, 3) contract_kernel(const float2 *_
         if (kc == nk - 1) {          // q finished: planar [n][t][m] stores, 16 lanes = 64 contiguous bytes
             const int q = q0 + it / nk;
             const int n = (q == N) ? 0 : q;
-            float *const re = Upk, *const im = Upk + (int64_t)N * Mc * Tc;
+            float *const re = Upk, *const im = Upk + (int64_t)Nout * Mc * Tc;   // planes of Nout rows
             const int64_t o = ((int64_t)n * Tc + bt) * Mc + bm;
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(CT_THREADS, 3) contract_kernel(const float2 *_
                 for (int j = 0; j < 4; ++j) {
                     const int64_t p = o + (int64_t)(ty * 4 + j) * Mc + tx + 16 * i;
                     if (q == 0) re[p] = acc[i][j].x;                 // U_0 (real) -> re plane slot 0
+                    else if (q == N && Nout > N) re[p + (int64_t)N * Tc * Mc] = 0.5f * acc[i][j].x;   // padded: split Nyquist
                     else if (q == N) im[p] = acc[i][j].x;            // U_N (real) -> im plane slot 0
                     else { re[p] = acc[i][j].x; im[p] = acc[i][j].y; }
                 }
@@ -136,6 +137,8 @@ struct AlignArgs {
     unsigned long long *best_key;
     float *X;
     int64_t ld_m, ld_t;
+    int Qout;              // output grid (Q, or Q * 2^p zero-padded: rsvd_align_*_fine)
+    float *best_gamma;     // PER_PAIR, optional: parabolic-refined angle
 };
 
 // Steps 3-4 kernel: fft2 (rsvd_fft2.cuh) for N = Q/2 <= 256, the original schedule (rsvd_fft.cuh)
@@ -190,6 +193,7 @@ static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const CUte
 
 static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const int N = a.Q / 2;
+    const int Nout = a.Qout / 2;             // spectrum rows per plane (zero-padded when Qout > Q)
     const int Kpad = (int)kpad_of(a.H);
     const bool tc = resolve_path(a.Q, a.H) == PATH_TC;
     // pair tiles: SIMT 64 x 64; TC 128 images x 256 templates (one tcgen05 CTA-pair tile)
@@ -198,7 +202,7 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const int64_t Tpad = tc ? tc_rows_pad_side(a.T, RSVD_SIDE_TEMPLATE) : rows_pad_of(a.T);
     // chunk: Mc x Tc pairs (multiples of the tile) with Mc * Tc * N * 8 <= work_bytes.  Chunks are
     // visited t-outer / m-inner, so a chunk's template blocks stay in L2 while image blocks stream.
-    const int64_t tile_bytes = TM * TT * N * (int64_t)sizeof(float2);
+    const int64_t tile_bytes = TM * TT * Nout * (int64_t)sizeof(float2);
     const int64_t ntiles = a.work_bytes / tile_bytes;
     if (ntiles < 1) return fail(RSVD_ERR_ARG, "workspace smaller than rsvd_align_min_workspace_bytes(Q)");
     const int64_t tmax = Tpad / TT, mmax = Mpad / TM;
@@ -217,8 +221,14 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     float *Upk = reinterpret_cast<float *>(a.work);
     const FftOut o{a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t, a.T, a.t_offset,
                    tc ? tc_scales(a.alpha, a.M, a.Q, a.H, RSVD_SIDE_IMAGE) : nullptr,
-                   tc ? tc_scales(a.beta, a.T, a.Q, a.H, RSVD_SIDE_TEMPLATE) : nullptr};
-    const int LOGN = ilog2(N);
+                   tc ? tc_scales(a.beta, a.T, a.Q, a.H, RSVD_SIDE_TEMPLATE) : nullptr, a.best_gamma};
+    if (Nout > N) {
+        // rows the contraction never writes (im row 0, rows N..Nout-1 except re row N) must read as 0;
+        // they are written here once per call and never discarded from L2 (no discard when padded)
+        e = cudaMemsetAsync(Upk, 0, (size_t)2 * Nout * Mc * Tc * sizeof(float), s);
+        if (e != cudaSuccess) return cuda_check(e, "padded workspace reset");
+    }
+    const int LOGN = ilog2(Nout);
     CUtensorMap tmap;
     if ((e = make_tmap_any(LOGN, &tmap, Upk, Mc, Tc)) != cudaSuccess) return cuda_check(e, "spectrum tensor map");
     const bool timed = timing_enabled();
@@ -230,15 +240,15 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
             const int64_t mcv = std::min(mc, a.M - m0);
             cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
             if (tc) {
-                e = launch_contract_tc(tmA, tmB, a.H, N, m0, t0, mc, tc_, Mc, Tc, Upk, num_sms(), s);
+                e = launch_contract_tc(tmA, tmB, a.H, N, Nout, m0, t0, mc, tc_, Mc, Tc, Upk, num_sms(), s);
                 if (e != cudaSuccess) return cuda_check(e, "contract (tcgen05) launch");
             } else {
                 dim3 g1((unsigned)(tc_ / CT_TILE), (unsigned)(mc / CT_TILE), (unsigned)((N + 1 + CT_QB - 1) / CT_QB));
-                contract_kernel<<<g1, CT_THREADS, 0, s>>>(a.alpha, a.beta, Mpad, Tpad, Kpad, N, m0, t0, Mc, Tc, Upk);
+                contract_kernel<<<g1, CT_THREADS, 0, s>>>(a.alpha, a.beta, Mpad, Tpad, Kpad, N, m0, t0, Mc, Tc, Upk, Nout);
                 if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "contract launch");
             }
             cudaEvent_t ev1 = timed ? timing_event(s) : nullptr;
-            e = launch_fft_any(LOGN, a.mode, s, tmap, Mc, Tc, m0, t0, mcv, tcv, o, Upk);
+            e = launch_fft_any(LOGN, a.mode, s, tmap, Mc, Tc, m0, t0, mcv, tcv, o, Nout > N ? nullptr : Upk);
             if (e != cudaSuccess) return cuda_check(e, "fft_reduce launch");
             count_launches(2);
             if (timed) {
@@ -305,40 +315,67 @@ extern "C" int64_t rsvd_align_workspace_bytes(int64_t M, int64_t T, int32_t Q, i
     return std::max(rsvd_align_min_workspace_bytes(Q), std::min(full, target));
 }
 
-extern "C" rsvd_status rsvd_align_argmax(const void *img_blocks, int64_t M, const void *tmpl_blocks, int64_t T,
-                                         int64_t t_offset, int32_t Q, int32_t H, rsvd_reduce mode, void *work,
-                                         int64_t work_bytes, float *best_val, int32_t *best_k, uint64_t *best_key,
-                                         rsvd_stream_t stream) {
+static rsvd_status check_qout(int32_t Q, int32_t Qout, int64_t work_bytes) {
+    if (Qout < Q || !is_pow2(Qout) || Qout > 1024)
+        return fail(RSVD_ERR_UNSUPPORTED, "Q_out must be Q times a power of two, at most 1024");
+    if (work_bytes < rsvd_align_min_workspace_bytes(Qout)) return fail(RSVD_ERR_ARG, "workspace too small for Q_out");
+    return RSVD_OK;
+}
+
+extern "C" rsvd_status rsvd_align_argmax_fine(const void *img_blocks, int64_t M, const void *tmpl_blocks, int64_t T,
+                                              int64_t t_offset, int32_t Q, int32_t H, int32_t Q_out,
+                                              rsvd_reduce mode, void *work, int64_t work_bytes, float *best_val,
+                                              int32_t *best_k, uint64_t *best_key, float *best_gamma,
+                                              rsvd_stream_t stream) {
     rsvd_status st = check_common(img_blocks, M, tmpl_blocks, T, Q, H, work, work_bytes);
     if (st != RSVD_OK || M == 0 || T == 0) return st;
+    if ((st = check_qout(Q, Q_out, work_bytes)) != RSVD_OK) return st;
     if (mode == RSVD_PER_PAIR) {
         if (!best_val || !best_k) return fail(RSVD_ERR_ARG, "PER_PAIR needs best_val and best_k");
     } else if (mode == RSVD_PER_IMAGE) {
         if (!best_key) return fail(RSVD_ERR_ARG, "PER_IMAGE needs best_key");
+        if (best_gamma) return fail(RSVD_ERR_ARG, "best_gamma is a PER_PAIR output");
         if (t_offset < 0) return fail(RSVD_ERR_ARG, "t_offset must be >= 0");
-        if ((uint64_t)(t_offset + T) * (uint64_t)Q >= 0xFFFFFFFFull)
-            return fail(RSVD_ERR_UNSUPPORTED, "(t_offset + T) * Q must be < 2^32 for packed keys");
+        if ((uint64_t)(t_offset + T) * (uint64_t)Q_out >= 0xFFFFFFFFull)
+            return fail(RSVD_ERR_UNSUPPORTED, "(t_offset + T) * Q_out must be < 2^32 for packed keys");
     } else {
         return fail(RSVD_ERR_ARG, "bad mode");
     }
     AlignArgs a{reinterpret_cast<const float2 *>(img_blocks), reinterpret_cast<const float2 *>(tmpl_blocks),
                 M, T, t_offset, Q, H, mode == RSVD_PER_PAIR ? MODE_PAIR : MODE_IMAGE, work, work_bytes,
-                best_val, best_k, reinterpret_cast<unsigned long long *>(best_key), nullptr, 0, 0};
+                best_val, best_k, reinterpret_cast<unsigned long long *>(best_key), nullptr, 0, 0, Q_out, best_gamma};
+    return run_align(a, (cudaStream_t)stream);
+}
+
+extern "C" rsvd_status rsvd_align_argmax(const void *img_blocks, int64_t M, const void *tmpl_blocks, int64_t T,
+                                         int64_t t_offset, int32_t Q, int32_t H, rsvd_reduce mode, void *work,
+                                         int64_t work_bytes, float *best_val, int32_t *best_k, uint64_t *best_key,
+                                         rsvd_stream_t stream) {
+    return rsvd_align_argmax_fine(img_blocks, M, tmpl_blocks, T, t_offset, Q, H, Q, mode, work, work_bytes, best_val,
+                                  best_k, best_key, nullptr, stream);
+}
+
+extern "C" rsvd_status rsvd_align_landscape_fine(const void *img_blocks, int64_t M, const void *tmpl_blocks,
+                                                 int64_t T, int32_t Q, int32_t H, int32_t Q_out, void *work,
+                                                 int64_t work_bytes, float *X, int64_t ld_m, int64_t ld_t,
+                                                 rsvd_stream_t stream) {
+    rsvd_status st = check_common(img_blocks, M, tmpl_blocks, T, Q, H, work, work_bytes);
+    if (st != RSVD_OK || M == 0 || T == 0) return st;
+    if ((st = check_qout(Q, Q_out, work_bytes)) != RSVD_OK) return st;
+    if (!X) return fail(RSVD_ERR_ARG, "NULL landscape pointer");
+    if (ld_t < Q_out || ld_m < 0) return fail(RSVD_ERR_ARG, "bad landscape strides");
+    if ((ld_t & 1) || (ld_m & 1) || (reinterpret_cast<uintptr_t>(X) & 7u))
+        return fail(RSVD_ERR_ARG, "landscape strides must be even and X 8-byte aligned");
+    AlignArgs a{reinterpret_cast<const float2 *>(img_blocks), reinterpret_cast<const float2 *>(tmpl_blocks),
+                M, T, 0, Q, H, MODE_LANDSCAPE, work, work_bytes, nullptr, nullptr, nullptr, X, ld_m, ld_t, Q_out,
+                nullptr};
     return run_align(a, (cudaStream_t)stream);
 }
 
 extern "C" rsvd_status rsvd_align_landscape(const void *img_blocks, int64_t M, const void *tmpl_blocks, int64_t T,
                                             int32_t Q, int32_t H, void *work, int64_t work_bytes, float *X,
                                             int64_t ld_m, int64_t ld_t, rsvd_stream_t stream) {
-    rsvd_status st = check_common(img_blocks, M, tmpl_blocks, T, Q, H, work, work_bytes);
-    if (st != RSVD_OK || M == 0 || T == 0) return st;
-    if (!X) return fail(RSVD_ERR_ARG, "NULL landscape pointer");
-    if (ld_t < Q || ld_m < 0) return fail(RSVD_ERR_ARG, "bad landscape strides");
-    if ((ld_t & 1) || (ld_m & 1) || (reinterpret_cast<uintptr_t>(X) & 7u))
-        return fail(RSVD_ERR_ARG, "landscape strides must be even and X 8-byte aligned");
-    AlignArgs a{reinterpret_cast<const float2 *>(img_blocks), reinterpret_cast<const float2 *>(tmpl_blocks),
-                M, T, 0, Q, H, MODE_LANDSCAPE, work, work_bytes, nullptr, nullptr, nullptr, X, ld_m, ld_t};
-    return run_align(a, (cudaStream_t)stream);
+    return rsvd_align_landscape_fine(img_blocks, M, tmpl_blocks, T, Q, H, Q, work, work_bytes, X, ld_m, ld_t, stream);
 }
 
 extern "C" rsvd_status rsvd_winners_reset(uint64_t *keys, int64_t M, rsvd_stream_t stream) {

@@ -48,8 +48,9 @@ cudaError_t launch_compress_tc(const float2 *rings, int64_t n, int R, int Q, con
 cudaError_t launch_unpack_tc(const float *blocks, int64_t n, int Q, int H, int side, float2 *coeffs, cudaStream_t s);
 cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t rows, int Q, int H, int side);
 const float *tc_scales(const void *blocks, int64_t rows, int Q, int H, int side);
-cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int64_t m0, int64_t t0,
-                               int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms, cudaStream_t s);
+cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int Nout, int64_t m0,
+                               int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms,
+                               cudaStream_t s);
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }

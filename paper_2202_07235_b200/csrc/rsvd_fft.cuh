@@ -72,7 +72,39 @@ struct FftOut {
     float *X;
     int64_t ld_m, ld_t, T, t_offset;
     const float *sc_m, *sc_t;      // TC path: exact power-of-two row scales of the operands (NULL = 1)
+    float *best_gamma;             // PER_PAIR, optional: parabolic-refined argmax angle (radians)
 };
+
+// 3-point parabolic refinement of the first argmax bk (SPEC.md argmax_refine, reading in DESIGN.md):
+// the lanes of a pair hold Re X at k = 2 (k1 + N2 k2) + {0, 1} in wj[brev(k2)] (x, y); the samples at
+// bk -+ 1 (cyclic) are fetched from their owner lanes, gamma = 2 pi (bk + d) / Q with the vertex
+// offset d = (y- - y+) / (2 (y- - 2 y0 + y+)) clamped to [-1/2, 1/2] (0 when not a strict maximum).
+template <int N1, int N2>
+__device__ __forceinline__ float parabolic_gamma(const float2 (&wj)[N1], int k1, int bk, float y0, unsigned gmask) {
+    constexpr int Qn = 2 * N1 * N2;
+    auto fetch = [&](int i) {
+        const int c = i >> 1, kk1 = c % N2, kk2 = c / N2;
+        float v = 0.f;
+        if (kk1 == k1) {
+#pragma unroll
+            for (int k2 = 0; k2 < N1; ++k2)
+                if (k2 == kk2) {
+                    const float2 z = wj[brev(k2, clog2(N1))];
+                    v = (i & 1) ? z.y : z.x;
+                }
+        }
+#pragma unroll
+        for (int off = N2 / 2; off >= 1; off >>= 1) v += __shfl_xor_sync(gmask, v, off);   // one nonzero term
+        return v;
+    };
+    const float ym = fetch((bk - 1) & (Qn - 1)), yp = fetch((bk + 1) & (Qn - 1));
+    const float den = ym - 2.f * y0 + yp;
+    float d = den < 0.f ? 0.5f * (ym - yp) / den : 0.f;
+    d = fminf(0.5f, fmaxf(-0.5f, d));
+    float g = 6.283185307179586f * ((float)bk + d) / (float)Qn;
+    if (g < 0.f) g += 6.283185307179586f;
+    return g;
+}
 
 __device__ __forceinline__ uint32_t fr_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void fr_mbar_wait(uint64_t *b, uint32_t parity) {
@@ -274,10 +306,15 @@ __global__ void __launch_bounds__(FR_THREADS, 2) fft_reduce_kernel(const __grid_
                     }
 #pragma unroll
                     for (int off = N2 / 2; off >= 1; off >>= 1) bk = min(bk, __shfl_xor_sync(gmask, bk, off));
+                    float gam = 0.f;
+                    if constexpr (MODE == MODE_PAIR) {
+                        if (out.best_gamma) gam = parabolic_gamma<N1, N2>(w[j], k1, bk, mx, gmask);
+                    }
                     if (k1 == 0) {
                         if constexpr (MODE == MODE_PAIR) {
                             out.best_val[m * out.T + t] = bv;
                             out.best_k[m * out.T + t] = bk;
+                            if (out.best_gamma) out.best_gamma[m * out.T + t] = gam;
                         } else {
                             const uint32_t idx = (uint32_t)((out.t_offset + t) * Q + bk);
                             const unsigned long long key =

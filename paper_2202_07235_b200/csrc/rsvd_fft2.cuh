@@ -258,10 +258,15 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
                     }
 #pragma unroll
                     for (int off = N2 / 2; off >= 1; off >>= 1) bk = min(bk, __shfl_xor_sync(gmask, bk, off));
+                    float gam = 0.f;
+                    if constexpr (MODE == MODE_PAIR) {
+                        if (out.best_gamma) gam = parabolic_gamma<N1, N2>(w[j], k1, bk, mx, gmask);
+                    }
                     if (k1 == 0) {
                         if constexpr (MODE == MODE_PAIR) {
                             out.best_val[m * out.T + t] = bv;
                             out.best_k[m * out.T + t] = bk;
+                            if (out.best_gamma) out.best_gamma[m * out.T + t] = gam;
                         } else {
                             const uint32_t idx = (uint32_t)((out.t_offset + t) * Q + bk);
                             const unsigned long long key =

@@ -168,7 +168,7 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int steps, int KB, int N,
     int mtl, int ntl, int mt0, int nt0, int qg, int nqg, int nitems, int64_t Mc, int64_t Tc,
-    float *__restrict__ Upk) {
+    float *__restrict__ Upk, int Nout) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint64_t *bars = reinterpret_cast<uint64_t *>(base + TC_STAGES * TC_STAGE_BYTES);
@@ -270,7 +270,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
         const int row = quad * 32 + lane;
         const bool re_rows = row < 64;
-        float *const plane_re = Upk, *const plane_im = Upk + (int64_t)N * Mc * Tc;
+        // planes of Nout rows; Nout > N is the zero-padded (finer-gamma) spectrum of rsvd_align_*_fine:
+        // U_N / 2 goes to row N of the re plane (the split Nyquist bin, reading G4)
+        float *const plane_re = Upk, *const plane_im = Upk + (int64_t)Nout * Mc * Tc;
+        const bool padded = Nout > N;
         const uint32_t te0 = rank == 0 ? smem_u32(tempty) : mapa_rank(smem_u32(tempty), 0);
         // PDL: operands are read-only, so TMA + MMA above may overlap the previous kernel's tail; the
         // workspace is only written after that kernel (Step 3 of the previous chunk) has finished.
@@ -287,8 +290,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
                 tc_fence_after();
                 // q = 0: Re U_0 -> re plane slot 0; q = N: Re U_N -> im plane slot 0; Im rows of both dropped
                 const bool store = (q != 0 && q != N) || re_rows;
-                float *plane = (q == N) ? plane_im : ((q == 0 || re_rows) ? plane_re : plane_im);
-                const int n = (q == N) ? 0 : q;
+                const bool nyq_packed = q == N && !padded;
+                float *plane = nyq_packed ? plane_im : ((q == 0 || q == N || re_rows) ? plane_re : plane_im);
+                const int n = nyq_packed ? 0 : q;
+                const float qs = (q == N && padded) ? 0.5f : 1.f;
                 // workspace [n][t][m]: the 32 lanes hold 32 consecutive images -> each store is one 128-B line
                 float *dst = plane + ((int64_t)n * Tc + (int64_t)nt_l * TC_TT) * Mc + ml;
                 const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256);
@@ -309,7 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
                         for (int h = 0; h < 2; ++h)
 #pragma unroll
                             for (int i = 0; i < 32; ++i)
-                                dst[(int64_t)(64 * b + 32 * h + i) * Mc] = __uint_as_float(v[cur][h][i]);
+                                dst[(int64_t)(64 * b + 32 * h + i) * Mc] = qs * __uint_as_float(v[cur][h][i]);
                     }
                     tmem_wait_ld();
                 }
@@ -677,8 +682,9 @@ cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t ro
 }
 
 // One chunk: images [m0, m0 + mc) (multiples of 128), templates [t0, t0 + tc) (multiples of 256).
-cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int64_t m0, int64_t t0,
-                               int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms, cudaStream_t s) {
+cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int Nout, int64_t m0,
+                               int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms,
+                               cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(contract_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
@@ -705,7 +711,7 @@ cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, i
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, contract_tc_kernel, tmA, tmB, tc_steps(H), tc_kb(H), N, mtl, ntl,
-                                       (int)(m0 / TC_PIMG), (int)(t0 / TC_TT), qg, nqg, nitems, Mc, Tc, Upk);
+                                       (int)(m0 / TC_PIMG), (int)(t0 / TC_TT), qg, nqg, nitems, Mc, Tc, Upk, Nout);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

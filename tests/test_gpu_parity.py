@@ -295,3 +295,42 @@ def test_streamed_host_path_matches_device_path(contraction_path):
     work = torch.empty(api.align_workspace_bytes(700, 300, Q, H) // 4, dtype=torch.float32, device="cuda")
     ref_keys = api.align_argmax(ib, 700, tb, 300, Q, H, api.PER_IMAGE, work)
     assert torch.equal(keys, ref_keys)
+
+
+@pytest.mark.parametrize("Q,p", [(32, 1), (64, 2), (128, 1), (256, 1), (512, 1)])
+def test_fine_gamma_landscape_and_refined_argmax(Q, p):
+    """Row f1: the landscape on the zero-padded grid Q_out = Q 2^p against the oracle's
+    term-by-term evaluation (F1), the per-pair argmax / parabolic-refined angle against the same
+    launch's landscape, and per-image winners on the fine grid."""
+    M, T, R, H = 70, 45, 12, 5
+    rng = np.random.default_rng(Q + p)
+    A = (rng.standard_normal((M, R, Q)) + 1j * rng.standard_normal((M, R, Q))).astype(np.complex64)
+    B = (rng.standard_normal((T, R, Q)) + 1j * rng.standard_normal((T, R, Q))).astype(np.complex64)
+    k, w = radial_grid(R)
+    U, _ = api.build_basis(cuda(B), w, H)
+    wd, Ud = cuda(w, torch.float64), cuda(U, torch.float64)
+    ib = api.compress(cuda(A), wd, Ud, api.SIDE_IMAGE)
+    tb = api.compress(cuda(B), wd, Ud, api.SIDE_TEMPLATE)
+    Qo = Q << p
+    work = torch.empty(api.align_workspace_bytes(M, T, Qo, H) // 4, dtype=torch.float32, device="cuda")
+    X = to_np(api.align_landscape_fine(ib, M, tb, T, Q, H, Qo, work))
+    m, t = rng.integers(0, M, 120), rng.integers(0, T, 120)
+    X_ref = ref.landscape_rank_fine(A, B, w, U, m, t, Qo)
+    tol_abs = TOL_FP32 * np.abs(X_ref).max()
+    assert np.abs(X[m, t] - X_ref).max() <= tol_abs
+    # the coarse landscape is the fine one's every 2^p-th sample
+    Xc = to_np(api.align_landscape(ib, M, tb, T, Q, H, work))
+    assert np.abs(X[:, :, ::(1 << p)] - Xc).max() <= 2 * TOL_FP32 * np.abs(Xc).max()
+    val, kk, gam = (to_np(x) for x in api.align_argmax_fine(ib, M, tb, T, Q, H, Qo, api.PER_PAIR, work))
+    assert np.abs(val - X.max(-1)).max() <= 1e-6 * np.abs(X).max()
+    assert_argmax_gated(kk[m, t], X_ref, tol_abs)
+    same = kk == ref.argmax_first(X)                          # where the launch agrees with its landscape
+    assert same.mean() > 0.95
+    g_ref = ref.argmax_refine(X)
+    dg = np.abs(np.angle(np.exp(1j * (gam - g_ref))))
+    assert dg[same].max() <= 1e-3 * 2 * np.pi / Qo + 1e-5
+    assert np.all((gam >= 0) & (gam < 2 * np.pi))
+    keys = api.align_argmax_fine(ib, M, tb, T, Q, H, Qo, api.PER_IMAGE, work)
+    v, ti, ki = (to_np(x) for x in api.winners_unpack(keys, Qo))
+    assert np.abs(v - val.max(1)).max() <= 1e-6 * np.abs(X).max()
+    assert np.all(val[np.arange(M), ti] == v)

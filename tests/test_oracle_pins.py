@@ -363,3 +363,77 @@ def test_generator_rotation_is_cyclic_shift():
     b0 = _slice_rows(p1, p2, torch.zeros(2, dtype=torch.float64), kt, Q).numpy()
     b1 = _slice_rows(p1, p2, torch.full((2,), 2 * np.pi * k0 / Q, dtype=torch.float64), kt, Q).numpy()
     assert np.abs(b1 - np.roll(b0, k0, axis=-1)).max() <= 1e-12 * np.abs(b0).max()
+
+
+# ------------------------------------------------------------------ F1: finer gamma
+def test_F1_fine_equals_O2_on_the_coarse_grid():
+    """At Q_out = Q the zero-padded evaluation is the plain rank-H landscape (a direct correlation
+    sum, O2), and at Q_out = 4Q every 4th sample is.  Catches a wrong frequency sign, a missing
+    1/Q or 2 pi, a mis-indexed negative frequency or a doubled Nyquist term."""
+    rng = np.random.default_rng(11)
+    R, Q, H = 5, 16, 3
+    A, B = _rand_rings(rng, 2, R, Q), _rand_rings(rng, 3, R, Q)
+    k, w = radial_grid(R)
+    U = _rand_orth(rng, R)[:, :H]
+    ia, ib = _all_pairs(2, 3)
+    X2 = ref.landscape_rank(A, B, w, U, ia, ib).real
+    F = ref.landscape_rank_fine(A, B, w, U, ia, ib, Q)
+    np.testing.assert_allclose(F, X2, atol=1e-12 * np.abs(X2).max())
+    F4 = ref.landscape_rank_fine(A, B, w, U, ia, ib, 4 * Q)
+    np.testing.assert_allclose(F4[:, ::4], X2, atol=1e-12 * np.abs(X2).max())
+
+
+@pytest.mark.parametrize("p", [1, 3, -5])
+def test_F1_single_frequency_is_exact_off_grid(p):
+    """A single angular frequency p (|p| < Q/2) on one ring has the band-limited landscape
+    2 pi w_r cos(p gamma) for EVERY gamma (P5 continued off the grid): the zero-padded samples must
+    reproduce it at gamma = 2 pi k / Q_out.  Catches an interpolation that is not the trigonometric
+    polynomial of the coefficients (e.g. a missing conjugate-frequency term)."""
+    R, Q, r = 4, 16, 2
+    k, w = radial_grid(R)
+    psi = 2 * np.pi * np.arange(Q) / Q
+    a = np.zeros((1, R, Q), complex)
+    a[0, r] = np.exp(1j * p * psi)
+    U = np.eye(R)
+    Qo = 8 * Q
+    F = ref.landscape_rank_fine(a, a, w, U, [0], [0], Qo)[0]
+    gam = 2 * np.pi * np.arange(Qo) / Qo
+    np.testing.assert_allclose(F, 2 * np.pi * w[r] * np.cos(p * gam), atol=1e-12)
+
+
+def test_F1_nyquist_bin_is_split():
+    """Reading G4 for f1: the unpaired bin Q/2 contributes cos(Q gamma/2) S_{Q/2}.  With
+    a = (-1)^j and b = i (-1)^j on one ring, S_{Q/2} = i w_r dpsi-free, so the split gives Re X = 0 at
+    every gamma (the one-sided '+Q/2' or '-Q/2' readings would give -+2 pi w_r sin(Q gamma / 2))."""
+    R, Q, r = 3, 8, 1
+    k, w = radial_grid(R)
+    alt = (-1.0) ** np.arange(Q)
+    a = np.zeros((1, R, Q), complex)
+    b = np.zeros((1, R, Q), complex)
+    a[0, r] = alt
+    b[0, r] = 1j * alt
+    F = ref.landscape_rank_fine(a, b, w, np.eye(R), [0], [0], 4 * Q)[0]
+    np.testing.assert_allclose(F, 0.0, atol=1e-13)
+    # and a real Nyquist ring gives 2 pi w_r cos(Q gamma / 2)
+    F2 = ref.landscape_rank_fine(a, a, w, np.eye(R), [0], [0], 4 * Q)[0]
+    gam = 2 * np.pi * np.arange(4 * Q) / (4 * Q)
+    np.testing.assert_allclose(F2, 2 * np.pi * w[r] * np.cos(Q / 2 * gam), atol=1e-12)
+
+
+def test_F1_argmax_refine_spec_examples():
+    """SPEC.md argmax_refine examples: unique max at index 5 of 98 with symmetric neighbours ->
+    2 pi 5/98; constant landscape -> 0 (smallest index, zero curvature); samples of a parabola with
+    its vertex between grid points -> the analytic vertex (exact for a parabola); wrap-around at k=0."""
+    x = np.zeros(98)
+    x[4], x[5], x[6] = 1.0, 2.0, 1.0
+    assert abs(ref.argmax_refine(x) - 2 * np.pi * 5 / 98) < 1e-15
+    assert ref.argmax_refine(np.full(17, 3.0)) == 0.0
+    Q, v = 64, 20.3
+    kk = np.arange(Q)
+    par = 5.0 - (kk - v) ** 2
+    assert abs(ref.argmax_refine(par) - 2 * np.pi * v / Q) < 1e-12
+    cyc = np.zeros(Q)
+    cyc[0], cyc[1], cyc[-1] = 4.0, 1.0, 3.0                     # vertex left of 0 -> wraps near 2 pi
+    g = ref.argmax_refine(cyc)
+    d = (3.0 - 1.0) / (2 * (3.0 - 8.0 + 1.0))
+    assert abs(g - np.mod(2 * np.pi * d / Q, 2 * np.pi)) < 1e-12
