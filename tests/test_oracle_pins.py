@@ -403,8 +403,8 @@ def test_F1_single_frequency_is_exact_off_grid(p):
 
 def test_F1_nyquist_bin_is_split():
     """Reading G4 for f1: the unpaired bin Q/2 contributes cos(Q gamma/2) S_{Q/2}.  With
-    a = (-1)^j and b = i (-1)^j on one ring, S_{Q/2} = i w_r dpsi-free, so the split gives Re X = 0 at
-    every gamma (the one-sided '+Q/2' or '-Q/2' readings would give -+2 pi w_r sin(Q gamma / 2))."""
+    a = (-1)^j and b = i (-1)^j on one ring, S_{Q/2} = i w_r (purely imaginary), so the split gives
+    Re X = 0 at every gamma (the one-sided '+Q/2' or '-Q/2' readings would give -+2 pi w_r sin(Q gamma/2))."""
     R, Q, r = 3, 8, 1
     k, w = radial_grid(R)
     alt = (-1.0) ** np.arange(Q)
