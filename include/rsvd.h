@@ -125,6 +125,22 @@ rsvd_status rsvd_compress(const void *rings, int64_t n, int32_t R, int32_t Q, co
 rsvd_status rsvd_blocks_unpack(const void *blocks, int64_t n, int32_t Q, int32_t H, rsvd_side side,
                                void *coeffs, rsvd_stream_t stream);
 
+/* ------------------------------------------------------------------ row f2: translations (NEXT)
+ * Translations inside the method (PAPER.md:37-39 defers them; configs "Translations"): compresses S
+ * translated copies of each base row without materialising them.  Output row b*S + s is the row
+ * rsvd_compress would produce from
+ *   a_s[r][j] = a_b[r][j] exp(-i k_r (dx_s cos psi_j + dy_s sin psi_j))
+ * (the Fourier shift theorem with the transform convention of PAPER.md:80; reading G15):
+ *   rings: device [n_base][R][Q] complex64;  k: device fp64 [R] radial wavenumbers k_r;
+ *   shifts: device fp64 [S][2] (dx_s, dy_s) in the units of 1/k;  w, U as for rsvd_compress;
+ *   blocks: device, rsvd_block_bytes(n_base * S, Q, H, side) bytes.  Each base ring is read once
+ *   from HBM (its S copies are built in registers); the ramp is evaluated in fp32 (|k d| <= ~2 rad
+ *   on the configs: phase error ~1e-7).  S >= 1; NULL k / shifts with n_base > 0 are RSVD_ERR_ARG. */
+rsvd_status rsvd_compress_translated(const void *rings, int64_t n_base, int32_t R, int32_t Q,
+                                     const double *w, const double *k, const double *U, int32_t H,
+                                     const double *shifts, int32_t S, rsvd_side side, void *blocks,
+                                     rsvd_stream_t stream);
+
 /* ------------------------------------------------------------------ rows a2-a4: align
  * Step 2: S_q[m,t] = sum_h conj(A_q[m,h]) B_q[t,h] for all q;
  * Step 3: X_k = 2 pi sum_q e^{-2 pi i q k/Q} S_q, k = 0..Q-1 (forward sign, G3);

@@ -34,6 +34,7 @@ SIGNATURES = [
     ("rsvd_build_basis", _I32, [_P, _I64, _I32, _I32, _P, _I32, _P, _P, _P]),
     ("rsvd_compress", _I32, [_P, _I64, _I32, _I32, _P, _P, _I32, _I32, _P, _P]),
     ("rsvd_blocks_unpack", _I32, [_P, _I64, _I32, _I32, _I32, _P, _P]),
+    ("rsvd_compress_translated", _I32, [_P, _I64, _I32, _I32, _P, _P, _P, _I32, _P, _I32, _I32, _P, _P]),
     ("rsvd_align_argmax", _I32, [_P, _I64, _P, _I64, _I64, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P]),
     ("rsvd_align_landscape", _I32, [_P, _I64, _P, _I64, _I32, _I32, _P, _I64, _P, _I64, _I64, _P]),
     ("rsvd_align_argmax_fine", _I32, [_P, _I64, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P, _P]),

@@ -17,7 +17,7 @@ from ._lib import PER_IMAGE, PER_PAIR, SIDE_IMAGE, SIDE_TEMPLATE, RsvdError, che
 
 __all__ = ["block_bytes", "path_for", "set_path", "PATH_AUTO", "PATH_SIMT", "PATH_TC", "kernel_chunk", "kernel_partials_bytes", "align_workspace_bytes",
            "align_min_workspace_bytes", "kernel_partials", "kernel_reduce", "eigen_basis", "build_basis",
-           "compress", "blocks_unpack", "align_argmax", "align_landscape", "align_argmax_fine",
+           "compress", "compress_translated", "blocks_unpack", "align_argmax", "align_landscape", "align_argmax_fine",
            "align_landscape_fine", "winners_reset",
            "winners_unpack", "combine_winners", "launch_count", "timing_enable", "timing_read", "Aligner", "RsvdError", "PER_PAIR", "PER_IMAGE",
            "SIDE_IMAGE", "SIDE_TEMPLATE"]
@@ -111,6 +111,23 @@ def compress(rings: torch.Tensor, w: torch.Tensor, U: torch.Tensor, side: int, o
     elif out.numel() * out.element_size() < nb:
         raise RsvdError(1, "block buffer too small")
     check(_lib.lib().rsvd_compress(ptr(rings), n, R, Q, ptr(w), ptr(U), H, side, ptr(out), stream_handle(stream)))
+    return out
+
+
+def compress_translated(rings: torch.Tensor, w: torch.Tensor, k: torch.Tensor, U: torch.Tensor,
+                        shifts: torch.Tensor, side: int, out=None, stream=None):
+    """rsvd_compress_translated: blocks of the S translated copies (row b*S + s) of every base row."""
+    require_cuda(rings, w, k, U, shifts)
+    n, R, Q = rings.shape
+    H = U.shape[1]
+    S = shifts.shape[0]
+    nb = block_bytes(n * S, Q, H, side)
+    if out is None:
+        out = torch.empty((nb + 3) // 4, dtype=torch.float32, device=rings.device)
+    elif out.numel() * out.element_size() < nb:
+        raise RsvdError(1, "block buffer too small")
+    check(_lib.lib().rsvd_compress_translated(ptr(rings), n, R, Q, ptr(w), ptr(k), ptr(U), H, ptr(shifts), S,
+                                              side, ptr(out), stream_handle(stream)))
     return out
 
 

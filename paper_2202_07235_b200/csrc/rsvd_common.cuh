@@ -44,7 +44,7 @@ int64_t tc_rows_pad(int64_t rows);
 int64_t tc_rows_pad_side(int64_t rows, int side);
 int64_t tc_block_bytes(int64_t rows, int Q, int H, int side);
 cudaError_t launch_compress_tc(const float2 *rings, int64_t n, int R, int Q, const double *w, const double *U, int H,
-                               int side, float *blocks, cudaStream_t s);
+                               int side, float *blocks, const double *kr, const double *shifts, int S, cudaStream_t s);
 cudaError_t launch_unpack_tc(const float *blocks, int64_t n, int Q, int H, int side, float2 *coeffs, cudaStream_t s);
 cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t rows, int Q, int H, int side);
 const float *tc_scales(const void *blocks, int64_t rows, int Q, int H, int side);

@@ -29,7 +29,9 @@ __global__ void __launch_bounds__(CP_THREADS) compress_kernel(const float2 *__re
                                                               int R, const double *__restrict__ w,
                                                               const double *__restrict__ U, int H,
                                                               int side, int64_t rows_pad, int Kpad,
-                                                              float2 *__restrict__ blocks) {
+                                                              float2 *__restrict__ blocks,
+                                                              const double *__restrict__ kr,
+                                                              const double *__restrict__ shifts, int S) {
     constexpr int Q = 1 << LOGQ;
     constexpr int L = 32;
     constexpr int E = Q / L;
@@ -39,12 +41,14 @@ __global__ void __launch_bounds__(CP_THREADS) compress_kernel(const float2 *__re
     float2 *at = tw + E * L;                                        // [CP_HC][Q]
     float *up = reinterpret_cast<float *>(at + CP_HC * Q);          // [R][CP_HC]
 
-    const int64_t row = blockIdx.x;
+    const int64_t row = blockIdx.x;                  // output row = base * S + shift
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < E * L; i += CP_THREADS) tw[i] = twiddle_N(i % L, i / L, Q);
     float2 stw[clog2(L)];
     lane_stage_twiddles<L>(lane, stw);
-    const float2 *ring = rings + row * (int64_t)R * Q;
+    const float2 *ring = rings + (row / S) * (int64_t)R * Q;
+    double dx = 0.0, dy = 0.0;                       // row f2: translated copy (row % S) of the base row
+    if (shifts) { dx = shifts[2 * (row % S)]; dy = shifts[2 * (row % S) + 1]; }
     const double invQ = 1.0 / (double)Q;
 
     for (int h0 = 0; h0 < H; h0 += CP_HC) {
@@ -60,8 +64,19 @@ __global__ void __launch_bounds__(CP_THREADS) compress_kernel(const float2 *__re
             float2 acc[CP_HC];
 #pragma unroll
             for (int hh = 0; hh < CP_HC; ++hh) acc[hh] = make_float2(0.f, 0.f);
+            float uj = 0.f;
+            if (shifts) {
+                double sn, cs;
+                sincospi(2.0 * (double)j / (double)Q, &sn, &cs);
+                uj = (float)(dx * cs + dy * sn);
+            }
             for (int r = 0; r < R; ++r) {
-                const float2 a = __ldg(ring + (int64_t)r * Q + j);
+                float2 a = __ldg(ring + (int64_t)r * Q + j);
+                if (shifts) {                        // a exp(-i k_r (dx cos psi_j + dy sin psi_j))
+                    float sn, cs;
+                    sincosf(-(float)kr[r] * uj, &sn, &cs);
+                    a = make_float2(a.x * cs - a.y * sn, a.x * sn + a.y * cs);
+                }
                 const float4 *u4 = reinterpret_cast<const float4 *>(up + r * CP_HC);
 #pragma unroll
                 for (int g = 0; g < CP_HC / 4; ++g) {
@@ -126,7 +141,7 @@ __global__ void unpack_kernel(const float2 *__restrict__ blocks, int64_t n, int 
 template <int LOGQ>
 static cudaError_t launch_compress(const float2 *rings, int64_t n, int R, const double *w,
                                    const double *U, int H, int side, int64_t rows_pad, int Kpad,
-                                   float2 *blocks, cudaStream_t s) {
+                                   float2 *blocks, const double *kr, const double *shifts, int S, cudaStream_t s) {
     constexpr int Q = 1 << LOGQ;
     const size_t smem = (size_t)Q * sizeof(float2) + (size_t)CP_HC * Q * sizeof(float2) +
                         (size_t)R * CP_HC * sizeof(float);
@@ -136,7 +151,7 @@ static cudaError_t launch_compress(const float2 *rings, int64_t n, int R, const 
     const bool timed = timing_enabled();
     cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
     compress_kernel<LOGQ><<<(unsigned)n, CP_THREADS, smem, s>>>(rings, n, R, w, U, H, side, rows_pad,
-                                                                 Kpad, blocks);
+                                                                 Kpad, blocks, kr, shifts, S);
     e = cudaGetLastError();
     if (e == cudaSuccess) {
         count_launches(1);
@@ -155,9 +170,10 @@ extern "C" int64_t rsvd_block_bytes(int64_t rows, int32_t Q, int32_t H, rsvd_sid
     return (int64_t)(Q / 2 + 1) * kpad_of(H) * rows_pad_of(rows) * (int64_t)sizeof(float2);
 }
 
-extern "C" rsvd_status rsvd_compress(const void *rings, int64_t n, int32_t R, int32_t Q, const double *w,
-                                     const double *U, int32_t H, rsvd_side side, void *blocks,
-                                     rsvd_stream_t stream) {
+// n = output rows (base rows * S); shifts == NULL is the plain compress (S = 1)
+static rsvd_status compress_impl(const void *rings, int64_t n, int32_t R, int32_t Q, const double *w,
+                                 const double *U, int32_t H, rsvd_side side, void *blocks, const double *kr,
+                                 const double *shifts, int32_t S, rsvd_stream_t stream) {
     if (R <= 0) return fail(RSVD_ERR_ARG, "R must be positive");
     if (R > 256) return fail(RSVD_ERR_UNSUPPORTED, "R > 256 is not supported");
     if (Q <= 0) return fail(RSVD_ERR_ARG, "Q must be positive");
@@ -178,7 +194,7 @@ extern "C" rsvd_status rsvd_compress(const void *rings, int64_t n, int32_t R, in
         const bool timed = timing_enabled();
         cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
         cudaError_t e = launch_compress_tc(reinterpret_cast<const float2 *>(rings), n, R, Q, w, U, H, side,
-                                           reinterpret_cast<float *>(blocks), s);
+                                           reinterpret_cast<float *>(blocks), kr, shifts, S, s);
         if (e == cudaSuccess) {
             count_launches(1);
             if (timed) timing_span(ev0, timing_event(s), TK_COMPRESS);
@@ -195,14 +211,31 @@ extern "C" rsvd_status rsvd_compress(const void *rings, int64_t n, int32_t R, in
     float2 *bl = reinterpret_cast<float2 *>(blocks);
     cudaError_t e;
     switch (ilog2(Q)) {
-        case 5: e = launch_compress<5>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, s); break;
-        case 6: e = launch_compress<6>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, s); break;
-        case 7: e = launch_compress<7>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, s); break;
-        case 8: e = launch_compress<8>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, s); break;
-        case 9: e = launch_compress<9>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, s); break;
-        default: e = launch_compress<10>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, s); break;
+        case 5: e = launch_compress<5>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, kr, shifts, S, s); break;
+        case 6: e = launch_compress<6>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, kr, shifts, S, s); break;
+        case 7: e = launch_compress<7>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, kr, shifts, S, s); break;
+        case 8: e = launch_compress<8>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, kr, shifts, S, s); break;
+        case 9: e = launch_compress<9>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, kr, shifts, S, s); break;
+        default: e = launch_compress<10>(rg, n, R, w, U, H, side, rows_pad, Kpad, bl, kr, shifts, S, s); break;
     }
     return cuda_check(e, "compress launch");
+}
+
+extern "C" rsvd_status rsvd_compress(const void *rings, int64_t n, int32_t R, int32_t Q, const double *w,
+                                     const double *U, int32_t H, rsvd_side side, void *blocks,
+                                     rsvd_stream_t stream) {
+    return compress_impl(rings, n, R, Q, w, U, H, side, blocks, nullptr, nullptr, 1, stream);
+}
+
+extern "C" rsvd_status rsvd_compress_translated(const void *rings, int64_t n_base, int32_t R, int32_t Q,
+                                                const double *w, const double *k, const double *U, int32_t H,
+                                                const double *shifts, int32_t S, rsvd_side side, void *blocks,
+                                                rsvd_stream_t stream) {
+    if (S < 1) return fail(RSVD_ERR_ARG, "S must be >= 1");
+    if (n_base < 0) return fail(RSVD_ERR_ARG, "n_base must be >= 0");
+    if (n_base > 0x7fffffffLL / S) return fail(RSVD_ERR_UNSUPPORTED, "too many rows in one call");
+    if (n_base > 0 && (!k || !shifts)) return fail(RSVD_ERR_ARG, "NULL pointer");
+    return compress_impl(rings, n_base * S, R, Q, w, U, H, side, blocks, k, shifts, S, stream);
 }
 
 extern "C" rsvd_status rsvd_blocks_unpack(const void *blocks, int64_t n, int32_t Q, int32_t H, rsvd_side side,

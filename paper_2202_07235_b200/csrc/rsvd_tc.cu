@@ -418,7 +418,9 @@ __global__ void __launch_bounds__(CptCfg<(1 << LOGQ)>::THREADS, 1) compress_tc_k
                                                                      const double *__restrict__ w,
                                                                      const double *__restrict__ U, int H, int side,
                                                                      int KB, int64_t op_rows, int slab_rings,
-                                                                     __half *__restrict__ ops, float *__restrict__ scales) {
+                                                                     __half *__restrict__ ops, float *__restrict__ scales,
+                                                                     const double *__restrict__ kr,
+                                                                     const double *__restrict__ shifts, int S) {
     constexpr int Q = 1 << LOGQ;
     constexpr int L = 32;
     constexpr int E = Q / L;
@@ -432,10 +434,23 @@ __global__ void __launch_bounds__(CptCfg<(1 << LOGQ)>::THREADS, 1) compress_tc_k
     float *up = reinterpret_cast<float *>(at + (size_t)H * Q);        // [R][HC]
     float *red = up + (size_t)R * HC;                                 // [33]
     uint64_t *bar = reinterpret_cast<uint64_t *>(red + 34);           // [2] (8-byte aligned: 34 floats)
-    const int64_t row = blockIdx.x;
+    const int64_t row = blockIdx.x;                                   // output row = base * S + shift
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const float2 *ring = rings + row * (int64_t)R * Q;
+    const float2 *ring = rings + (row / S) * (int64_t)R * Q;
     const int nslab = (R + slab_rings - 1) / slab_rings;
+    // row f2: translated copy s of the base row, a[r][j] exp(-i k_r (dx cos psi_j + dy sin psi_j))
+    // (the Fourier shift theorem with the convention of PAPER.md:80; reading G15)
+    float uj[JPT];
+    if (shifts) {
+        const int sh = (int)(row % S);
+        const double dx = shifts[2 * sh], dy = shifts[2 * sh + 1];
+#pragma unroll
+        for (int jj = 0; jj < JPT; ++jj) {
+            double sn, cs;
+            sincospi(2.0 * (double)(tid + CPT_THREADS * jj) / (double)Q, &sn, &cs);
+            uj[jj] = (float)(dx * cs + dy * sn);
+        }
+    }
     auto issue = [&](int s, int buf) {                                // thread 0
         const int r0 = s * slab_rings, nr = min(slab_rings, R - r0);
         const uint32_t bytes = (uint32_t)nr * Q * 8u;
@@ -492,6 +507,15 @@ __global__ void __launch_bounds__(CptCfg<(1 << LOGQ)>::THREADS, 1) compress_tc_k
                     float2 a[JPT];
 #pragma unroll
                     for (int jj = 0; jj < JPT; ++jj) a[jj] = sl[rr * Q + tid + CPT_THREADS * jj];
+                    if (shifts) {
+                        const float k = (float)kr[r0 + rr];
+#pragma unroll
+                        for (int jj = 0; jj < JPT; ++jj) {
+                            float sn, cs;
+                            sincosf(-k * uj[jj], &sn, &cs);
+                            a[jj] = make_float2(a[jj].x * cs - a[jj].y * sn, a[jj].x * sn + a[jj].y * cs);
+                        }
+                    }
 #pragma unroll
                     for (int g = 0; g < HC / 4; ++g) {
                         const float4 u = u4[g];
@@ -580,7 +604,8 @@ void set_path(int p) { g_path = (p == PATH_SIMT || p == PATH_TC) ? p : PATH_AUTO
 
 template <int LOGQ, int HC>
 static cudaError_t launch_compress_tc_qh(const float2 *rings, int64_t n, int R, const double *w, const double *U, int H,
-                                         int side, void *blocks, cudaStream_t s) {
+                                         int side, void *blocks, const double *kr, const double *shifts, int S,
+                                         cudaStream_t s) {
     const int Q = 1 << LOGQ;
     const int sr = compress_slab_rings(Q, H, R);
     if (sr < 1) return cudaErrorInvalidValue;
@@ -590,29 +615,31 @@ static cudaError_t launch_compress_tc_qh(const float2 *rings, int64_t n, int R, 
     float *scales = const_cast<float *>(tc_scales(blocks, n, Q, H, side));
     compress_tc_kernel<LOGQ, HC><<<(unsigned)n, CptCfg<(1 << LOGQ)>::THREADS, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H),
                                                                         tc_op_rows(n, side), sr,
-                                                                        reinterpret_cast<__half *>(blocks), scales);
+                                                                        reinterpret_cast<__half *>(blocks), scales,
+                                                                        kr, shifts, S);
     return cudaGetLastError();
 }
 template <int LOGQ>
 static cudaError_t launch_compress_tc_q(const float2 *rings, int64_t n, int R, const double *w, const double *U, int H,
-                                        int side, void *blocks, cudaStream_t s) {
+                                        int side, void *blocks, const double *kr, const double *shifts, int S,
+                                        cudaStream_t s) {
     switch (compress_hc(H)) {
-        case 8: return launch_compress_tc_qh<LOGQ, 8>(rings, n, R, w, U, H, side, blocks, s);
-        case 16: return launch_compress_tc_qh<LOGQ, 16>(rings, n, R, w, U, H, side, blocks, s);
-        case 24: return launch_compress_tc_qh<LOGQ, 24>(rings, n, R, w, U, H, side, blocks, s);
-        default: return launch_compress_tc_qh<LOGQ, 32>(rings, n, R, w, U, H, side, blocks, s);
+        case 8: return launch_compress_tc_qh<LOGQ, 8>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+        case 16: return launch_compress_tc_qh<LOGQ, 16>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+        case 24: return launch_compress_tc_qh<LOGQ, 24>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+        default: return launch_compress_tc_qh<LOGQ, 32>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
     }
 }
 
 cudaError_t launch_compress_tc(const float2 *rings, int64_t n, int R, int Q, const double *w, const double *U, int H,
-                               int side, float *blocks, cudaStream_t s) {
+                               int side, float *blocks, const double *kr, const double *shifts, int S, cudaStream_t s) {
     switch (ilog2(Q)) {
-        case 5: return launch_compress_tc_q<5>(rings, n, R, w, U, H, side, blocks, s);
-        case 6: return launch_compress_tc_q<6>(rings, n, R, w, U, H, side, blocks, s);
-        case 7: return launch_compress_tc_q<7>(rings, n, R, w, U, H, side, blocks, s);
-        case 8: return launch_compress_tc_q<8>(rings, n, R, w, U, H, side, blocks, s);
-        case 9: return launch_compress_tc_q<9>(rings, n, R, w, U, H, side, blocks, s);
-        default: return launch_compress_tc_q<10>(rings, n, R, w, U, H, side, blocks, s);
+        case 5: return launch_compress_tc_q<5>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+        case 6: return launch_compress_tc_q<6>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+        case 7: return launch_compress_tc_q<7>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+        case 8: return launch_compress_tc_q<8>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+        case 9: return launch_compress_tc_q<9>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+        default: return launch_compress_tc_q<10>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
     }
 }
 

@@ -106,6 +106,13 @@ def test_translations_streamed_landscape_and_argmax():
     w = to_np(d.w)
     U, _ = api.build_basis(d.templates, w, H)
     ib, tb = _blocks(d, U, H)
+    # row f2: the 9 translated copies compressed from the 4096 base images (shift 4 is (0, 0))
+    fused = api.compress_translated(d.images[4::9].contiguous(), d.w.contiguous(), d.k.contiguous(),
+                                    cuda(U, torch.float64), d.shift[:9].contiguous(), api.SIDE_IMAGE)
+    cf = api.blocks_unpack(fused, M, Q, H, api.SIDE_IMAGE)
+    cm = api.blocks_unpack(ib, M, Q, H, api.SIDE_IMAGE)
+    assert float((cf - cm).abs().max()) <= 2e-6 * float(cm.abs().max())
+    del cf, cm, fused
     work = torch.empty(WORK // 4, dtype=torch.float32, device="cuda")
     val, k = api.align_argmax(ib, M, tb, T, Q, H, api.PER_PAIR, work)
     val, k = to_np(val), to_np(k)

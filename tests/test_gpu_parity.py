@@ -334,3 +334,40 @@ def test_fine_gamma_landscape_and_refined_argmax(Q, p):
     v, ti, ki = (to_np(x) for x in api.winners_unpack(keys, Qo))
     assert np.abs(v - val.max(1)).max() <= 1e-6 * np.abs(X).max()
     assert np.all(val[np.arange(M), ti] == v)
+
+
+def test_translations_fused_into_compress():
+    """Row f2: rsvd_compress_translated builds the S phase-ramped copies of each base ring in the
+    compress kernel.  Its coefficients match compressing the materialised copies, and the alignment
+    of the fused blocks matches the oracle on rings translated in fp64 by the test itself
+    (a exp(-i k_r (dx cos psi + dy sin psi)), reading G15)."""
+    d = make_dataset("translations", M=20, T=40, device="cuda")
+    H, Q, R = 16, d.Q, d.R
+    S = 9
+    base = d.images[4::S].contiguous()                     # shift 4 is (0, 0): the base images
+    shifts = d.shift[:S].contiguous()
+    w, kr = d.w.contiguous(), d.k.contiguous()
+    U, _ = api.build_basis(d.templates, to_np(w), H)
+    Ud = cuda(U, torch.float64)
+    fused = api.compress_translated(base, w, kr, Ud, shifts, api.SIDE_IMAGE)
+    mat = api.compress(d.images, w, Ud, api.SIDE_IMAGE)
+    M = base.shape[0] * S
+    cf = to_np(api.blocks_unpack(fused, M, Q, H, api.SIDE_IMAGE))
+    cm = to_np(api.blocks_unpack(mat, M, Q, H, api.SIDE_IMAGE))
+    assert np.abs(cf - cm).max() <= 2e-6 * np.abs(cm).max()
+    tb = api.compress(d.templates, w, Ud, api.SIDE_TEMPLATE)
+    T = d.templates.shape[0]
+    work = torch.empty(api.align_workspace_bytes(M, T, Q, H) // 4, dtype=torch.float32, device="cuda")
+    val, k = (to_np(x) for x in api.align_argmax(fused, M, tb, T, Q, H, api.PER_PAIR, work))
+    # oracle: translate the base rings in fp64 here, then the rank-H direct sum
+    psi = 2 * np.pi * np.arange(Q) / Q
+    sh, kk = to_np(shifts), to_np(kr)
+    b64 = to_np(base).astype(np.complex128)
+    A = np.stack([b64[b] * np.exp(-1j * kk[:, None] * (sh[s, 0] * np.cos(psi) + sh[s, 1] * np.sin(psi))[None, :])
+                  for b in range(base.shape[0]) for s in range(S)])
+    rng = np.random.default_rng(3)
+    m, t = rng.integers(0, M, 150), rng.integers(0, T, 150)
+    X_ref = ref.landscape_rank(A, to_np(d.templates), to_np(w), U, m, t).real
+    tol_abs = TOL_FP32 * np.abs(X_ref).max()
+    assert np.abs(val[m, t] - X_ref.max(-1)).max() <= tol_abs
+    assert_argmax_gated(k[m, t], X_ref, tol_abs)
