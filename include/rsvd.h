@@ -136,6 +136,18 @@ rsvd_status rsvd_blocks_unpack(const void *blocks, int64_t n, int32_t Q, int32_t
  *   blocks: device, rsvd_block_bytes(n_base * S, Q, H, side) bytes.  Each base ring is read once
  *   from HBM (its S copies are built in registers); the ramp is evaluated in fp32 (|k d| <= ~2 rad
  *   on the configs: phase error ~1e-7).  S >= 1; NULL k / shifts with n_base > 0 are RSVD_ERR_ARG. */
+/* rsvd_build_basis_translated: as rsvd_build_basis, for the translation-averaged objective of
+ * Eq. eq_Image_single_cost_with_translations with a discrete distribution of S
+ * equally weighted shifts: C is averaged over the T x S translated templates (each angularly
+ * centred), C = (1/(T S Q)) sqrt(w w') sum_{t,s} Re sum_j W_ts W_ts^H.  The paper's closed form for a
+ * Gaussian shift distribution (:1152-1166) needs the molecule's spherical-harmonic coefficients,
+ * which a template set does not provide; this is the exact finite-sum kernel.  Host inputs: w, k
+ * [R] fp64 (weights, radial wavenumbers), shifts [S][2] fp64 (dx, dy).  The ramps are built in fp64
+ * on the device.  Synchronises; allocates scratch (S*R*Q complex fp64 + partials). */
+rsvd_status rsvd_build_basis_translated(const void *templates, int64_t T, int32_t R, int32_t Q,
+                                        const double *w_host, const double *k_host,
+                                        const double *shifts_host, int32_t S, int32_t H,
+                                        double *U_host, double *lambda_host, rsvd_stream_t stream);
 rsvd_status rsvd_compress_translated(const void *rings, int64_t n_base, int32_t R, int32_t Q,
                                      const double *w, const double *k, const double *U, int32_t H,
                                      const double *shifts, int32_t S, rsvd_side side, void *blocks,

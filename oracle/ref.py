@@ -29,6 +29,10 @@ F1 landscape_rank_fine Re X at gamma_k = 2 pi k / Q_out from the rank-H coeffici
                        directly (no FFT): "zero-padded prior to the FFT" with the
                        Nyquist bin split between +-Q/2 (reading G4).
 F1 argmax_refine       grid argmax + 3-point quadratic interpolation (SPEC.md argmax_refine).
+F2 translate           a exp(-i k_r (dx cos psi_j + dy sin psi_j)), the Fourier shift theorem with the
+                       transform convention of PAPER.md:80 (reading G15), fp64; the translation-averaged
+                       kernel of Eq. eq_Image_single_cost_with_translations (:1146-1150) for a discrete
+                       shift distribution is kernel_C of the translated templates.
 
 Parity pins for every function live in tests/test_oracle_pins.py.
 """
@@ -180,6 +184,20 @@ def landscape_rank_fine(A, B, w, U, ia, ib, Q_out: int) -> np.ndarray:
     E = np.exp(-1j * np.outer(qs, gam))                    # [freq, gamma]
     X = S[:, cols] @ E + S[:, N][:, None] * np.cos(N * gam)[None, :]
     return (2.0 * np.pi * X).real
+
+
+def translate(A, k, shifts) -> np.ndarray:
+    """F2: rows b*S + s = A[b] exp(-i k_r (dx_s cos psi_j + dy_s sin psi_j)) in fp64 (reading G15)."""
+    A = _c128(A)
+    n, R, Q = A.shape
+    k = np.asarray(k, dtype=np.float64)
+    sh = np.asarray(shifts, dtype=np.float64).reshape(-1, 2)
+    psi = 2.0 * np.pi * np.arange(Q) / Q
+    out = np.empty((n * sh.shape[0], R, Q), dtype=np.complex128)
+    for s, (dx, dy) in enumerate(sh):
+        ramp = np.exp(-1j * k[:, None] * (dx * np.cos(psi) + dy * np.sin(psi))[None, :])
+        out[s::sh.shape[0]] = A * ramp[None]
+    return out
 
 
 def argmax_refine(x: np.ndarray) -> np.ndarray:

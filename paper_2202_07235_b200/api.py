@@ -17,7 +17,7 @@ from ._lib import PER_IMAGE, PER_PAIR, SIDE_IMAGE, SIDE_TEMPLATE, RsvdError, che
 
 __all__ = ["block_bytes", "path_for", "set_path", "PATH_AUTO", "PATH_SIMT", "PATH_TC", "kernel_chunk", "kernel_partials_bytes", "align_workspace_bytes",
            "align_min_workspace_bytes", "kernel_partials", "kernel_reduce", "eigen_basis", "build_basis",
-           "compress", "compress_translated", "blocks_unpack", "align_argmax", "align_landscape", "align_argmax_fine",
+           "build_basis_translated", "compress", "compress_translated", "blocks_unpack", "align_argmax", "align_landscape", "align_argmax_fine",
            "align_landscape_fine", "winners_reset",
            "winners_unpack", "combine_winners", "launch_count", "timing_enable", "timing_read", "Aligner", "RsvdError", "PER_PAIR", "PER_IMAGE",
            "SIDE_IMAGE", "SIDE_TEMPLATE"]
@@ -96,6 +96,20 @@ def build_basis(templates: torch.Tensor, w, H: int, stream=None):
     lam = np.zeros(R, dtype=np.float64)
     check(_lib.lib().rsvd_build_basis(ptr(templates), T, R, Q, ptr(w), H, ptr(U), ptr(lam),
                                       stream_handle(stream)))
+    return U, lam
+
+
+def build_basis_translated(templates: torch.Tensor, w, k, shifts, H: int, stream=None):
+    """rsvd_build_basis_translated: basis of the kernel averaged over the S translated copies of
+    every template (row f2).  w, k: [R] radial weights / wavenumbers; shifts: [S, 2] (dx, dy)."""
+    require_cuda(templates)
+    T, R, Q = templates.shape
+    as64 = lambda x: np.ascontiguousarray(np.asarray(x.cpu() if torch.is_tensor(x) else x), dtype=np.float64)
+    w, k, sh = as64(w), as64(k), as64(shifts).reshape(-1, 2)
+    U = np.zeros((R, H), dtype=np.float64)
+    lam = np.zeros(R, dtype=np.float64)
+    check(_lib.lib().rsvd_build_basis_translated(ptr(templates), T, R, Q, ptr(w), ptr(k), ptr(sh), sh.shape[0], H,
+                                                 ptr(U), ptr(lam), stream_handle(stream)))
     return U, lam
 
 

@@ -26,9 +26,13 @@ constexpr int NTHR = 256;
 // r_a = ti*64 + ty + 16a and r'_b = tj*64 + tx + 16b, a, b < 4.  Samples are widened to fp64 once,
 // when staged in shared memory, so the inner loop is pure DFMA (products of fp32 values are exact in
 // fp64; accumulation order is fixed).
+// ramp (row f2, may be NULL): [S][R][Q] fp64 complex factors exp(-i k_r (dx_s cos psi_j + dy_s sin psi_j));
+// every template then contributes its S translated copies (the discrete translation average of
+// Eq. eq_Image_single_cost_with_translations).
 __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__restrict__ tmpl,
                                                                int64_t T, int R, int Q,
-                                                               double *__restrict__ partials) {
+                                                               double *__restrict__ partials,
+                                                               const double2 *__restrict__ ramp, int S) {
     const int ti = blockIdx.x, tj = blockIdx.y;
     if (ti < tj) return;
     const int64_t c = blockIdx.z;
@@ -46,7 +50,9 @@ __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__r
 
     const int64_t t_begin = c * KCHUNK;
     const int64_t t_end = min(T, t_begin + KCHUNK);
-    for (int64_t t = t_begin; t < t_end; ++t) {
+    for (int64_t ts = t_begin * S; ts < t_end * S; ++ts) {
+        const int64_t t = ts / S;
+        const double2 *rp = ramp ? ramp + (ts % S) * (int64_t)R * Q : nullptr;
         const float2 *bt = tmpl + t * (int64_t)R * Q;
         if (tid < BT) { si[tid][0] = si[tid][1] = 0.0; sj[tid][0] = sj[tid][1] = 0.0; }
         for (int j0 = 0; j0 < Q; j0 += JB) {
@@ -59,8 +65,15 @@ __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__r
                 const float2 z = make_float2(0.f, 0.f);
                 const float2 u = (r1 < R && j < Q) ? __ldg(bt + (int64_t)r1 * Q + j) : z;
                 const float2 v = (r2 < R && j < Q) ? __ldg(bt + (int64_t)r2 * Q + j) : z;
-                xi[rr][jj] = make_double2((double)u.x, (double)u.y);
-                xj[rr][jj] = make_double2((double)v.x, (double)v.y);
+                double2 du = make_double2((double)u.x, (double)u.y), dv = make_double2((double)v.x, (double)v.y);
+                if (rp) {                                  // translated copy: exact fp64 complex product
+                    const double2 a = (r1 < R && j < Q) ? rp[(int64_t)r1 * Q + j] : make_double2(1.0, 0.0);
+                    const double2 b = (r2 < R && j < Q) ? rp[(int64_t)r2 * Q + j] : make_double2(1.0, 0.0);
+                    du = make_double2(du.x * a.x - du.y * a.y, du.x * a.y + du.y * a.x);
+                    dv = make_double2(dv.x * b.x - dv.y * b.y, dv.x * b.y + dv.y * b.x);
+                }
+                xi[rr][jj] = du;
+                xj[rr][jj] = dv;
             }
             __syncthreads();
             // row sums (fp64, fixed order)
@@ -124,6 +137,20 @@ __global__ void kernel_reduce_kernel(const double *__restrict__ partials, int64_
     C[idx] = acc * scale * sqrt(w[r]) * sqrt(w[s]);
 }
 
+// ramp[s][r][j] = exp(-i k_r (dx_s cos psi_j + dy_s sin psi_j)), fp64 (row f2; reading G15)
+__global__ void ramp_kernel(const double *__restrict__ k, const double *__restrict__ shifts, int S, int R, int Q,
+                            double2 *__restrict__ ramp) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)S * R * Q) return;
+    const int j = (int)(idx % Q), r = (int)((idx / Q) % R), s = (int)(idx / ((int64_t)R * Q));
+    double sn, cs;
+    sincospi(2.0 * j / (double)Q, &sn, &cs);
+    const double ph = -k[r] * (shifts[2 * s] * cs + shifts[2 * s + 1] * sn);
+    double ps, pc;
+    sincos(ph, &ps, &pc);
+    ramp[idx] = make_double2(pc, ps);
+}
+
 }  // namespace rsvd
 
 using namespace rsvd;
@@ -166,7 +193,7 @@ extern "C" rsvd_status rsvd_kernel_partials(const void *templates, int64_t T, in
         attr = true;
     }
     kernel_partials_kernel<<<grid, NTHR, KP_SMEM, (cudaStream_t)stream>>>(
-        reinterpret_cast<const float2 *>(templates), T, R, Q, partials);
+        reinterpret_cast<const float2 *>(templates), T, R, Q, partials, nullptr, 1);
     count_launches(1);
     if (timed) timing_span(ev0, timing_event((cudaStream_t)stream), TK_BASIS);
     return cuda_check(cudaGetLastError(), "kernel_partials launch");
@@ -185,6 +212,76 @@ extern "C" rsvd_status rsvd_kernel_reduce(const double *partials, int64_t nchunk
         partials, nchunks, R, scale, w, C);
     count_launches(1);
     return cuda_check(cudaGetLastError(), "kernel_reduce launch");
+}
+
+extern "C" rsvd_status rsvd_build_basis_translated(const void *templates, int64_t T, int32_t R, int32_t Q,
+                                                   const double *w_host, const double *k_host,
+                                                   const double *shifts_host, int32_t S, int32_t H, double *U_host,
+                                                   double *lambda_host, rsvd_stream_t stream) {
+    rsvd_status st = check_grid(R, Q);
+    if (st != RSVD_OK) return st;
+    if (T <= 0) return fail(RSVD_ERR_ARG, "T must be >= 1 to build a basis");
+    if (S < 1) return fail(RSVD_ERR_ARG, "S must be >= 1");
+    if (H < 1 || H > R) return fail(RSVD_ERR_UNSUPPORTED, "H must satisfy 1 <= H <= R");
+    if (!templates || !w_host || !k_host || !shifts_host || !U_host) return fail(RSVD_ERR_ARG, "NULL pointer");
+    if (!aligned16(templates)) return fail(RSVD_ERR_ARG, "misaligned pointer");
+    for (int r = 0; r < R; ++r)
+        if (!std::isfinite(w_host[r]) || !(w_host[r] > 0.0) || !std::isfinite(k_host[r]))
+            return fail(RSVD_ERR_ARG, "weights must be finite and > 0, wavenumbers finite");
+    for (int i = 0; i < 2 * S; ++i)
+        if (!std::isfinite(shifts_host[i])) return fail(RSVD_ERR_ARG, "shifts must be finite");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nchunks = (T + KCHUNK - 1) / KCHUNK;
+    if (nchunks > 65535) return fail(RSVD_ERR_UNSUPPORTED, "too many template chunks in one call");
+    const size_t pbytes = (size_t)nchunks * R * R * sizeof(double);
+    const size_t rbytes = (size_t)S * R * Q * sizeof(double2);
+    const size_t wbytes = (size_t)R * sizeof(double), cbytes = (size_t)R * R * sizeof(double);
+    const size_t kbytes = (size_t)R * sizeof(double), sbytes = (size_t)2 * S * sizeof(double);
+    void *scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, rbytes + pbytes + wbytes + cbytes + kbytes + sbytes, s);
+    if (e != cudaSuccess) return cuda_check(e, "cudaMallocAsync(basis scratch)");
+    double2 *ramp = (double2 *)scratch;
+    double *partials = (double *)((char *)scratch + rbytes);
+    double *w_dev = partials + (size_t)nchunks * R * R;
+    double *C_dev = w_dev + R;
+    double *k_dev = C_dev + (size_t)R * R;
+    double *s_dev = k_dev + R;
+    std::vector<double> C((size_t)R * R);
+    st = RSVD_OK;
+    if ((e = cudaMemcpyAsync(w_dev, w_host, wbytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) st = cuda_check(e, "copy w");
+    if (st == RSVD_OK && (e = cudaMemcpyAsync(k_dev, k_host, kbytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        st = cuda_check(e, "copy k");
+    if (st == RSVD_OK && (e = cudaMemcpyAsync(s_dev, shifts_host, sbytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        st = cuda_check(e, "copy shifts");
+    if (st == RSVD_OK) {
+        const int64_t n = (int64_t)S * R * Q;
+        ramp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(k_dev, s_dev, S, R, Q, ramp);
+        count_launches(1);
+        st = cuda_check(cudaGetLastError(), "ramp launch");
+    }
+    if (st == RSVD_OK) {
+        static bool attr = false;
+        if (!attr) {
+            e = cudaFuncSetAttribute(kernel_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KP_SMEM);
+            if (e != cudaSuccess) st = cuda_check(e, "kernel_partials attribute");
+            attr = (e == cudaSuccess);
+        }
+    }
+    if (st == RSVD_OK) {
+        const int nt = (R + BT - 1) / BT;
+        dim3 grid(nt, nt, (unsigned)nchunks);
+        kernel_partials_kernel<<<grid, NTHR, KP_SMEM, s>>>(reinterpret_cast<const float2 *>(templates), T, R, Q,
+                                                          partials, ramp, S);
+        count_launches(1);
+        st = cuda_check(cudaGetLastError(), "kernel_partials (translated) launch");
+    }
+    if (st == RSVD_OK) st = rsvd_kernel_reduce(partials, nchunks, R, T * (int64_t)S, Q, w_dev, C_dev, stream);
+    if (st == RSVD_OK && (e = cudaMemcpyAsync(C.data(), C_dev, cbytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        st = cuda_check(e, "copy C");
+    cudaFreeAsync(scratch, s);
+    if (st != RSVD_OK) return st;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_check(e, "basis sync");
+    return rsvd_eigen_basis(C.data(), R, H, U_host, lambda_host);
 }
 
 extern "C" rsvd_status rsvd_build_basis(const void *templates, int64_t T, int32_t R, int32_t Q,

@@ -371,3 +371,28 @@ def test_translations_fused_into_compress():
     tol_abs = TOL_FP32 * np.abs(X_ref).max()
     assert np.abs(val[m, t] - X_ref.max(-1)).max() <= tol_abs
     assert_argmax_gated(k[m, t], X_ref, tol_abs)
+
+
+def test_translation_averaged_basis():
+    """Row f2: rsvd_build_basis_translated (fp64 ramps on the device, every template's S translated
+    copies in the kernel partials) against the oracle's kernel of the fp64-translated templates."""
+    d = make_dataset("small", T=96, M=8)
+    B, w, k = to_np(d.templates), to_np(d.w), to_np(d.k)
+    R = d.R
+    shifts = np.array([[0.0, 0.0], [0.03, 0.0], [0.0, -0.03], [0.02, 0.02]])
+    U, lam = api.build_basis_translated(cuda(B), w, k, shifts, R)
+    C_ref = ref.kernel_C(ref.translate(B, k, shifts), w)
+    Ur, lr = ref.basis(C_ref, R)
+    assert np.abs(lam - lr).max() <= 1e-12 * lr[0]
+    assert np.linalg.norm(C_ref @ U - U * lam[None, :]) <= 1e-11 * lr[0]
+    nz = int((lr > 1e-9 * lr[0]).sum())
+    for h in range(1, nz):
+        relgap = (lr[h - 1] - lr[h]) / lr[0]
+        if relgap < 1e-6:
+            continue
+        P = U[:, :h] @ U[:, :h].T
+        Pr = Ur[:, :h] @ Ur[:, :h].T
+        assert np.linalg.norm(P - Pr, 2) <= 1e-9 / relgap, (h, relgap)
+    # shifts change the kernel (the test is not vacuous)
+    U0, lam0 = api.build_basis(cuda(B), w, R)
+    assert np.abs(lam0 - lam).max() > 1e-6 * lam0[0]

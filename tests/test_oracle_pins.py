@@ -437,3 +437,44 @@ def test_F1_argmax_refine_spec_examples():
     g = ref.argmax_refine(cyc)
     d = (3.0 - 1.0) / (2 * (3.0 - 8.0 + 1.0))
     assert abs(g - np.mod(2 * np.pi * d / Q, 2 * np.pi)) < 1e-12
+
+
+# ------------------------------------------------------------------ F2: translations
+def test_F2_translate_is_the_shift_theorem_of_the_analytic_templates():
+    """translate() (reading G15) against the generator's analytic transform: moving every atom of a
+    slice by (dx, dy) must equal ramping the unmoved slice.  Catches a sign error in the ramp (it
+    would move the atoms the other way), swapped cos/sin or a missing k_r."""
+    import torch
+    from synth.generator import _slice_rows
+    R, Q = 6, 32
+    k, w = radial_grid(R)
+    rng = np.random.default_rng(5)
+    p1 = torch.tensor(rng.uniform(-0.3, 0.3, (1, 7)))
+    p2 = torch.tensor(rng.uniform(-0.3, 0.3, (1, 7)))
+    kt = torch.tensor(k)
+    g0 = torch.zeros(1, dtype=torch.float64)
+    base = _slice_rows(p1, p2, g0, kt, Q).numpy()
+    shifts = np.array([[0.02, -0.03], [-0.05, 0.0], [0.0, 0.0]])
+    tr = ref.translate(base, k, shifts)
+    for s, (dx, dy) in enumerate(shifts):
+        moved = _slice_rows(p1 + dx, p2 + dy, g0, kt, Q).numpy()[0]
+        np.testing.assert_allclose(tr[s], moved, atol=1e-12 * np.abs(moved).max())
+
+
+def test_F2_translation_averaged_kernel_reduces_to_O3():
+    """With the single shift (0, 0) the translation-averaged kernel is O3's kernel; with shifts the
+    kernel stays symmetric PSD and rotation-invariant (each translated template's C contribution is
+    invariant to rotating it, P9).  Catches a mis-normalised average over shifts."""
+    rng = np.random.default_rng(6)
+    R, Q = 5, 16
+    k, w = radial_grid(R)
+    B = _rand_rings(rng, 4, R, Q)
+    C0 = ref.kernel_C(B, w)
+    np.testing.assert_allclose(ref.kernel_C(ref.translate(B, k, [[0.0, 0.0]]), w), C0, atol=1e-14 * np.abs(C0).max())
+    sh = [[0.01, 0.0], [0.0, -0.02], [0.015, 0.015]]
+    Ct = ref.kernel_C(ref.translate(B, k, sh), w)
+    assert np.abs(Ct - Ct.T).max() <= 1e-15 * np.abs(Ct).max()
+    assert np.linalg.eigvalsh(Ct).min() >= -1e-12 * np.abs(Ct).max()
+    # averaging over the 3 shifts == averaging the 3 single-shift kernels
+    Cs = sum(ref.kernel_C(ref.translate(B, k, [s]), w) for s in sh) / 3
+    np.testing.assert_allclose(Ct, Cs, atol=1e-13 * np.abs(Ct).max())
