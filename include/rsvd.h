@@ -105,6 +105,15 @@ rsvd_status rsvd_kernel_partials(const void *templates, int64_t T, int32_t R, in
 rsvd_status rsvd_kernel_reduce(const double *partials, int64_t nchunks, int32_t R, int64_t T_total,
                                int32_t Q, const double *w, double *C, rsvd_stream_t stream);
 rsvd_status rsvd_eigen_basis(const double *C, int32_t R, int32_t H, double *U, double *lambda);
+/* Row f3 (per-CTF-group bases; PAPER.md:715-724 builds one kernel and basis per CTF): host only.
+ * For targets = templates multiplied ring by ring by a radial CTF ctf[r] = c_g(k_r), the group's
+ * kernel is diag(ctf) C diag(ctf) with C the raw templates' kernel (rsvd_kernel_reduce output
+ * copied to the host), so one kernel-partials pass serves every group.  U (host [R][H]): the group
+ * basis, used to compress the group's images; U_tmpl (host [R][H], may be NULL) = diag(ctf) U:
+ * compressing the RAW templates with it yields the group's CTF-corrected targets.  Same
+ * eigen-solver, ordering, sign rule and errors as rsvd_eigen_basis; non-finite ctf is RSVD_ERR_ARG. */
+rsvd_status rsvd_eigen_basis_ctf(const double *C, int32_t R, const double *ctf, int32_t H, double *U,
+                                 double *U_tmpl, double *lambda);
 rsvd_status rsvd_build_basis(const void *templates, int64_t T, int32_t R, int32_t Q,
                              const double *w_host, int32_t H, double *U_host, double *lambda_host,
                              rsvd_stream_t stream);

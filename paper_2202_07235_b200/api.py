@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import PER_IMAGE, PER_PAIR, SIDE_IMAGE, SIDE_TEMPLATE, RsvdError, check, ptr, require_cuda, stream_handle
 
 __all__ = ["block_bytes", "path_for", "set_path", "PATH_AUTO", "PATH_SIMT", "PATH_TC", "kernel_chunk", "kernel_partials_bytes", "align_workspace_bytes",
-           "align_min_workspace_bytes", "kernel_partials", "kernel_reduce", "eigen_basis", "build_basis",
+           "align_min_workspace_bytes", "kernel_partials", "kernel_reduce", "eigen_basis", "eigen_basis_ctf", "ctf_group_bases", "build_basis",
            "build_basis_translated", "compress", "compress_translated", "blocks_unpack", "align_argmax", "align_landscape", "align_argmax_fine",
            "align_landscape_fine", "winners_reset",
            "winners_unpack", "combine_winners", "launch_count", "timing_enable", "timing_read", "Aligner", "RsvdError", "PER_PAIR", "PER_IMAGE",
@@ -85,6 +85,28 @@ def eigen_basis(C: np.ndarray, H: int):
     lam = np.zeros(R, dtype=np.float64)
     check(_lib.lib().rsvd_eigen_basis(ptr(C), R, H, ptr(U), ptr(lam)))
     return U, lam
+
+
+def eigen_basis_ctf(C: np.ndarray, ctf, H: int):
+    """rsvd_eigen_basis_ctf (row f3): (U, U_tmpl, lambda) of one CTF group from the raw kernel C."""
+    C = np.ascontiguousarray(C, dtype=np.float64)
+    R = C.shape[0]
+    ctf = np.ascontiguousarray(np.asarray(ctf), dtype=np.float64)
+    U = np.zeros((R, H), dtype=np.float64)
+    Ut = np.zeros((R, H), dtype=np.float64)
+    lam = np.zeros(R, dtype=np.float64)
+    check(_lib.lib().rsvd_eigen_basis_ctf(ptr(C), R, ptr(ctf), H, ptr(U), ptr(Ut), ptr(lam)))
+    return U, Ut, lam
+
+
+def ctf_group_bases(templates: torch.Tensor, w: torch.Tensor, ctfs, H: int):
+    """Row f3: one kernel-partials pass over the raw templates, then per CTF group g (ctfs[g] = c_g(k_r),
+    [G, R]) the group basis U_g (for its images) and U_tmpl_g = diag(c_g) U_g (compresses the raw
+    templates into the group's CTF-corrected targets).  Returns [(U_g, U_tmpl_g, lambda_g)]."""
+    require_cuda(templates, w)
+    T, R, Q = templates.shape
+    C = kernel_reduce(kernel_partials(templates), T, Q, w).cpu().numpy()
+    return [eigen_basis_ctf(C, c, H) for c in np.asarray(ctfs, dtype=np.float64).reshape(-1, R)]
 
 
 def build_basis(templates: torch.Tensor, w, H: int, stream=None):

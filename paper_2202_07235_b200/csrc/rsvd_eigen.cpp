@@ -182,3 +182,26 @@ extern "C" rsvd_status rsvd_eigen_basis(const double *C, int32_t R, int32_t H, d
         for (int i = 0; i < n; ++i) lambda[i] = d[order[i]];
     return RSVD_OK;
 }
+
+// Row f3 (per-CTF-group bases): targets of CTF group g are the templates multiplied
+// ring by ring by a radial CTF c_g(k_r), so that group's kernel is D C D with D = diag(c_g) (C the
+// kernel of the raw templates: every term of C is bilinear in one ring r and one ring r').  U is the
+// basis of D C D (for the group's images); U_tmpl = D U compresses the RAW templates into the
+// group's CTF-corrected targets (the projection sum_r U[r,h] sqrt(w_r) c_g(k_r) b[r,j]).
+extern "C" rsvd_status rsvd_eigen_basis_ctf(const double *C, int32_t R, const double *ctf, int32_t H, double *U,
+                                            double *U_tmpl, double *lambda) {
+    using rsvd::fail;
+    if (R <= 0 || R > 256) return fail(RSVD_ERR_UNSUPPORTED, "R must be in [1, 256]");
+    if (!C || !ctf || !U) return fail(RSVD_ERR_ARG, "NULL pointer");
+    std::vector<double> Cg((size_t)R * R);
+    for (int r = 0; r < R; ++r) {
+        if (!std::isfinite(ctf[r])) return fail(RSVD_ERR_ARG, "CTF values must be finite");
+        for (int c = 0; c < R; ++c) Cg[(size_t)r * R + c] = ctf[r] * C[(size_t)r * R + c] * ctf[c];
+    }
+    const rsvd_status st = rsvd_eigen_basis(Cg.data(), R, H, U, lambda);
+    if (st != RSVD_OK) return st;
+    if (U_tmpl)
+        for (int r = 0; r < R; ++r)
+            for (int h = 0; h < H; ++h) U_tmpl[(size_t)r * H + h] = ctf[r] * U[(size_t)r * H + h];
+    return RSVD_OK;
+}

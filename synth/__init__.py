@@ -2,4 +2,4 @@
 
 Holds none of the method's arithmetic (see generator.py's header)."""
 from .generator import (CONFIGS, Dataset, make_dataset, radial_grid, sample_pairs,  # noqa: F401
-                        counter_complex_normal, counter_uniform, view_frames, molecule_centres)
+                        counter_complex_normal, counter_uniform, view_frames, molecule_centres, toy_ctf)

@@ -278,6 +278,13 @@ def make_dataset(name: str, device="cpu", *, M: int | None = None, T: int | None
                    t_range=(t0, t1), meta=meta)
 
 
+def toy_ctf(k, lam: float) -> np.ndarray:
+    """Radial toy contrast-transfer function c(k) = -sin(pi lam k^2 / 2) (SPEC.md design decision:
+    sign-oscillating contrast; real per-micrograph CTFs are out of scope).  Input model for row f3."""
+    k = np.asarray(k.cpu() if torch.is_tensor(k) else k, dtype=np.float64)
+    return -np.sin(np.pi * lam * k * k / 2.0)
+
+
 def sample_pairs(name: str, M: int, T: int, n_random: int, n_true: int, t_true=None):
     """Seeded (m, t) pair sample: n_random uniform pairs plus n_true (m, t*(m)) pairs."""
     rng = np.random.default_rng(seed_children(CONFIGS[name]["cfg"])[5])

@@ -396,3 +396,30 @@ def test_translation_averaged_basis():
     # shifts change the kernel (the test is not vacuous)
     U0, lam0 = api.build_basis(cuda(B), w, R)
     assert np.abs(lam0 - lam).max() > 1e-6 * lam0[0]
+
+
+def test_ctf_group_bases_end_to_end():
+    """Row f3: two CTF groups sharing one kernel-partials pass.  Group g's images carry c_g; its
+    targets are the raw templates compressed with diag(c_g) U_g; the alignment equals the oracle's
+    rank-H landscape of (images_g, c_g * templates) through U_g."""
+    from synth import toy_ctf
+    d = make_dataset("small", M=24, T=60, device="cuda")
+    H, Q, R = 8, d.Q, d.R
+    k = to_np(d.k)
+    ctfs = np.stack([toy_ctf(k, 0.02), toy_ctf(k, 0.035)])
+    w = d.w.contiguous()
+    bases = api.ctf_group_bases(d.templates, w, ctfs, H)
+    T = d.templates.shape[0]
+    work = torch.empty(api.align_workspace_bytes(24, T, Q, H) // 4, dtype=torch.float32, device="cuda")
+    B = to_np(d.templates)
+    for g, (U, Ut, lam) in enumerate(bases):
+        c = torch.tensor(ctfs[g], dtype=torch.complex64, device="cuda")
+        imgs = (d.images * c[None, :, None]).contiguous()
+        ib = api.compress(imgs, w, cuda(U, torch.float64), api.SIDE_IMAGE)
+        tb = api.compress(d.templates, w, cuda(Ut, torch.float64), api.SIDE_TEMPLATE)
+        X = to_np(api.align_landscape(ib, 24, tb, T, Q, H, work))
+        rng = np.random.default_rng(g)
+        m, t = rng.integers(0, 24, 80), rng.integers(0, T, 80)
+        Bg = (B.astype(np.complex128) * ctfs[g][None, :, None])
+        X_ref = ref.landscape_rank(to_np(imgs), Bg, to_np(w), U, m, t).real
+        assert np.abs(X[m, t] - X_ref).max() <= TOL_FP32 * np.abs(X_ref).max()

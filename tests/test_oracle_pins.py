@@ -478,3 +478,38 @@ def test_F2_translation_averaged_kernel_reduces_to_O3():
     # averaging over the 3 shifts == averaging the 3 single-shift kernels
     Cs = sum(ref.kernel_C(ref.translate(B, k, [s]), w) for s in sh) / 3
     np.testing.assert_allclose(Ct, Cs, atol=1e-13 * np.abs(Ct).max())
+
+
+# ------------------------------------------------------------------ F3: per-CTF-group bases
+def test_F3_ctf_group_kernel_is_diagonally_scaled():
+    """For targets multiplied ring-wise by a radial CTF c(k_r), O3's kernel is diag(c) C diag(c):
+    every term of C is bilinear in one ring r and one ring r'.  Catches a CTF applied to the weights
+    instead of the rings (c^2 on the diagonal only) or a transposed scaling."""
+    from synth import toy_ctf
+    rng = np.random.default_rng(8)
+    R, Q = 6, 16
+    k, w = radial_grid(R)
+    B = _rand_rings(rng, 5, R, Q)
+    c = toy_ctf(k, 0.05)
+    assert np.all(np.abs(c) > 1e-3)                      # not degenerate at these k
+    C = ref.kernel_C(B, w)
+    Cg = ref.kernel_C(B * c[None, :, None], w)
+    np.testing.assert_allclose(Cg, c[:, None] * C * c[None, :], atol=1e-13 * np.abs(Cg).max())
+
+
+def test_F3_library_ctf_basis_matches_oracle(lib_built=None):
+    """Host entry rsvd_eigen_basis_ctf (no GPU): its U is the oracle basis of the CTF-corrected
+    targets' kernel (projector agreement), and U_tmpl = diag(c) U."""
+    from synth import toy_ctf
+    from paper_2202_07235_b200 import api, build
+    build.build()
+    rng = np.random.default_rng(9)
+    R, Q, H = 8, 16, 4
+    k, w = radial_grid(R)
+    B = _rand_rings(rng, 40, R, Q)
+    c = toy_ctf(k, 0.05)
+    U, Ut, lam = api.eigen_basis_ctf(ref.kernel_C(B, w), c, H)
+    Ur, lr = ref.basis(ref.kernel_C(B * c[None, :, None], w), H)
+    assert np.abs(lam - lr).max() <= 1e-12 * lr[0]
+    assert np.linalg.norm(U @ U.T - Ur @ Ur.T, 2) <= 1e-9 / ((lr[H - 1] - lr[H]) / lr[0])
+    np.testing.assert_allclose(Ut, c[:, None] * U, rtol=0, atol=1e-15)
