@@ -52,6 +52,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-kernel-timing", action="store_true", help="(diagnostic) no per-kernel CUDA events in the timed region")
     p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-img-block", type=int, default=512, help="image rows per streamed block (e2e)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--work-mb", type=int, default=None, help="align workspace (default: library recommendation)")
     p.add_argument("--path", default=None, choices=["auto", "simt", "tc"], help="contraction path override")
@@ -361,6 +362,8 @@ def run_ours(args):
             d_img = torch.empty_like(images)
             d_tmp = torch.empty_like(tmpl)
             h_out = [torch.empty(M, dtype=x, pin_memory=True) for x in (torch.float32, torch.int32, torch.int32)]
+            # one untimed pass: allocator growth for the per-block buffers, first-touch of the pinned pages
+            pdist.align_from_host(h_img, h_tmp, T, t0, w_dev, H, d_img, d_tmp, work=work, img_block=args.e2e_img_block)
             torch.cuda.synchronize()
             barrier(world)
             e0 = torch.cuda.Event(enable_timing=True)
@@ -368,7 +371,8 @@ def run_ours(args):
             e0.record(stream)
             for _ in range(args.e2e_steps):
                 # public streamed path: copies of template / image blocks overlap partials, compress, align
-                (kk, val, tt, k), _ = pdist.align_from_host(h_img, h_tmp, T, t0, w_dev, H, d_img, d_tmp, work=work)
+                (kk, val, tt, k), _ = pdist.align_from_host(h_img, h_tmp, T, t0, w_dev, H, d_img, d_tmp, work=work,
+                                                            img_block=args.e2e_img_block)
                 for h, d in zip(h_out, (val, tt, k)):
                     h.copy_(d, non_blocking=True)
             e1.record(stream)
