@@ -42,7 +42,7 @@
 namespace rsvd {
 
 constexpr int TC_THREADS = 6 * 32;
-constexpr int TC_STAGES = 6;
+constexpr int TC_STAGES = 7;
 constexpr int TC_PIMG = 128;                        // images per CTA pair (64 per CTA)
 constexpr int TC_TT = 256;                          // templates per CTA pair (128 per CTA)
 constexpr uint32_t TC_OPND_BYTES = 128u * 128u;     // 128 rows x (32 hi + 32 lo) fp16
