@@ -147,6 +147,51 @@ __device__ __forceinline__ void dif_reg(float2 (&v)[E]) {
     if constexpr (E > 1) DifStage<E, E / 2>::run(v);
 }
 
+// In-register radix-4 DIF DFT of length E in {4, 8, 16} (fewer nontrivial twiddles than radix-2 for
+// E = 16): stage 1 = 4-point DFTs over v[i + E/4 l] times W_E^{i m}, stored at i + (E/4) m; stage 2 =
+// 4- (E = 16) or 2-point (E = 8) DFTs over i.  Output order: v[dpos4<E>(k)] = X[k].
+template <int E>
+__host__ __device__ constexpr int dpos4(int k) {
+    return E == 16 ? 4 * (k & 3) + (k >> 2) : (E == 8 ? 2 * (k & 3) + (k >> 2) : k);
+}
+__device__ __forceinline__ void dft4_inplace(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
+    const float2 a = c_add(x0, x2), b = c_sub(x0, x2), c = c_add(x1, x3), d = c_sub(x1, x3);
+    const float2 dm = make_float2(d.y, -d.x);                 // -i d
+    x0 = c_add(a, c);
+    x1 = c_add(b, dm);
+    x2 = c_sub(a, c);
+    x3 = c_sub(b, dm);
+}
+template <int E, int I>
+struct Dif4Stage1 {
+    static constexpr int SP = E / 4;
+    static __device__ __forceinline__ void run(float2 (&v)[E]) {
+        float2 x0 = v[I], x1 = v[I + SP], x2 = v[I + 2 * SP], x3 = v[I + 3 * SP];
+        dft4_inplace(x0, x1, x2, x3);
+        v[I] = x0;
+        v[I + SP] = c_mul_w<E, I>(x1);
+        v[I + 2 * SP] = c_mul_w<E, 2 * I>(x2);
+        v[I + 3 * SP] = c_mul_w<E, 3 * I>(x3);
+        if constexpr (I + 1 < SP) Dif4Stage1<E, I + 1>::run(v);
+    }
+};
+template <int E>
+__device__ __forceinline__ void dif4(float2 (&v)[E]) {
+    static_assert(E == 4 || E == 8 || E == 16, "dif4: E in {4, 8, 16}");
+    Dif4Stage1<E, 0>::run(v);
+    if constexpr (E == 16) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) dft4_inplace(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]);
+    } else if constexpr (E == 8) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const float2 a = v[2 * m], b = v[2 * m + 1];
+            v[2 * m] = c_add(a, b);
+            v[2 * m + 1] = c_sub(a, b);
+        }
+    }
+}
+
 // Radix-2 DIF DFT of length L across the lanes of an L-lane group (lanes l ^ h exchange).
 // stw[s] = W_{2h}^{l & (h-1)} for stage s (h = L/2 >> s), computed by lane_stage_twiddles.
 template <int E, int L>

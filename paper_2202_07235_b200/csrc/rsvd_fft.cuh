@@ -79,7 +79,7 @@ struct FftOut {
 // the lanes of a pair hold Re X at k = 2 (k1 + N2 k2) + {0, 1} in wj[brev(k2)] (x, y); the samples at
 // bk -+ 1 (cyclic) are fetched from their owner lanes, gamma = 2 pi (bk + d) / Q with the vertex
 // offset d = (y- - y+) / (2 (y- - 2 y0 + y+)) clamped to [-1/2, 1/2] (0 when not a strict maximum).
-template <int N1, int N2>
+template <int N1, int N2, bool R4 = false>
 __device__ __forceinline__ float parabolic_gamma(const float2 (&wj)[N1], int k1, int bk, float y0, unsigned gmask) {
     constexpr int Qn = 2 * N1 * N2;
     auto fetch = [&](int i) {
@@ -89,7 +89,7 @@ __device__ __forceinline__ float parabolic_gamma(const float2 (&wj)[N1], int k1,
 #pragma unroll
             for (int k2 = 0; k2 < N1; ++k2)
                 if (k2 == kk2) {
-                    const float2 z = wj[brev(k2, clog2(N1))];
+                    const float2 z = wj[R4 ? dpos4<N1>(k2) : brev(k2, clog2(N1))];
                     v = (i & 1) ? z.y : z.x;
                 }
         }

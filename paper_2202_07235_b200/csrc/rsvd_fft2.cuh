@@ -185,14 +185,14 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
             }
         }
         gbar();                                                // (A) every U read: slot becomes ZY
-        dif_reg<N2>(za);
-        dif_reg<N2>(zb);
+        dif4<N2>(za);
+        dif4<N2>(zb);
         {
             float2 *ywa = ZY + lane * SZ + ca, *ywb = ZY + lane * SZ + cb;
             const float2 *twa = Wn + ca * N2, *twb = Wn + cb * N2;
 #pragma unroll
             for (int k1 = 0; k1 < N2; ++k1) {
-                float2 xa = za[brev(k1, clog2(N2))], xb = zb[brev(k1, clog2(N2))];
+                float2 xa = za[dpos4<N2>(k1)], xb = zb[dpos4<N2>(k1)];
                 if (k1) {
                     xa = c_mul(xa, twa[k1]);
                     xb = c_mul(xb, twb[k1]);
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
         for (int j = 0; j < C::P2_PER; ++j) {
             const int task = gt + GT * j;
             const int p = task / N2, k1 = task % N2;
-            dif_reg<N1>(w[j]);                                 // w[brev(k2)] = z[k1 + N2 k2]
+            dif4<N1>(w[j]);                                    // w[dpos4(k2)] = z[k1 + N2 k2]
             const int64_t ml = mb0 + p;
             const bool valid = ml < mcv;
             const int64_t m = m0 + ml;
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
                     float2 *dst = reinterpret_cast<float2 *>(out.X + m * out.ld_m + t * out.ld_t);
 #pragma unroll
                     for (int k2 = 0; k2 < N1; ++k2) {
-                        const float2 z = w[j][brev(k2, clog2(N1))];
+                        const float2 z = w[j][dpos4<N1>(k2)];
                         dst[k1 + N2 * k2] = make_float2(mul * z.x, mul * z.y);
                     }
                 }
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
                     int bk = 0x7fffffff;
 #pragma unroll
                     for (int k2 = N1 - 1; k2 >= 0; --k2) {     // descending: the smallest index wins
-                        const float2 z = w[j][brev(k2, clog2(N1))];
+                        const float2 z = w[j][dpos4<N1>(k2)];
                         const int kx = 2 * (k1 + N2 * k2);
                         if (z.y == mx) bk = kx + 1;
                         if (z.x == mx) bk = kx;
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
                     for (int off = N2 / 2; off >= 1; off >>= 1) bk = min(bk, __shfl_xor_sync(gmask, bk, off));
                     float gam = 0.f;
                     if constexpr (MODE == MODE_PAIR) {
-                        if (out.best_gamma) gam = parabolic_gamma<N1, N2>(w[j], k1, bk, mx, gmask);
+                        if (out.best_gamma) gam = parabolic_gamma<N1, N2, true>(w[j], k1, bk, mx, gmask);
                     }
                     if (k1 == 0) {
                         if constexpr (MODE == MODE_PAIR) {
