@@ -17,7 +17,7 @@
 
 namespace rsvd {
 
-constexpr int KCHUNK = 32;     // templates per partial (rsvd_kernel_chunk)
+constexpr int KCHUNK = 16;     // templates per partial (rsvd_kernel_chunk)
 constexpr int BT = 64;         // output tile (rows) of C per CTA
 constexpr int JB = 32;         // angular samples per smem slab
 constexpr int NTHR = 256;

@@ -333,6 +333,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
 }
 
 // ------------------------------------------------------------------ TC operand emission (Step 1 tail)
+// Position of coefficient q in a principal ring's row of `at` after the in-place DFT: the lane that
+// produced q = k1 + E b writes E consecutive coefficients, so the k1 slot is XOR-permuted by b
+// within each group of E (E = Q/32) -- lanes of one store then hit distinct banks.
+__device__ __forceinline__ int at_pos(int q, int E) { return (q & ~(E - 1)) | ((q ^ (q / E)) & (E - 1)); }
+
 // From the coefficients at[h][q] (smem, [H][Q]) of one row: the exact power-of-two row scale s
 // (max |Re|,|Im| of the stored values times s in [2^13, 2^14)), then the hi/lo fp16 operand rows.
 __device__ float row_scale(const float2 *at, int count, float *red) {
@@ -362,6 +367,7 @@ __device__ __forceinline__ void split_h(float x, __half &hi, __half &lo) {
 __device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, int64_t row, int64_t op_rows,
                              float s, __half *__restrict__ ops) {
     const int N = Q / 2;
+    const int E = Q / 32;
     const int total = (N + 1) * KB * 4;                 // (q, kb, quarter of the 32-element k-block)
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
         const int qu = idx & 3;
@@ -373,10 +379,10 @@ __device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, i
             const int j = kb * 16 + qu * 4 + jj;          // complex index of alpha/beta
             float2 a = make_float2(0.f, 0.f);
             if (j < H) {
-                a = at[j * Q + q];
+                a = at[j * Q + at_pos(q, E)];
                 if (side == RSVD_SIDE_IMAGE) a = c_conj(a);
             } else if (j < 2 * H) {
-                a = at[(j - H) * Q + ((Q - q) & (Q - 1))];
+                a = at[(j - H) * Q + at_pos((Q - q) & (Q - 1), E)];
                 if (side == RSVD_SIDE_TEMPLATE) a = c_conj(a);
             }
             c[jj] = make_float2(a.x * s, a.y * s);
@@ -557,7 +563,7 @@ __global__ void __launch_bounds__(CptCfg<(1 << LOGQ)>::THREADS, 1) compress_tc_k
         __syncwarp();
         const int b = (int)(__brev((unsigned)lane) >> 27);
 #pragma unroll
-        for (int k1 = 0; k1 < E; ++k1) at[h * Q + k1 + E * b] = v[brev(k1, clog2(E))];
+        for (int k1 = 0; k1 < E; ++k1) at[h * Q + at_pos(k1 + E * b, E)] = v[brev(k1, clog2(E))];
     }
     __syncthreads();
     const float s = row_scale(at, H * Q, red);

@@ -1,7 +1,7 @@
 """Multi-GPU plumbing: templates sharded over the ranks of one box (one process per GPU, NCCL over
 NVLink/NVSwitch via torch.distributed).  Data path per step:
 
-  a0  each rank: rsvd_kernel_partials on its template shard (global, fixed 32-template chunks)
+  a0  each rank: rsvd_kernel_partials on its template shard (global, fixed 16-template chunks)
       -> all-gather of the chunk partials (rank order == global chunk order) -> rsvd_kernel_reduce
       -> host eigen-solver.  The fixed chunking makes C and U bitwise identical for any G.
   a1  each rank compresses all images (replicated) and its template shard.
