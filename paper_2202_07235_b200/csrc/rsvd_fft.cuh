@@ -40,7 +40,7 @@ __device__ __forceinline__ uint32_t ord_f32(float v) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-template <int LOGN, int TWR = 0>
+template <int LOGN>
 struct FftCfg {
     static constexpr int N = 1 << LOGN;
     static constexpr int Q = 2 * N;
@@ -52,7 +52,6 @@ struct FftCfg {
     static constexpr int ST_TASKS = NH * C4;          // staging tasks: (row pair, 4 images)
     static constexpr int ST_PER = (ST_TASKS + FR_THREADS - 1) / FR_THREADS;
     static constexpr int P2_PER = TB * N2 / FR_THREADS;
-    static constexpr bool TW_REG = TWR && N2 <= 16;   // pass-1 twiddles in registers, else a table
     static constexpr int SZ = N + 1;                  // ZY row stride (float2): SZ = 1 mod 4
     static constexpr int SWD = N1 >= 16 ? 1 : 16 / N1;
     static constexpr int ROWS = 2 * N;                // plane rows of an item (re then im)
@@ -117,11 +116,11 @@ __device__ __forceinline__ void fr_mbar_wait(uint64_t *b, uint32_t parity) {
         : "memory");
 }
 
-template <int LOGN, int MODE, int TWR>
+template <int LOGN, int MODE>
 __global__ void __launch_bounds__(FR_THREADS, 2) fft_reduce_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                    int64_t Mc, int64_t Tc, int64_t m0, int64_t t0,
                                                                    int64_t mcv, int64_t tcv, FftOut out) {
-    using C = FftCfg<LOGN, TWR>;
+    using C = FftCfg<LOGN>;
     constexpr int N = C::N, Q = C::Q, NH = C::NH, N1 = C::N1, N2 = C::N2, TB = C::TB, C4 = C::C4, SZ = C::SZ;
     constexpr int SP = C::ST_PER;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -168,11 +167,6 @@ __global__ void __launch_bounds__(FR_THREADS, 2) fft_reduce_kernel(const __grid_
     }
     for (int i = tid; i < N2 * N1; i += FR_THREADS) Tw[i] = twiddle_N(i % N1, i / N1, N);
     const int p1 = tid / N1, n1 = tid % N1;
-    float2 tw1[C::TW_REG ? N2 : 1];
-    if constexpr (C::TW_REG) {
-#pragma unroll
-        for (int k1 = 0; k1 < N2; ++k1) tw1[k1] = twiddle_N(n1, k1, N);
-    }
     __syncthreads();
 
     const float PI = 3.14159265358979323846f;
@@ -243,7 +237,7 @@ __global__ void __launch_bounds__(FR_THREADS, 2) fft_reduce_kernel(const __grid_
 #pragma unroll
             for (int k1 = 0; k1 < N2; ++k1) {
                 float2 x = v[brev(k1, clog2(N2))];
-                if (k1) x = c_mul(x, C::TW_REG ? tw1[C::TW_REG ? k1 : 0] : Tw[k1 * N1 + n1]);
+                if (k1) x = c_mul(x, Tw[k1 * N1 + n1]);
                 yw[k1 * N1 + (n1 ^ ((k1 / C::SWD) % N1))] = x;
             }
         }
@@ -371,37 +365,31 @@ static cudaError_t make_spectrum_tmap(CUtensorMap *tm, const float *Upk, int64_t
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int LOGN, int MODE, int TWR>
+template <int LOGN, int MODE>
 static cudaError_t launch_fft_mode(cudaStream_t s, const CUtensorMap &tm, int64_t Mc, int64_t Tc, int64_t m0,
                                    int64_t t0, int64_t mcv, int64_t tcv, const FftOut &out) {
-    using C = FftCfg<LOGN, TWR>;
+    using C = FftCfg<LOGN>;
     const size_t smem = C::smem_bytes();
     static int occ = 0;
     if (!occ) {
-        cudaError_t e = cudaFuncSetAttribute(fft_reduce_kernel<LOGN, MODE, TWR>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(fft_reduce_kernel<LOGN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fft_reduce_kernel<LOGN, MODE, TWR>, FR_THREADS, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fft_reduce_kernel<LOGN, MODE>, FR_THREADS, smem);
         if (e != cudaSuccess || occ < 1) occ = 1;
     }
     const int64_t nitems = tcv * ((mcv + C::TB - 1) / C::TB);
     const int64_t grid = std::min<int64_t>(nitems, (int64_t)num_sms() * occ);
-    fft_reduce_kernel<LOGN, MODE, TWR><<<(unsigned)grid, FR_THREADS, smem, s>>>(tm, Mc, Tc, m0, t0, mcv, tcv, out);
+    fft_reduce_kernel<LOGN, MODE><<<(unsigned)grid, FR_THREADS, smem, s>>>(tm, Mc, Tc, m0, t0, mcv, tcv, out);
     return cudaGetLastError();
 }
 
 template <int LOGN>
 static cudaError_t launch_fft(int mode, cudaStream_t s, const CUtensorMap &tm, int64_t Mc, int64_t Tc, int64_t m0,
                               int64_t t0, int64_t mcv, int64_t tcv, const FftOut &out) {
-    static const int twr = [] { const char *e = getenv("RSVD_FFT_TWREG"); return e ? atoi(e) : 0; }();
-    if (twr) {
-        if (mode == MODE_PAIR) return launch_fft_mode<LOGN, MODE_PAIR, 1>(s, tm, Mc, Tc, m0, t0, mcv, tcv, out);
-        if (mode == MODE_IMAGE) return launch_fft_mode<LOGN, MODE_IMAGE, 1>(s, tm, Mc, Tc, m0, t0, mcv, tcv, out);
-        return launch_fft_mode<LOGN, MODE_LANDSCAPE, 1>(s, tm, Mc, Tc, m0, t0, mcv, tcv, out);
-    }
-    if (mode == MODE_PAIR) return launch_fft_mode<LOGN, MODE_PAIR, 0>(s, tm, Mc, Tc, m0, t0, mcv, tcv, out);
-    if (mode == MODE_IMAGE) return launch_fft_mode<LOGN, MODE_IMAGE, 0>(s, tm, Mc, Tc, m0, t0, mcv, tcv, out);
-    return launch_fft_mode<LOGN, MODE_LANDSCAPE, 0>(s, tm, Mc, Tc, m0, t0, mcv, tcv, out);
+    if (mode == MODE_PAIR) return launch_fft_mode<LOGN, MODE_PAIR>(s, tm, Mc, Tc, m0, t0, mcv, tcv, out);
+    if (mode == MODE_IMAGE) return launch_fft_mode<LOGN, MODE_IMAGE>(s, tm, Mc, Tc, m0, t0, mcv, tcv, out);
+    return launch_fft_mode<LOGN, MODE_LANDSCAPE>(s, tm, Mc, Tc, m0, t0, mcv, tcv, out);
 }
 
 }  // namespace rsvd

@@ -4,6 +4,6 @@ TAG=${1:-prep}
 mkdir -p gpurun_out
 ARGS="--M 4096 --T 4096 --reps 1"
 timeout 300 python tools/prof_align.py $ARGS > gpurun_out/${TAG}_plain.log 2>&1 && \
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"kernel_partials|compress" -c 2 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"kernel_partials|compress" -c 3 \
   -o gpurun_out/${TAG} python tools/prof_align.py $ARGS > gpurun_out/${TAG}_ncu.log 2>&1
 echo "exit $?"; tail -2 gpurun_out/${TAG}_ncu.log
