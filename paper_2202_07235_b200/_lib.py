@@ -10,7 +10,7 @@ import threading
 import numpy as np
 import torch
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librsvd.so")
+LIB_PATH = os.environ.get("RSVD_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "librsvd.so")
 STATUS = {0: "RSVD_OK", 1: "RSVD_ERR_ARG", 2: "RSVD_ERR_UNSUPPORTED", 3: "RSVD_ERR_CUDA",
           4: "RSVD_ERR_NUMERIC"}
 SIDE_IMAGE, SIDE_TEMPLATE = 0, 1

@@ -340,11 +340,11 @@ __device__ __forceinline__ int at_pos(int q, int E) { return (q & ~(E - 1)) | ((
 
 // From the coefficients at[h][q] (smem, [H][Q]) of one row: the exact power-of-two row scale s
 // (max |Re|,|Im| of the stored values times s in [2^13, 2^14)), then the hi/lo fp16 operand rows.
-__device__ float row_scale(const float2 *at, int count, float *red) {
-    float mx = 0.f;
-    for (int i = threadIdx.x; i < count; i += blockDim.x) mx = fmaxf(mx, fmaxf(fabsf(at[i].x), fabsf(at[i].y)));
+// block-wide max of one float per thread (exact, order-independent)
+__device__ float block_max(float mx, float *red) {
 #pragma unroll
     for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    __syncthreads();
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -354,7 +354,10 @@ __device__ float row_scale(const float2 *at, int count, float *red) {
         if (threadIdx.x == 0) red[32] = v;
     }
     __syncthreads();
-    const float m = red[32];
+    return red[32];
+}
+// exact power-of-two row scale that maps a bound m on the row's |coefficients| into [2^13, 2^14)
+__device__ __forceinline__ float scale_for(float m) {
     if (!(m > 0.f) || !isfinite(m)) return 1.f;
     return ldexpf(1.f, 13 - ilogbf(m));
 }
@@ -364,25 +367,31 @@ __device__ __forceinline__ void split_h(float x, __half &hi, __half &lo) {
     lo = __float2half_rn(x - __half2float(hi));
 }
 
-__device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, int64_t row, int64_t op_rows,
-                             float s, __half *__restrict__ ops) {
+// Operand rows of this CTA's quarters (4 complex k-slots = 16 B of hi and 16 B of lo): global quarter
+// gq of the row's 4*KB quarters holds alpha/beta slots j = 4 gq .. 4 gq + 3 (j < H: coefficient h = j,
+// H <= j < 2H: mirror h = j - H, j >= 2H: zero padding).  at holds principal rings h0 .. h0 + hg - 1.
+struct QuarterSet { int a0, a1, b0, b1, c0, c1; };        // up to three ranges [x0, x1) of global quarters
+__device__ void emit_tc_rows(const float2 *at, int h0, int H, int Q, int KB, int side, int64_t row,
+                             int64_t op_rows, float s, QuarterSet qs, __half *__restrict__ ops) {
     const int N = Q / 2;
     const int E = Q / 32;
-    const int total = (N + 1) * KB * 4;                 // (q, kb, quarter of the 32-element k-block)
+    const int na = qs.a1 - qs.a0, nb = qs.b1 - qs.b0, nc = qs.c1 - qs.c0, nq = na + nb + nc;
+    const int total = (N + 1) * nq;                       // (q, owned quarter)
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-        const int qu = idx & 3;
-        const int kb = (idx >> 2) % KB;
-        const int q = (idx >> 2) / KB;
+        const int lq = idx % nq;
+        const int q = idx / nq;
+        const int gq = lq < na ? qs.a0 + lq : (lq < na + nb ? qs.b0 + lq - na : qs.c0 + lq - na - nb);
+        const int qu = gq & 3, kb = gq >> 2;
         float2 c[4];
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-            const int j = kb * 16 + qu * 4 + jj;          // complex index of alpha/beta
+            const int j = gq * 4 + jj;                    // complex index of alpha/beta
             float2 a = make_float2(0.f, 0.f);
             if (j < H) {
-                a = at[j * Q + at_pos(q, E)];
+                a = at[(j - h0) * Q + at_pos(q, E)];
                 if (side == RSVD_SIDE_IMAGE) a = c_conj(a);
             } else if (j < 2 * H) {
-                a = at[(j - H) * Q + at_pos((Q - q) & (Q - 1), E)];
+                a = at[(j - H - h0) * Q + at_pos((Q - q) & (Q - 1), E)];
                 if (side == RSVD_SIDE_TEMPLATE) a = c_conj(a);
             }
             c[jj] = make_float2(a.x * s, a.y * s);
@@ -412,35 +421,47 @@ __device__ void emit_tc_rows(const float2 *at, int H, int Q, int KB, int side, i
     }
 }
 
-// Step 1 for the TC layout, one CTA per row: rings -> principal rings (psi-space projection with the
-// fp64 basis rounded to fp32) -> length-Q DFT -> row scale -> fp16 hi/lo operand rows.  The row's R
-// rings stream through shared memory in slabs of whole rings with double-buffered bulk copies
-// (cp.async.bulk + mbarrier), so loads run ahead of the projection FMAs.
-template <int Q>
-struct CptCfg { static constexpr int THREADS = Q >= 512 ? 512 : 256; };
+// Step 1 for the TC layout: rings -> principal rings (psi-space projection with the fp64 basis rounded
+// to fp32) -> length-Q DFT -> row scale -> fp16 hi/lo operand rows.  Normally one CTA per row holds
+// the row's whole [H][Q] coefficient block in shared memory and projects all H rings in one pass over
+// the rings.  When that block does not fit (large H x Q) and 4 | H, the row is split over
+// ceil(H / CPT_HG) CTAs, one per group of CPT_HG principal rings (adjacent in the grid, so the row's
+// rings come from HBM once and from L2 for the other groups).  Every CTA of a row derives the same row
+// scale without communicating, from the bound |coefficient| <= sqrt(2) max|Re, Im a| * max_h
+// sum_r |U'[r][h]|.  The rings stream through shared memory in slabs of whole rings with
+// double-buffered bulk copies (cp.async.bulk + mbarrier), so loads run ahead of the projection FMAs.
+constexpr int CPT_HG = 8;                                  // principal rings per CTA when split
+template <int Q, bool SPLIT>
+struct CptCfg {
+    static constexpr int THREADS = (SPLIT || Q < 512) ? 256 : 512;
+    static constexpr int MIN_BLOCKS = SPLIT ? (Q >= 1024 ? 2 : 3) : (Q <= 256 ? 2 : 1);
+};
 
-template <int LOGQ, int HC>
-__global__ void __launch_bounds__(CptCfg<(1 << LOGQ)>::THREADS, 1) compress_tc_kernel(const float2 *__restrict__ rings, int64_t n, int R,
-                                                                     const double *__restrict__ w,
-                                                                     const double *__restrict__ U, int H, int side,
-                                                                     int KB, int64_t op_rows, int slab_rings,
-                                                                     __half *__restrict__ ops, float *__restrict__ scales,
-                                                                     const double *__restrict__ kr,
-                                                                     const double *__restrict__ shifts, int S) {
+template <int LOGQ, int HC, bool SPLIT>
+__global__ void __launch_bounds__(CptCfg<(1 << LOGQ), SPLIT>::THREADS, CptCfg<(1 << LOGQ), SPLIT>::MIN_BLOCKS)
+compress_tc_kernel(
+    const float2 *__restrict__ rings, int64_t n, int R, const double *__restrict__ w, const double *__restrict__ U,
+    int H, int side, int KB, int64_t op_rows, int slab_rings, int ngroups, __half *__restrict__ ops,
+    float *__restrict__ scales, const double *__restrict__ kr, const double *__restrict__ shifts, int S) {
     constexpr int Q = 1 << LOGQ;
     constexpr int L = 32;
     constexpr int E = Q / L;
-    constexpr int CPT_THREADS = CptCfg<Q>::THREADS;
+    constexpr int CPT_THREADS = CptCfg<Q, SPLIT>::THREADS;
     constexpr int JPT = Q >= CPT_THREADS ? Q / CPT_THREADS : 1;      // angular samples per thread
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int group = (int)(blockIdx.x % ngroups);
+    const int64_t row = blockIdx.x / ngroups;                         // output row = base * S + shift
+    const int gh0 = ngroups > 1 ? group * CPT_HG : 0;                 // this CTA's principal rings
+    const int ghc = ngroups > 1 ? min(CPT_HG, H - gh0) : H;
+    const int hmax = ngroups > 1 ? CPT_HG : H;
     const int slab_f2 = slab_rings * Q;
     float2 *slab = reinterpret_cast<float2 *>(smem_raw);              // [2][slab_rings][Q]
-    float2 *tw = slab + 2 * slab_f2;                                  // [E][L]
-    float2 *at = tw + E * L;                                          // [H][Q]
-    float *up = reinterpret_cast<float *>(at + (size_t)H * Q);        // [R][HC]
+    double *sw = reinterpret_cast<double *>(slab + 2 * slab_f2);     // [R] sqrt(w_r) (R rounded to even)
+    float2 *tw = reinterpret_cast<float2 *>(sw + (R + 1) / 2 * 2);    // [E][L] (16-B aligned: up is read as float4)
+    float2 *at = tw + E * L;                                          // [hmax][Q]
+    float *up = reinterpret_cast<float *>(at + (size_t)hmax * Q);     // [R][HC]
     float *red = up + (size_t)R * HC;                                 // [33]
     uint64_t *bar = reinterpret_cast<uint64_t *>(red + 34);           // [2] (8-byte aligned: 34 floats)
-    const int64_t row = blockIdx.x;                                   // output row = base * S + shift
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float2 *ring = rings + (row / S) * (int64_t)R * Q;
     const int nslab = (R + slab_rings - 1) / slab_rings;
@@ -473,16 +494,28 @@ __global__ void __launch_bounds__(CptCfg<(1 << LOGQ)>::THREADS, 1) compress_tc_k
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = tid; i < E * L; i += CPT_THREADS) tw[i] = twiddle_N(i % L, i / L, Q);
+    for (int r = tid; r < R; r += CPT_THREADS) sw[r] = sqrt(w[r]);
     float2 stw[clog2(L)];
     lane_stage_twiddles<L>(lane, stw);
     const double invQ = 1.0 / (double)Q;
+    __syncthreads();
+    // c = max_h sum_r |U[r][h]| sqrt(w_r) / Q, every h, fixed summation order (identical in every group)
+    float cmax = 0.f;
+    for (int h = warp; h < H; h += CPT_THREADS / 32) {
+        double c = 0.0;
+        for (int r = lane; r < R; r += 32) c += fabs(U[(int64_t)r * H + h]) * sw[r];
+#pragma unroll
+        for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+        cmax = fmaxf(cmax, (float)(c * invQ));
+    }
+    float amax = 0.f;                                                 // max |Re|, |Im| of the row's samples
     int ks = 0;                                                       // slabs consumed so far (all passes)
-    for (int h0 = 0; h0 < H; h0 += HC) {
-        const int hc = min(HC, H - h0);
+    for (int hp = 0; hp < ghc; hp += HC) {
+        const int hc = min(HC, ghc - hp);
         __syncthreads();
         for (int i = tid; i < R * HC; i += CPT_THREADS) {
             const int r = i / HC, hh = i % HC;
-            up[i] = (hh < hc) ? (float)(U[(int64_t)r * H + h0 + hh] * sqrt(w[r]) * invQ) : 0.f;
+            up[i] = (hh < hc) ? (float)(U[(int64_t)r * H + gh0 + hp + hh] * sw[r] * invQ) : 0.f;
         }
         if (tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -512,7 +545,10 @@ __global__ void __launch_bounds__(CptCfg<(1 << LOGQ)>::THREADS, 1) compress_tc_k
                     const float4 *u4 = reinterpret_cast<const float4 *>(up + (r0 + rr) * HC);
                     float2 a[JPT];
 #pragma unroll
-                    for (int jj = 0; jj < JPT; ++jj) a[jj] = sl[rr * Q + tid + CPT_THREADS * jj];
+                    for (int jj = 0; jj < JPT; ++jj) {
+                        a[jj] = sl[rr * Q + tid + CPT_THREADS * jj];
+                        amax = fmaxf(amax, fmaxf(fabsf(a[jj].x), fabsf(a[jj].y)));
+                    }
                     if (shifts) {
                         const float k = (float)kr[r0 + rr];
 #pragma unroll
@@ -550,12 +586,12 @@ __global__ void __launch_bounds__(CptCfg<(1 << LOGQ)>::THREADS, 1) compress_tc_k
             for (int jj = 0; jj < JPT; ++jj)
 #pragma unroll
                 for (int hh = 0; hh < HC; ++hh)
-                    if (hh < hc) at[(h0 + hh) * Q + tid + CPT_THREADS * jj] = acc[jj][hh];
+                    if (hh < hc) at[(hp + hh) * Q + tid + CPT_THREADS * jj] = acc[jj][hh];
         }
     }
     __syncthreads();
     // in-place length-Q forward DFT of each principal ring, natural order
-    for (int h = warp; h < H; h += CPT_THREADS / 32) {
+    for (int h = warp; h < ghc; h += CPT_THREADS / 32) {
         float2 v[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = at[h * Q + lane + L * e];
@@ -565,34 +601,58 @@ __global__ void __launch_bounds__(CptCfg<(1 << LOGQ)>::THREADS, 1) compress_tc_k
 #pragma unroll
         for (int k1 = 0; k1 < E; ++k1) at[h * Q + at_pos(k1 + E * b, E)] = v[brev(k1, clog2(E))];
     }
-    __syncthreads();
-    const float s = row_scale(at, H * Q, red);
-    if (tid == 0) scales[row] = s;
-    emit_tc_rows(at, H, Q, KB, side, row, op_rows, s, ops);
+    // |A_q[h]| <= sum_r |U'[r][h]| sum_j |a[r][j]| <= sqrt(2) amax * Q cmax (U' holds the 1/Q)
+    cmax = block_max(cmax, red);                                      // block_max syncs: at[] complete
+    amax = block_max(amax, red);
+    const float s = scale_for(1.41421356f * (float)Q * amax * cmax * 1.0000002f);
+    if (tid == 0 && group == 0) scales[row] = s;
+    QuarterSet qs;
+    if (ngroups > 1) {                                                // 4 | H: quarters never straddle groups
+        qs = {gh0 / 4, (gh0 + ghc) / 4, (H + gh0) / 4, (H + gh0 + ghc) / 4, group == 0 ? H / 2 : 0,
+              group == 0 ? 4 * KB : 0};
+    } else {
+        qs = {0, 4 * KB, 0, 0, 0, 0};
+    }
+    emit_tc_rows(at, gh0, H, Q, KB, side, row, op_rows, s, qs, ops);
 }
 
-// principal rings per projection pass: the whole H in one pass up to 32 (one read of the rings)
-static int compress_hc(int H) { return H <= 8 ? 8 : (H <= 16 ? 16 : (H <= 24 ? 24 : 32)); }
-static size_t compress_fixed_smem(int Q, int H, int R) {
-    return (size_t)Q * sizeof(float2) + (size_t)H * Q * sizeof(float2) + (size_t)R * compress_hc(H) * sizeof(float) +
-           34 * 4 + 16;
+// principal rings per projection pass (acc[JPT][HC] in registers; more passes re-stream the rings)
+static int compress_hc(int H, bool split) {
+    if (split) return CPT_HG;
+    return H <= 8 ? 8 : (H <= 16 ? 16 : (H <= 24 ? 24 : 32));
 }
-constexpr size_t CPT_SMEM_BUDGET = 200 * 1024;
-// rings per slab: the largest of 32 / 16 / 8 KB slabs (at least one ring) that fits the budget
-static int compress_slab_rings(int Q, int H, int R) {
+static size_t compress_fixed_smem(int Q, int H, int R, bool split) {
+    const int hmax = split ? CPT_HG : H;
+    return (size_t)(R + 1) / 2 * 2 * sizeof(double) + (size_t)Q * sizeof(float2) + (size_t)hmax * Q * sizeof(float2) +
+           (size_t)R * compress_hc(H, split) * sizeof(float) + 34 * 4 + 16;
+}
+// rings per slab: the largest of 32 / 16 / 8 KB slabs (at least one ring) that fits the budget: 200 KB
+// for one CTA per row; a split row targets MIN_BLOCKS CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
+static int slab_rings_for(int Q, int H, int R, bool split) {
     const size_t ring = (size_t)Q * sizeof(float2);
+    const size_t budget = split ? (Q >= 1024 ? 112 : 74) * 1024 : 200 * 1024;
     for (size_t slab : {32768u, 16384u, 8192u}) {
         const size_t sb = std::max(slab, ring);
-        if (compress_fixed_smem(Q, H, R) + 2 * sb <= CPT_SMEM_BUDGET) return (int)std::min<size_t>(sb / ring, (size_t)R);
+        if (compress_fixed_smem(Q, H, R, split) + 2 * sb <= budget) return (int)std::min<size_t>(sb / ring, (size_t)R);
     }
     return 0;
 }
+// CTAs per row: 1 when the row's [H][Q] block fits, else groups of CPT_HG rings (needs 4 | H), else 0
+static int compress_groups(int Q, int H, int R) {
+    if (slab_rings_for(Q, H, R, false) > 0) return 1;
+    if (H % 4 == 0 && slab_rings_for(Q, H, R, true) > 0) return (H + CPT_HG - 1) / CPT_HG;
+    return 0;
+}
+static int compress_slab_rings(int Q, int H, int R) {
+    const int ng = compress_groups(Q, H, R);
+    return ng ? slab_rings_for(Q, H, R, ng > 1) : 0;
+}
 size_t compress_tc_smem(int Q, int H, int R) {
     const int sr = compress_slab_rings(Q, H, R);
-    return compress_fixed_smem(Q, H, R) + 2 * (size_t)std::max(sr, 1) * Q * sizeof(float2);
+    return compress_fixed_smem(Q, H, R, compress_groups(Q, H, R) > 1) + 2 * (size_t)std::max(sr, 1) * Q * sizeof(float2);
 }
 
-// TC layout needs the whole [H][Q] coefficient block of a row in shared memory (R <= 256).
+// TC layout needs a CTA's [hmax][Q] coefficient block in shared memory (R <= 256).
 bool tc_supported(int Q, int H) { return compress_slab_rings(Q, H, 256) > 0; }
 
 static int g_path = -1;
@@ -608,32 +668,35 @@ int resolve_path(int Q, int H) {
 }
 void set_path(int p) { g_path = (p == PATH_SIMT || p == PATH_TC) ? p : PATH_AUTO; }
 
-template <int LOGQ, int HC>
+template <int LOGQ, int HC, bool SPLIT>
 static cudaError_t launch_compress_tc_qh(const float2 *rings, int64_t n, int R, const double *w, const double *U, int H,
                                          int side, void *blocks, const double *kr, const double *shifts, int S,
                                          cudaStream_t s) {
     const int Q = 1 << LOGQ;
     const int sr = compress_slab_rings(Q, H, R);
-    if (sr < 1) return cudaErrorInvalidValue;
+    const int ng = compress_groups(Q, H, R);
+    if (sr < 1 || ng < 1 || n * ng > 0x7fffffffLL) return cudaErrorInvalidValue;
     const size_t smem = compress_tc_smem(Q, H, R);
-    cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel<LOGQ, HC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel<LOGQ, HC, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return e;
     float *scales = const_cast<float *>(tc_scales(blocks, n, Q, H, side));
-    compress_tc_kernel<LOGQ, HC><<<(unsigned)n, CptCfg<(1 << LOGQ)>::THREADS, smem, s>>>(rings, n, R, w, U, H, side, tc_kb(H),
-                                                                        tc_op_rows(n, side), sr,
-                                                                        reinterpret_cast<__half *>(blocks), scales,
-                                                                        kr, shifts, S);
+    compress_tc_kernel<LOGQ, HC, SPLIT><<<(unsigned)(n * ng), CptCfg<Q, SPLIT>::THREADS, smem, s>>>(
+        rings, n, R, w, U, H, side, tc_kb(H), tc_op_rows(n, side), sr, ng, reinterpret_cast<__half *>(blocks), scales,
+        kr, shifts, S);
     return cudaGetLastError();
 }
 template <int LOGQ>
 static cudaError_t launch_compress_tc_q(const float2 *rings, int64_t n, int R, const double *w, const double *U, int H,
                                         int side, void *blocks, const double *kr, const double *shifts, int S,
                                         cudaStream_t s) {
-    switch (compress_hc(H)) {
-        case 8: return launch_compress_tc_qh<LOGQ, 8>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
-        case 16: return launch_compress_tc_qh<LOGQ, 16>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
-        case 24: return launch_compress_tc_qh<LOGQ, 24>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
-        default: return launch_compress_tc_qh<LOGQ, 32>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+    if (compress_groups(1 << LOGQ, H, R) > 1)
+        return launch_compress_tc_qh<LOGQ, CPT_HG, true>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+    switch (compress_hc(H, false)) {
+        case 8: return launch_compress_tc_qh<LOGQ, 8, false>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+        case 16: return launch_compress_tc_qh<LOGQ, 16, false>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+        case 24: return launch_compress_tc_qh<LOGQ, 24, false>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
+        default: return launch_compress_tc_qh<LOGQ, 32, false>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
     }
 }
 

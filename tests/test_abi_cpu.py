@@ -50,7 +50,8 @@ def test_sizes(lib):
         assert api.block_bytes(8192, 512, 24, api.SIDE_TEMPLATE) == 257 * 3 * 2 * 8192 * 64 + 8192 * 4
         assert api.block_bytes(10, 64, 4, api.SIDE_TEMPLATE) == 33 * 1 * 2 * 256 * 64 + 1024
         assert api.block_bytes(10, 64, 4, api.SIDE_IMAGE) == 33 * 1 * 2 * 256 * 64 + 512
-        assert api.path_for(1024, 256) == api.PATH_SIMT        # H x Q block too large for the TC compress
+        assert api.path_for(1024, 255) == api.PATH_SIMT        # H x Q block too large for the TC compress
+        assert api.path_for(1024, 256) == api.PATH_TC          # 4 | H: the row splits into groups of 8 rings
     finally:
         api.set_path(api.PATH_AUTO)
     assert api.path_for(512, 24) == api.PATH_TC

@@ -109,9 +109,9 @@ def test_basis_parity_and_determinism():
 def test_compress_parity():
     d = make_dataset("small", M=40, T=24)
     A, B, w = to_np(d.images), to_np(d.templates), to_np(d.w)
-    H = 8
-    U, _ = api.build_basis(cuda(B), w, H)
-    for rings, side in [(A, api.SIDE_IMAGE), (B, api.SIDE_TEMPLATE)]:
+    for H, rings, side in [(8, A, api.SIDE_IMAGE), (8, B, api.SIDE_TEMPLATE), (12, A, api.SIDE_IMAGE),
+                           (24, B, api.SIDE_TEMPLATE), (20, A, api.SIDE_IMAGE)]:
+        U, _ = api.build_basis(cuda(B), w, H)         # 4 | H > 8: rows split over groups of 8 rings
         blocks = api.compress(cuda(rings), cuda(w, torch.float64), cuda(U, torch.float64), side)
         got = to_np(api.blocks_unpack(blocks, rings.shape[0], d.Q, H, side))       # [n, Q, H]
         coef = ref.fb_coefficients(rings)                                           # [n, R, Q]
@@ -147,6 +147,12 @@ def test_small_full_argmax_sampled_pairs():
     (3, 67, 12, 128, 7),
     (2, 5, 8, 1024, 3),        # maximum Q
     (9, 11, 33, 256, 33),      # K = 2H not a multiple of 16
+    (20, 30, 24, 512, 12),     # zero-padded k-block
+    (17, 40, 40, 256, 20),
+    (5, 9, 36, 1024, 32),      # H x Q block too large for one CTA: row split over 4 groups of 8 rings
+    (4, 7, 64, 1024, 28),      # split, last group of 4, zero-padded k-block
+    (6, 10, 64, 512, 52),      # split at Q = 512 (7 groups)
+    (3, 300, 24, 64, 16),
 ])
 def test_edge_shapes_random_rings(M, T, R, Q, H):
     rng = np.random.default_rng(M * 1000 + T)
