@@ -55,7 +55,8 @@ typedef enum { RSVD_PER_PAIR = 0, RSVD_PER_IMAGE = 1 } rsvd_reduce;
 
 /* Thread-local message describing the last non-OK status returned on this thread. */
 const char *rsvd_last_error(void);
-/* ABI version of this header (bumped when a signature or the block layout changes): 4. */
+/* ABI version of this header (bumped when a signature or the block layout changes): 5 (5 adds the
+ * f4 volume entry points of rsvd_vol.h). */
 int32_t rsvd_abi_version(void);
 
 /* ------------------------------------------------------------------ sizes */

@@ -47,6 +47,13 @@ SIGNATURES = [
     ("rsvd_launch_count", _I64, []),
     ("rsvd_timing_enable", None, [_I32]),
     ("rsvd_timing_read", _I32, [_P, _P, _I32]),
+    # row f4 (include/rsvd_vol.h)
+    ("rsvd_vol_ncoef", _I64, [_I32]),
+    ("rsvd_vol_kernels", _I32, [_P, _I64, _I32, _I32, _P, _P, _P, _P]),
+    ("rsvd_vol_compress", _I32, [_P, _I64, _I32, _I32, _P, _P, _I32, _P, _P]),
+    ("rsvd_vol_wigner_table", _I32, [_P, _I32, _I32, _P, _I32, _P, _P]),
+    ("rsvd_vol_degrees", _I32, [_P, _I64, _P, _I32, _I32, _P, _I32, _P, _P]),
+    ("rsvd_vol_align", _I32, [_P, _I64, _P, _I32, _I32, _I32, _I32, _P, _P, _P]),
 ]
 
 

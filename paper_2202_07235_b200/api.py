@@ -20,7 +20,8 @@ __all__ = ["block_bytes", "path_for", "set_path", "PATH_AUTO", "PATH_SIMT", "PAT
            "build_basis_translated", "compress", "compress_translated", "blocks_unpack", "align_argmax", "align_landscape", "align_argmax_fine",
            "align_landscape_fine", "winners_reset",
            "winners_unpack", "combine_winners", "launch_count", "timing_enable", "timing_read", "Aligner", "RsvdError", "PER_PAIR", "PER_IMAGE",
-           "SIDE_IMAGE", "SIDE_TEMPLATE"]
+           "SIDE_IMAGE", "SIDE_TEMPLATE", "vol_ncoef", "vol_grid", "vol_kernels", "vol_bases", "vol_compress",
+           "vol_wigner_table", "vol_degrees", "vol_align", "vol_best", "VolumeAligner"]
 
 
 # ------------------------------------------------------------------ sizes
@@ -354,3 +355,110 @@ class Aligner:
             return self.align_blocks(ib, M, tb, T, Q, PER_PAIR)
         keys = self.align_blocks(ib, M, tb, T, Q, PER_IMAGE)
         return winners_unpack(keys, Q)
+
+
+# ------------------------------------------------------------------ row f4: volumes (include/rsvd_vol.h)
+def vol_ncoef(L: int) -> int:
+    return int(_lib.lib().rsvd_vol_ncoef(L))
+
+
+def vol_grid(L: int) -> int:
+    """Default alpha/gamma grid size P: the smallest power of two >= max(32, 2L + 1) (V1)."""
+    P = 32
+    while P < 2 * L + 1:
+        P *= 2
+    return P
+
+
+def vol_kernels(B: torch.Tensor, w: torch.Tensor, L: int, stream=None):
+    """rsvd_vol_kernels: B complex64 [nB, R, (L+1)^2] -> (C [R, R], D [L+1, L+1]) float64 device tensors."""
+    require_cuda(B, w)
+    nB, R, _ = B.shape
+    C = torch.empty(R, R, dtype=torch.float64, device=B.device)
+    D = torch.empty(L + 1, L + 1, dtype=torch.float64, device=B.device)
+    check(_lib.lib().rsvd_vol_kernels(ptr(B), nB, R, L, ptr(w), ptr(C), ptr(D), stream_handle(stream)))
+    return C, D
+
+
+def vol_bases(B: torch.Tensor, w: torch.Tensor, L: int, HC: int, HD: int, stream=None):
+    """Kernels on the device, eigen-solves in the library's host solver -> (U [R, HC], V [L+1, HD]) fp64 numpy."""
+    C, D = vol_kernels(B, w, L, stream)
+    U, _ = eigen_basis(C.cpu().numpy(), HC)
+    V, _ = eigen_basis(D.cpu().numpy(), HD)
+    return U, V
+
+
+def vol_compress(A: torch.Tensor, w: torch.Tensor, U: torch.Tensor, L: int, out=None, stream=None):
+    """rsvd_vol_compress: A complex64 [n, R, (L+1)^2] -> principal shells complex64 [n, (L+1)^2, HC]."""
+    require_cuda(A, w, U)
+    n, R, _ = A.shape
+    HC = U.shape[1]
+    if out is None:
+        out = torch.empty(n, (L + 1) ** 2, HC, dtype=torch.complex64, device=A.device)
+    check(_lib.lib().rsvd_vol_compress(ptr(A), n, R, L, ptr(w), ptr(U), HC, ptr(out), stream_handle(stream)))
+    return out
+
+
+def vol_wigner_table(beta: torch.Tensor, L: int, V: torch.Tensor, out=None, stream=None):
+    """rsvd_vol_wigner_table: beta float64 [nb], V float64 [L+1, HD] -> T float32 [nb, M, M, HD]."""
+    require_cuda(beta, V)
+    nb, HD, M = beta.numel(), V.shape[1], 2 * L + 1
+    if out is None:
+        out = torch.empty(nb, M, M, HD, dtype=torch.float32, device=V.device)
+    check(_lib.lib().rsvd_vol_wigner_table(ptr(beta), nb, L, ptr(V), HD, ptr(out), stream_handle(stream)))
+    return out
+
+
+def vol_degrees(shells_a: torch.Tensor, shell_b: torch.Tensor, L: int, V: torch.Tensor, out=None, stream=None):
+    """rsvd_vol_degrees (Steps 1 + 1b): -> Y complex64 [n, M, M, HD]."""
+    require_cuda(shells_a, shell_b, V)
+    n, _, HC = shells_a.shape
+    HD, M = V.shape[1], 2 * L + 1
+    if out is None:
+        out = torch.empty(n, M, M, HD, dtype=torch.complex64, device=shells_a.device)
+    check(_lib.lib().rsvd_vol_degrees(ptr(shells_a), n, ptr(shell_b), L, HC, ptr(V), HD, ptr(out), stream_handle(stream)))
+    return out
+
+
+def vol_align(Y: torch.Tensor, T: torch.Tensor, L: int, P: int, landscape: bool = True, keys=None, X=None,
+              stream=None):
+    """rsvd_vol_align (Steps 2 + 3): -> (X float32 [n, nb, P, P] or None, keys int64 [n] or None)."""
+    require_cuda(Y, T)
+    n, HD = Y.shape[0], Y.shape[3]
+    nb = T.shape[0]
+    if landscape and X is None:
+        X = torch.empty(n, nb, P, P, dtype=torch.float32, device=Y.device)
+    check(_lib.lib().rsvd_vol_align(ptr(Y), n, ptr(T), nb, L, HD, P, ptr(X) if landscape else None,
+                                    ptr(keys) if keys is not None else None, stream_handle(stream)))
+    return (X if landscape else None), keys
+
+
+def vol_best(keys: torch.Tensor, P: int, stream=None):
+    """Decode packed per-volume keys -> (value, b, a, g) with rsvd_winners_unpack (Q := P*P)."""
+    val, b, ag = winners_unpack(keys, P * P, stream)
+    return val, b, ag // P, ag % P
+
+
+class VolumeAligner:
+    """Row f4 end to end: bases from the target -> principal shells -> Wigner table ->
+    Steps 1/1b -> Steps 2/3 with the per-volume argmax.  All arithmetic runs in librsvd's kernels."""
+
+    def __init__(self, target: torch.Tensor, w: torch.Tensor, L: int, HC: int, HD: int, betas: torch.Tensor,
+                 P: int | None = None, stream=None):
+        self.L, self.P = L, P or vol_grid(L)
+        self.w = w
+        self.stream = stream
+        tgt = target if target.dim() == 3 else target[None]
+        U, V = vol_bases(tgt, w, L, HC, HD, stream)
+        self.U = torch.as_tensor(U, device=w.device)
+        self.V = torch.as_tensor(V, device=w.device)
+        self.shell_b = vol_compress(tgt[:1], w, self.U, L, stream=stream)[0]
+        self.T = vol_wigner_table(betas, L, self.V, stream=stream)
+
+    def align(self, volumes: torch.Tensor, landscape: bool = False):
+        """-> (X or None, (value, b, a, g)) for every volume."""
+        sa = vol_compress(volumes, self.w, self.U, self.L, stream=self.stream)
+        Y = vol_degrees(sa, self.shell_b, self.L, self.V, stream=self.stream)
+        keys = torch.zeros(volumes.shape[0], dtype=torch.int64, device=volumes.device)
+        X, keys = vol_align(Y, self.T, self.L, self.P, landscape=landscape, keys=keys, stream=self.stream)
+        return X, vol_best(keys, self.P, self.stream)

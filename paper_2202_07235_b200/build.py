@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "librsvd.so")
-SOURCES = ["rsvd_api.cpp", "rsvd_eigen.cpp", "rsvd_basis.cu", "rsvd_compress.cu", "rsvd_align.cu", "rsvd_tc.cu"]
+SOURCES = ["rsvd_api.cpp", "rsvd_eigen.cpp", "rsvd_basis.cu", "rsvd_compress.cu", "rsvd_align.cu", "rsvd_tc.cu", "rsvd_vol.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -22,8 +22,9 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "rsvd.h"),
-                                                                os.path.abspath(__file__)]
+    inc = os.path.join(ROOT, "include")
+    deps = ([os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(inc, f) for f in os.listdir(inc)]
+            + [os.path.abspath(__file__)])
     return any(os.path.getmtime(d) > t for d in deps)
 
 

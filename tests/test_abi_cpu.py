@@ -19,7 +19,8 @@ def lib():
 
 
 def _declared():
-    src = open(os.path.join(ROOT, "include", "rsvd.h")).read()
+    inc = os.path.join(ROOT, "include")
+    src = "".join(open(os.path.join(inc, f)).read() for f in sorted(os.listdir(inc)) if f.endswith(".h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(rsvd_[a-z_0-9]+)\s*\(", src)))
 
@@ -58,7 +59,7 @@ def test_sizes(lib):
     assert api.kernel_chunk() == 16
     assert api.kernel_partials_bytes(8192, 128) == 512 * 128 * 128 * 8
     assert api.align_min_workspace_bytes(512) == 128 * 256 * 256 * 8
-    assert lib.rsvd_abi_version() == 4
+    assert lib.rsvd_abi_version() == 5
 
 
 def test_eigen_solver_matches_lapack(lib):
