@@ -8,12 +8,12 @@
  *   w              fp64 [R]: radial quadrature weights for k^2 dk.
  *   U              fp64 [R][HC] radial principal vectors, V fp64 [L+1][HD] degree principal vectors
  *                  (columns; from rsvd_vol_kernels + rsvd_eigen_basis).
- *   shells         complex64 [n][(L+1)^2][HC]: [u_h^T A]_l^m = sum_r U[r][h] sqrt(w_r) A_l^m(k_r)
+ *   shells         complex64 [n][HC][(L+1)^2]: [u_h^T A]_l^m = sum_r U[r][h] sqrt(w_r) A_l^m(k_r)
  *                  (PAPER.md:921-927 with eta_r = sqrt(w_r)).
- *   Y              complex64 [n][M][M][HD], M = 2L+1: Steps 1 + 1b of Eq. volume_innerproduct_pm
- *                  (PAPER.md:1017-1020), entry (m1 + L, m2 + L).
- *   T              fp32 [nb][M][M][HD]: [v_j^T d]_{m1 m2}(beta_b) = sum_l V[l][j] d^l_{m1 m2}(beta_b)
- *                  (PAPER.md:981-984), entry (m1 + L, m2 + L).
+ *   Y              complex64 [n][HD][M][M], M = 2L+1: Steps 1 + 1b of Eq. volume_innerproduct_pm
+ *                  (PAPER.md:1017-1020), Y_j(m1, m2) at [i][j][m2 + L][m1 + L] (m1 fastest).
+ *   T              fp32 [nb][HD][M][M]: [v_j^T d]_{m1 m2}(beta_b) = sum_l V[l][j] d^l_{m1 m2}(beta_b)
+ *                   at [b][j][m2 + L][m1 + L] (m1 fastest).
  *   X              fp32 [n][nb][P][P]: Re X(tau) at tau = (gamma_g, beta_b, alpha_a),
  *                  alpha_a = 2 pi a / P, gamma_g = 2 pi g / P, element ((i*nb + b)*P + a)*P + g
  *                  (Step 3; the P-point grid is DESIGN.md reading V1).

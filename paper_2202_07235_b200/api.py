@@ -389,33 +389,33 @@ def vol_bases(B: torch.Tensor, w: torch.Tensor, L: int, HC: int, HD: int, stream
 
 
 def vol_compress(A: torch.Tensor, w: torch.Tensor, U: torch.Tensor, L: int, out=None, stream=None):
-    """rsvd_vol_compress: A complex64 [n, R, (L+1)^2] -> principal shells complex64 [n, (L+1)^2, HC]."""
+    """rsvd_vol_compress: A complex64 [n, R, (L+1)^2] -> principal shells complex64 [n, HC, (L+1)^2]."""
     require_cuda(A, w, U)
     n, R, _ = A.shape
     HC = U.shape[1]
     if out is None:
-        out = torch.empty(n, (L + 1) ** 2, HC, dtype=torch.complex64, device=A.device)
+        out = torch.empty(n, HC, (L + 1) ** 2, dtype=torch.complex64, device=A.device)
     check(_lib.lib().rsvd_vol_compress(ptr(A), n, R, L, ptr(w), ptr(U), HC, ptr(out), stream_handle(stream)))
     return out
 
 
 def vol_wigner_table(beta: torch.Tensor, L: int, V: torch.Tensor, out=None, stream=None):
-    """rsvd_vol_wigner_table: beta float64 [nb], V float64 [L+1, HD] -> T float32 [nb, M, M, HD]."""
+    """rsvd_vol_wigner_table: beta float64 [nb], V float64 [L+1, HD] -> T float32 [nb, HD, M (m2), M (m1)]."""
     require_cuda(beta, V)
     nb, HD, M = beta.numel(), V.shape[1], 2 * L + 1
     if out is None:
-        out = torch.empty(nb, M, M, HD, dtype=torch.float32, device=V.device)
+        out = torch.empty(nb, HD, M, M, dtype=torch.float32, device=V.device)
     check(_lib.lib().rsvd_vol_wigner_table(ptr(beta), nb, L, ptr(V), HD, ptr(out), stream_handle(stream)))
     return out
 
 
 def vol_degrees(shells_a: torch.Tensor, shell_b: torch.Tensor, L: int, V: torch.Tensor, out=None, stream=None):
-    """rsvd_vol_degrees (Steps 1 + 1b): -> Y complex64 [n, M, M, HD]."""
+    """rsvd_vol_degrees (Steps 1 + 1b): -> Y complex64 [n, HD, M (m2), M (m1)]."""
     require_cuda(shells_a, shell_b, V)
-    n, _, HC = shells_a.shape
+    n, HC, _ = shells_a.shape
     HD, M = V.shape[1], 2 * L + 1
     if out is None:
-        out = torch.empty(n, M, M, HD, dtype=torch.complex64, device=shells_a.device)
+        out = torch.empty(n, HD, M, M, dtype=torch.complex64, device=shells_a.device)
     check(_lib.lib().rsvd_vol_degrees(ptr(shells_a), n, ptr(shell_b), L, HC, ptr(V), HD, ptr(out), stream_handle(stream)))
     return out
 
@@ -424,7 +424,7 @@ def vol_align(Y: torch.Tensor, T: torch.Tensor, L: int, P: int, landscape: bool 
               stream=None):
     """rsvd_vol_align (Steps 2 + 3): -> (X float32 [n, nb, P, P] or None, keys int64 [n] or None)."""
     require_cuda(Y, T)
-    n, HD = Y.shape[0], Y.shape[3]
+    n, HD = Y.shape[0], Y.shape[1]
     nb = T.shape[0]
     if landscape and X is None:
         X = torch.empty(n, nb, P, P, dtype=torch.float32, device=Y.device)

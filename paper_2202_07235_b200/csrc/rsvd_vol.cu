@@ -8,11 +8,13 @@
 //   vol_wigner_kernel            [v_j^T d]_{m1 m2}(beta) (:981-984); thread per (beta, m1, m2), d^l from the
 //                                closed-form seed at l0 = max(|m1|,|m2|) and the three-term recurrence in l
 //                                (fp64), accumulated against V.
-//   vol_degrees_kernel           Steps 1 + 1b (:1017-1020); CTA per (volume, m1), thread per m2.
-//   vol_align_kernel             Steps 2 + 3 (+ argmax) (:1021-1023); CTA per (volume, beta): F on a
-//                                padded P x (P+1) shared-memory grid, row DFTs of the M nonzero rows and
-//                                column DFTs with the warp-distributed FFT of rsvd_common.cuh, Re, then a
-//                                coalesced landscape store and/or a packed-key max per volume.
+//   vol_degrees_kernel           Steps 1 + 1b (:1017-1020); CTA per (volume, m2), thread per m1.
+//   vol_align_kernel             Steps 2 + 3 (+ argmax) (:1021-1023); CTA per (volume, beta): Step 2 and
+//                                the DFT over m1 per m2 column (warp-distributed FFT of rsvd_common.cuh)
+//                                into a P x M shared tile, then the DFT over m2 per alpha row, Re, landscape
+//                                row stores and/or a packed-key max per volume.
+// Layouts (include/rsvd_vol.h): shells [n][HC][NC], T [nb][HD][M(m2)][M(m1)], Y [n][HD][M(m2)][M(m1)] --
+// the index a warp's lanes walk is always the fastest one.
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -99,7 +101,7 @@ __global__ void vol_compress_kernel(const float2 *__restrict__ A, int64_t n, int
         }
 #pragma unroll
         for (int h = 0; h < VC_HB; ++h)
-            if (h0 + h < HC) shells[idx * HC + h0 + h] = acc[h];
+            if (h0 + h < HC) shells[(v * HC + h0 + h) * NC + j] = acc[h];          // [n][HC][NC]
     }
 }
 
@@ -130,10 +132,11 @@ __global__ void vol_wigner_kernel(const double *__restrict__ beta, int nb, int L
     for (int i = threadIdx.x; i < (L + 1) * HD; i += blockDim.x) vs[i] = V[i];
     __syncthreads();
     const int M = 2 * L + 1;
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;                 // (b, m1, m2)
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;                 // (b, m2, m1)
     if (idx >= (int64_t)nb * M * M) return;
     const int b = (int)(idx / (M * M));
-    const int m1 = (int)((idx / M) % M) - L, m2 = (int)(idx % M) - L;
+    const int e = (int)(idx % (M * M));
+    const int m2 = e / M - L, m1 = e % M - L;
     const double bt = beta[b];
     double sh, ch, sb, cb;
     sincos(0.5 * bt, &sh, &ch);
@@ -159,126 +162,133 @@ __global__ void vol_wigner_kernel(const double *__restrict__ beta, int nb, int L
         dprev = d;
         d = dn;
     }
-    float *out = T + idx * HD;
+    float *out = T + (int64_t)b * HD * M * M + e;                                       // [nb][HD][M(m2)][M(m1)]
 #pragma unroll
     for (int j = 0; j < VOL_HMAX; ++j)
-        if (j < HD) out[j] = (float)acc[j];
+        if (j < HD) out[(int64_t)j * M * M] = (float)acc[j];
 }
 
 // ------------------------------------------------------------------ Steps 1 + 1b
-__global__ void vol_degrees_kernel(const float2 *__restrict__ sA, const float2 *__restrict__ sB, int L, int HC,
-                                   const double *__restrict__ V, int HD, float2 *__restrict__ Y) {
+// CTA per (volume, m2): the target's (l, m2) shells and V staged in shared memory; thread per m1 reads
+// the volume's shells sA[v][h][(l, m1)] (consecutive m1 -> consecutive addresses) and writes
+// Y[v][j][m2][m1] (coalesced).
+template <int HDM>
+__global__ void __launch_bounds__(128) vol_degrees_kernel(const float2 *__restrict__ sA, const float2 *__restrict__ sB,
+                                                          int L, int HC, const double *__restrict__ V, int HD,
+                                                          float2 *__restrict__ Y) {
     extern __shared__ float2 smem_f2[];
     const int M = 2 * L + 1, NC = (L + 1) * (L + 1);
     const int64_t v = blockIdx.y;
-    const int m1 = (int)blockIdx.x - L;
-    float2 *a = smem_f2;                                   // [L+1][HC] conj of the volume's (l, m1) shells
-    float *vv = reinterpret_cast<float *>(a + (L + 1) * HC); // [L+1][HD]
+    const int m2 = (int)blockIdx.x - L;
+    float2 *bs = smem_f2;                                   // [L+1][HC] target shells at (l, m2)
+    float *vv = reinterpret_cast<float *>(bs + (L + 1) * HC); // [L+1][HD]
     for (int i = threadIdx.x; i < (L + 1) * HC; i += blockDim.x) {
         const int l = i / HC, h = i % HC;
-        a[i] = l >= abs(m1) ? sA[(v * NC + l * l + l + m1) * HC + h] : make_float2(0.f, 0.f);
+        bs[i] = l >= abs(m2) ? sB[(int64_t)h * NC + l * l + l + m2] : make_float2(0.f, 0.f);
     }
     for (int i = threadIdx.x; i < (L + 1) * HD; i += blockDim.x) vv[i] = (float)V[i];
     __syncthreads();
-    for (int m2i = threadIdx.x; m2i < M; m2i += blockDim.x) {
-        const int m2 = m2i - L;
-        float2 acc[VOL_HMAX];
+    const float2 *av = sA + v * HC * NC;
+    for (int m1i = threadIdx.x; m1i < M; m1i += blockDim.x) {
+        const int m1 = m1i - L;
+        float2 acc[HDM];
 #pragma unroll
-        for (int j = 0; j < VOL_HMAX; ++j) acc[j] = make_float2(0.f, 0.f);
+        for (int j = 0; j < HDM; ++j) acc[j] = make_float2(0.f, 0.f);
         for (int l = max(abs(m1), abs(m2)); l <= L; ++l) {
-            const float2 *b = sB + (int64_t)(l * l + l + m2) * HC;
-            const float2 *al = a + l * HC;
+            const float2 *a = av + l * l + l + m1;
+            const float2 *bl = bs + l * HC;
             float2 x = make_float2(0.f, 0.f);
             for (int h = 0; h < HC; ++h) {                                               // conj(a) b
-                const float2 p = al[h], q = b[h];
+                const float2 p = a[(int64_t)h * NC], q = bl[h];
                 x.x = fmaf(p.x, q.x, fmaf(p.y, q.y, x.x));
                 x.y = fmaf(p.x, q.y, fmaf(-p.y, q.x, x.y));
             }
 #pragma unroll
-            for (int j = 0; j < VOL_HMAX; ++j)
+            for (int j = 0; j < HDM; ++j)
                 if (j < HD) {
                     const float vj = vv[l * HD + j];
                     acc[j].x = fmaf(vj, x.x, acc[j].x);
                     acc[j].y = fmaf(vj, x.y, acc[j].y);
                 }
         }
-        float2 *out = Y + ((v * M + (m1 + L)) * M + m2i) * HD;
+        float2 *out = Y + (v * HD * M + (m2 + L)) * M + m1i;                            // [n][HD][M(m2)][M(m1)]
 #pragma unroll
-        for (int j = 0; j < VOL_HMAX; ++j)
-            if (j < HD) out[j] = acc[j];
+        for (int j = 0; j < HDM; ++j)
+            if (j < HD) out[(int64_t)j * M * M] = acc[j];
     }
 }
 
 // ------------------------------------------------------------------ Steps 2 + 3 (+ argmax)
+// CTA per (volume, beta), 2 CTAs per SM at P = 128.  Pass 1 (warp per m2 column): Step 2 for the column
+// straight from global memory (lanes over m1, coalesced in the m1-fastest layouts of T and Y), DFT over
+// m1 in registers, store G[a][m2] (P x M tile).  Pass 2 (warp per alpha row a): DFT over m2 (positions
+// m2 mod P, zero outside [-L, L]), Re, landscape row store and packed-key max.
 constexpr int VA_THREADS = 256;
 template <int P>
-__global__ void __launch_bounds__(VA_THREADS) vol_align_kernel(const float2 *__restrict__ Y, const float *__restrict__ T,
-                                                               int nb, int L, int HD, float *__restrict__ X,
-                                                               unsigned long long *__restrict__ best_key) {
+__global__ void __launch_bounds__(VA_THREADS, 2) vol_align_kernel(const float2 *__restrict__ Y, const float *__restrict__ T,
+                                                                  int nb, int L, int HD, float *__restrict__ X,
+                                                                  unsigned long long *__restrict__ best_key) {
     constexpr int E = P / 32;
-    constexpr int SP = P + 1;                              // padded row stride (float2)
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2 *G = reinterpret_cast<float2 *>(smem_raw);      // [P][SP]
-    float2 *tw = G + P * SP;                               // [E][32]
+    float2 *tw = reinterpret_cast<float2 *>(smem_raw);     // [E][32]
+    float2 *G = tw + E * 32;                               // [P][M] (M odd: conflict-free column stores)
     __shared__ unsigned long long red[VA_THREADS / 32];
     const int M = 2 * L + 1;
     const int b = blockIdx.x;
     const int64_t v = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < P * SP; i += VA_THREADS) G[i] = make_float2(0.f, 0.f);
     for (int i = tid; i < E * 32; i += VA_THREADS) tw[i] = twiddle_N(i % 32, i / 32, P);
     float2 stw[5];
     lane_stage_twiddles<32>(lane, stw);
     __syncthreads();
-    // Step 2: F(m1, m2) = sum_j T[b][m1][m2][j] Y[v][m1][m2][j] at grid position (m1 mod P, m2 mod P)
-    const float *Tb = T + (int64_t)b * M * M * HD;
-    const float2 *Yv = Y + v * M * M * HD;
-    for (int e = tid; e < M * M; e += VA_THREADS) {
-        const float *t = Tb + (int64_t)e * HD;
-        const float2 *y = Yv + (int64_t)e * HD;
-        float2 f = make_float2(0.f, 0.f);
-        for (int j = 0; j < HD; ++j) {
-            const float tj = t[j];
-            const float2 yj = y[j];
-            f.x = fmaf(tj, yj.x, f.x);
-            f.y = fmaf(tj, yj.y, f.y);
-        }
-        const int m1 = e / M - L, m2 = e % M - L;
-        G[((m1 + P) & (P - 1)) * SP + ((m2 + P) & (P - 1))] = f;
-    }
-    __syncthreads();
-    // Step 3a: DFT along m2 of the M nonzero rows (the other rows stay 0)
     const int b5 = (int)(__brev((unsigned)lane) >> 27);
-    for (int ri = warp; ri < M; ri += VA_THREADS / 32) {
-        const int row = (ri - L + P) & (P - 1);
-        float2 x[E];
+    const int64_t MM = (int64_t)M * M;
+    const float *Tb = T + (int64_t)b * HD * MM;
+    const float2 *Yv = Y + v * HD * MM;
+    // FFT position n = lane + 32 e <-> order m = n (n <= L) or n - P (n >= P - L), else 0
+    int mi[E];
 #pragma unroll
-        for (int e = 0; e < E; ++e) x[e] = G[row * SP + lane + 32 * e];
-        fft_dist<E, 32>(x, lane, tw, stw);
-        __syncwarp();
-#pragma unroll
-        for (int k1 = 0; k1 < E; ++k1) G[row * SP + k1 + E * b5] = x[brev(k1, clog2(E))];
+    for (int e = 0; e < E; ++e) {
+        const int n = lane + 32 * e;
+        mi[e] = n <= L ? n + L : (n >= P - L ? n - P + L : -1);
     }
-    __syncthreads();
-    // Step 3b: DFT along m1 of every column; Re X(a, g) written back into G[a][g].x
-    for (int g = warp; g < P; g += VA_THREADS / 32) {
+    for (int c = warp; c < M; c += VA_THREADS / 32) {                                   // m2 column c = m2 + L
         float2 x[E];
 #pragma unroll
-        for (int e = 0; e < E; ++e) x[e] = G[(lane + 32 * e) * SP + g];
-        fft_dist<E, 32>(x, lane, tw, stw);
-        __syncwarp();
+        for (int e = 0; e < E; ++e) x[e] = make_float2(0.f, 0.f);
+        const float *tc = Tb + (int64_t)c * M;
+        const float2 *yc = Yv + (int64_t)c * M;
+        for (int j = 0; j < HD; ++j) {                                                   // Step 2
 #pragma unroll
-        for (int k1 = 0; k1 < E; ++k1) G[(k1 + E * b5) * SP + g].x = x[brev(k1, clog2(E))].x;
+            for (int e = 0; e < E; ++e)
+                if (mi[e] >= 0) {
+                    const float t = __ldg(tc + j * MM + mi[e]);
+                    const float2 y = __ldg(yc + j * MM + mi[e]);
+                    x[e].x = fmaf(t, y.x, x[e].x);
+                    x[e].y = fmaf(t, y.y, x[e].y);
+                }
+        }
+        fft_dist<E, 32>(x, lane, tw, stw);                                               // over m1 -> alpha
+#pragma unroll
+        for (int k1 = 0; k1 < E; ++k1) G[(k1 + E * b5) * M + c] = x[brev(k1, clog2(E))];
     }
     __syncthreads();
     unsigned long long best = 0ull;
     float *Xo = X ? X + ((v * nb + b) * (int64_t)P) * P : nullptr;
-    for (int i = tid; i < P * P; i += VA_THREADS) {
-        const float val = G[(i / P) * SP + (i % P)].x;
-        if (Xo) Xo[i] = val;
-        const uint32_t flat = (uint32_t)(b * P * P + i);
-        const unsigned long long key = ((unsigned long long)vol_ord(val) << 32) | (0xFFFFFFFFu - flat);
-        best = key > best ? key : best;
+    for (int r = warp; r < P; r += VA_THREADS / 32) {                                   // alpha row r
+        float2 x[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = mi[e] >= 0 ? G[r * M + mi[e]] : make_float2(0.f, 0.f);
+        fft_dist<E, 32>(x, lane, tw, stw);                                               // over m2 -> gamma
+#pragma unroll
+        for (int k1 = 0; k1 < E; ++k1) {
+            const int g = k1 + E * b5;
+            const float val = x[brev(k1, clog2(E))].x;
+            if (Xo) Xo[r * P + g] = val;
+            const uint32_t flat = (uint32_t)((b * P + r) * P + g);
+            const unsigned long long key = ((unsigned long long)vol_ord(val) << 32) | (0xFFFFFFFFu - flat);
+            best = key > best ? key : best;
+        }
     }
     if (best_key) {
 #pragma unroll
@@ -298,7 +308,7 @@ __global__ void __launch_bounds__(VA_THREADS) vol_align_kernel(const float2 *__r
 template <int P>
 static cudaError_t launch_vol_align(const float2 *Y, int64_t n, const float *T, int nb, int L, int HD, float *X,
                                     unsigned long long *keys, cudaStream_t s) {
-    const size_t smem = ((size_t)P * (P + 1) + (P / 32) * 32) * sizeof(float2);
+    const size_t smem = ((size_t)(P / 32) * 32 + (size_t)P * (2 * L + 1)) * sizeof(float2);
     cudaError_t e = cudaFuncSetAttribute(vol_align_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     vol_align_kernel<P><<<dim3((unsigned)nb, (unsigned)n), VA_THREADS, smem, s>>>(Y, T, nb, L, HD, X, keys);
@@ -367,9 +377,14 @@ extern "C" rsvd_status rsvd_vol_degrees(const void *shellsA, int64_t n, const vo
     if (!shellsA || !shellB || !V || !Y) return fail(RSVD_ERR_ARG, "vol_degrees: NULL pointer");
     const int M = 2 * L + 1;
     const size_t smem = (size_t)(L + 1) * HC * sizeof(float2) + (size_t)(L + 1) * HD * sizeof(float);
-    vol_degrees_kernel<<<dim3((unsigned)M, (unsigned)n), 128, smem, (cudaStream_t)stream>>>(
-        reinterpret_cast<const float2 *>(shellsA), reinterpret_cast<const float2 *>(shellB), L, HC, V, HD,
-        reinterpret_cast<float2 *>(Y));
+    const dim3 grid((unsigned)M, (unsigned)n);
+    auto a = reinterpret_cast<const float2 *>(shellsA);
+    auto b = reinterpret_cast<const float2 *>(shellB);
+    auto y = reinterpret_cast<float2 *>(Y);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (HD <= 8) vol_degrees_kernel<8><<<grid, 128, smem, s>>>(a, b, L, HC, V, HD, y);
+    else if (HD <= 16) vol_degrees_kernel<16><<<grid, 128, smem, s>>>(a, b, L, HC, V, HD, y);
+    else vol_degrees_kernel<32><<<grid, 128, smem, s>>>(a, b, L, HC, V, HD, y);
     count_launches(1);
     return cuda_check(cudaGetLastError(), "vol_degrees launch");
 }

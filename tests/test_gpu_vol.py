@@ -21,12 +21,13 @@ def dev(x, dtype=None):
 
 
 def _ref_table(L, betas, V):
+    """[nb][HD][m2 + L][m1 + L] (the library's layout, include/rsvd_vol.h)."""
     M = 2 * L + 1
-    T = np.zeros((len(betas), M, M, V.shape[1]))
+    T = np.zeros((len(betas), V.shape[1], M, M))
     for ib, b in enumerate(betas):
-        d = ov.wigner_d(L, b)
+        d = ov.wigner_d(L, b)                                              # d[l][m1 + l, m2 + l]
         for l in range(L + 1):
-            T[ib, L - l:L + l + 1, L - l:L + l + 1] += d[l][:, :, None] * V[l][None, None, :]
+            T[ib, :, L - l:L + l + 1, L - l:L + l + 1] += V[l][:, None, None] * d[l].T[None]
     return T
 
 
@@ -53,9 +54,9 @@ def test_wigner_table_matches_oracle(L, HD):
 def test_compress_matches_oracle():
     vs = sv.make_volumes(9, 11, 3, nb=4, atoms=8, K=7.0, seed=12)
     U, _ = ov.vol_basis(ov.vol_kernel_C(vs.target, vs.w), 7)
-    sh = to_np(api.vol_compress(dev(vs.volumes), dev(vs.w), dev(U), vs.L))          # [n, NC, HC]
+    sh = to_np(api.vol_compress(dev(vs.volumes), dev(vs.w), dev(U), vs.L))          # [n, HC, NC]
     for i in range(3):
-        want = ov.vol_shells(vs.volumes[i], vs.w, U).T
+        want = ov.vol_shells(vs.volumes[i], vs.w, U)
         assert np.abs(sh[i] - want).max() <= TOL_FP32 * np.abs(want).max()
 
 
@@ -120,8 +121,8 @@ def test_max_size_sampled():
 
 def test_errors_and_empty():
     L = 10
-    Y = torch.zeros(1, 21, 21, 4, dtype=torch.complex64, device="cuda")
-    T = torch.zeros(2, 21, 21, 4, dtype=torch.float32, device="cuda")
+    Y = torch.zeros(1, 4, 21, 21, dtype=torch.complex64, device="cuda")
+    T = torch.zeros(2, 4, 21, 21, dtype=torch.float32, device="cuda")
     with pytest.raises(api.RsvdError):
         api.vol_align(Y, T, L, 16)                                           # P < 2L+1 / not supported
     with pytest.raises(api.RsvdError):
