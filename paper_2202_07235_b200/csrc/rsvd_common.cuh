@@ -69,10 +69,38 @@ inline int64_t kpad_of(int H) { return round_up(2 * (int64_t)H, KPAD); }
 inline int64_t rows_pad_of(int64_t rows) { return round_up(rows, ROWPAD); }
 
 // ------------------------------------------------------------------ complex helpers
-__host__ __device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__host__ __device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// On the device these are sm_100 packed-fp32 instructions (FADD2 / FMUL2 / FFMA2: two IEEE fp32
+// lanes per instruction, operand swizzles, partial negation and scalar broadcast folded in), so a
+// complex add costs one issue slot and a complex multiply two -- the FFT stages are issue-bound.
+__host__ __device__ __forceinline__ float2 c_add(float2 a, float2 b) {
+#ifdef __CUDA_ARCH__
+    return __fadd2_rn(a, b);
+#else
+    return make_float2(a.x + b.x, a.y + b.y);
+#endif
+}
+__host__ __device__ __forceinline__ float2 c_sub(float2 a, float2 b) {
+#ifdef __CUDA_ARCH__
+    return __fadd2_rn(a, make_float2(-b.x, -b.y));
+#else
+    return make_float2(a.x - b.x, a.y - b.y);
+#endif
+}
 __host__ __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
+#ifdef __CUDA_ARCH__
+    // (a.x b.x - a.y b.y, a.x b.y + a.y b.x) = a.y * (-b.y, b.x) + a.x * b
+    return __ffma2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), b));
+#else
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+#endif
+}
+// c * (s, s): a real scale of a complex value
+__host__ __device__ __forceinline__ float2 c_scale(float2 a, float s) {
+#ifdef __CUDA_ARCH__
+    return __fmul2_rn(a, make_float2(s, s));
+#else
+    return make_float2(a.x * s, a.y * s);
+#endif
 }
 __host__ __device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
 
@@ -156,11 +184,10 @@ __host__ __device__ constexpr int dpos4(int k) {
 }
 __device__ __forceinline__ void dft4_inplace(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
     const float2 a = c_add(x0, x2), b = c_sub(x0, x2), c = c_add(x1, x3), d = c_sub(x1, x3);
-    const float2 dm = make_float2(d.y, -d.x);                 // -i d
     x0 = c_add(a, c);
-    x1 = c_add(b, dm);
+    x1 = c_add(b, make_float2(d.y, -d.x));                   // b - i d
     x2 = c_sub(a, c);
-    x3 = c_sub(b, dm);
+    x3 = c_add(b, make_float2(-d.y, d.x));                   // b + i d
 }
 template <int E, int I>
 struct Dif4Stage1 {

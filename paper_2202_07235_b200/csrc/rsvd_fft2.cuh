@@ -49,11 +49,11 @@ struct Fft2Cfg {
 
 // Z_r and Z_{N-r} from a = U_r, b = U_{N-r} (0 < r < N/2), w = W_Q^r.
 __device__ __forceinline__ void z_pair(float2 a, float2 b, float2 w, float2 &zr, float2 &zm) {
-    const float sx = a.x + b.x, sy = a.y - b.y;            // s = U_r + conj U_{N-r}
-    const float dx = a.x - b.x, dy = a.y + b.y;            // d = U_r - conj U_{N-r}
-    const float px = w.x * dx - w.y * dy, py = w.x * dy + w.y * dx;
-    zr = make_float2(sx - py, sy + px);                    // s + i p
-    zm = make_float2(sx + py, px - sy);                    // conj(s) + i conj(p)
+    const float2 sv = c_add(a, make_float2(b.x, -b.y));     // s = U_r + conj U_{N-r}
+    const float2 dv = c_add(a, make_float2(-b.x, b.y));     // d = U_r - conj U_{N-r}
+    const float2 p = c_mul(dv, w);
+    zr = c_add(sv, make_float2(-p.y, p.x));                // s + i p
+    zm = c_add(make_float2(sv.x, -sv.y), make_float2(p.y, p.x));   // conj(s) + i conj(p)
 }
 
 template <int LOGN, int MODE>
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
 #pragma unroll
                     for (int k2 = 0; k2 < N1; ++k2) {
                         const float2 z = w[j][dpos4<N1>(k2)];
-                        dst[k1 + N2 * k2] = make_float2(mul * z.x, mul * z.y);
+                        dst[k1 + N2 * k2] = c_scale(z, mul);
                     }
                 }
             } else {
