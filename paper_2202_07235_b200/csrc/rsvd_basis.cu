@@ -20,10 +20,12 @@ namespace rsvd {
 constexpr int KCHUNK = 16;     // templates per partial (rsvd_kernel_chunk)
 constexpr int BT = 64;         // output tile (rows) of C per CTA
 constexpr int JB = 32;         // angular samples per smem slab
-constexpr int NTHR = 256;
+constexpr int NTHR = 128;
+constexpr int KA = 8, KBB = 4; // per-thread register tile: rows ty + 8a (a < 8) x columns tx + 16b (b < 4)
 
 // grid: (ntile, ntile, nchunks), only tiles with ti >= tj.  Thread (ty, tx) owns rows
-// r_a = ti*64 + ty + 16a and r'_b = tj*64 + tx + 16b, a, b < 4.  Samples are widened to fp64 once,
+// r_a = ti*64 + ty + 8a (a < 8) and r'_b = tj*64 + tx + 16b (b < 4): 64 DFMA per 12 shared loads (the
+// eight row loads are warp broadcasts), so the fp64 pipe, not shared memory, sets the pace.  Samples are widened to fp64 once,
 // when staged in shared memory, so the inner loop is pure DFMA (products of fp32 values are exact in
 // fp64; accumulation order is fixed).
 // ramp (row f2, may be NULL): [S][R][Q] fp64 complex factors exp(-i k_r (dx_s cos psi_j + dy_s sin psi_j));
@@ -36,17 +38,17 @@ __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__r
     const int ti = blockIdx.x, tj = blockIdx.y;
     if (ti < tj) return;
     const int64_t c = blockIdx.z;
-    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;     // ty < 8, tx < 16
     extern __shared__ __align__(16) double2 kp_smem[];
     double2 (*xi)[JB + 1] = reinterpret_cast<double2 (*)[JB + 1]>(kp_smem);
     double2 (*xj)[JB + 1] = reinterpret_cast<double2 (*)[JB + 1]>(kp_smem + BT * (JB + 1));
     __shared__ double si[BT][2], sj[BT][2];       // per-template row sums (re, im)
 
-    double acc[4][4];
+    double acc[KA][KBB];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < KA; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (int b = 0; b < KBB; ++b) acc[a][b] = 0.0;
 
     const int64_t t_begin = c * KCHUNK;
     const int64_t t_end = min(T, t_begin + KCHUNK);
@@ -89,35 +91,35 @@ __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__r
             // Gram: Re(x_r conj(x_r')) = xr xr' + xi xi'
 #pragma unroll 4
             for (int jj = 0; jj < JB; ++jj) {
-                double2 av[4], bv[4];
+                double2 av[KA], bv[KBB];
 #pragma unroll
-                for (int a = 0; a < 4; ++a) av[a] = xi[ty + 16 * a][jj];
+                for (int a = 0; a < KA; ++a) av[a] = xi[ty + 8 * a][jj];
 #pragma unroll
-                for (int b = 0; b < 4; ++b) bv[b] = xj[tx + 16 * b][jj];
+                for (int b = 0; b < KBB; ++b) bv[b] = xj[tx + 16 * b][jj];
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
+                for (int a = 0; a < KA; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a].x, bv[b].x, fma(av[a].y, bv[b].y, acc[a][b]));
+                    for (int b = 0; b < KBB; ++b) acc[a][b] = fma(av[a].x, bv[b].x, fma(av[a].y, bv[b].y, acc[a][b]));
             }
         }
         __syncthreads();
         // remove the angular mean: - (1/Q) Re(S_r conj(S_r'))
         const double invQ = 1.0 / (double)Q;
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < KA; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const double re = si[ty + 16 * a][0] * sj[tx + 16 * b][0] + si[ty + 16 * a][1] * sj[tx + 16 * b][1];
+            for (int b = 0; b < KBB; ++b) {
+                const double re = si[ty + 8 * a][0] * sj[tx + 16 * b][0] + si[ty + 8 * a][1] * sj[tx + 16 * b][1];
                 acc[a][b] -= re * invQ;
             }
         __syncthreads();           // every thread has read si/sj before the next template zeroes them
     }
     double *out = partials + c * (int64_t)R * R;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < KA; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int r1 = ti * BT + ty + 16 * a, r2 = tj * BT + tx + 16 * b;
+        for (int b = 0; b < KBB; ++b) {
+            const int r1 = ti * BT + ty + 8 * a, r2 = tj * BT + tx + 16 * b;
             if (r1 < R && r2 < R) out[(int64_t)r1 * R + r2] = acc[a][b];
         }
 }

@@ -81,10 +81,10 @@ __global__ void __launch_bounds__(CP_THREADS) compress_kernel(const float2 *__re
 #pragma unroll
                 for (int g = 0; g < CP_HC / 4; ++g) {
                     const float4 u = u4[g];
-                    acc[4 * g + 0].x = fmaf(u.x, a.x, acc[4 * g + 0].x); acc[4 * g + 0].y = fmaf(u.x, a.y, acc[4 * g + 0].y);
-                    acc[4 * g + 1].x = fmaf(u.y, a.x, acc[4 * g + 1].x); acc[4 * g + 1].y = fmaf(u.y, a.y, acc[4 * g + 1].y);
-                    acc[4 * g + 2].x = fmaf(u.z, a.x, acc[4 * g + 2].x); acc[4 * g + 2].y = fmaf(u.z, a.y, acc[4 * g + 2].y);
-                    acc[4 * g + 3].x = fmaf(u.w, a.x, acc[4 * g + 3].x); acc[4 * g + 3].y = fmaf(u.w, a.y, acc[4 * g + 3].y);
+                    acc[4 * g + 0] = __ffma2_rn(a, make_float2(u.x, u.x), acc[4 * g + 0]);
+                    acc[4 * g + 1] = __ffma2_rn(a, make_float2(u.y, u.y), acc[4 * g + 1]);
+                    acc[4 * g + 2] = __ffma2_rn(a, make_float2(u.z, u.z), acc[4 * g + 2]);
+                    acc[4 * g + 3] = __ffma2_rn(a, make_float2(u.w, u.w), acc[4 * g + 3]);
                 }
             }
 #pragma unroll

@@ -563,14 +563,10 @@ compress_tc_kernel(
                         const float4 u = u4[g];
 #pragma unroll
                         for (int jj = 0; jj < JPT; ++jj) {
-                            acc[jj][4 * g + 0].x = fmaf(u.x, a[jj].x, acc[jj][4 * g + 0].x);
-                            acc[jj][4 * g + 0].y = fmaf(u.x, a[jj].y, acc[jj][4 * g + 0].y);
-                            acc[jj][4 * g + 1].x = fmaf(u.y, a[jj].x, acc[jj][4 * g + 1].x);
-                            acc[jj][4 * g + 1].y = fmaf(u.y, a[jj].y, acc[jj][4 * g + 1].y);
-                            acc[jj][4 * g + 2].x = fmaf(u.z, a[jj].x, acc[jj][4 * g + 2].x);
-                            acc[jj][4 * g + 2].y = fmaf(u.z, a[jj].y, acc[jj][4 * g + 2].y);
-                            acc[jj][4 * g + 3].x = fmaf(u.w, a[jj].x, acc[jj][4 * g + 3].x);
-                            acc[jj][4 * g + 3].y = fmaf(u.w, a[jj].y, acc[jj][4 * g + 3].y);
+                            acc[jj][4 * g + 0] = __ffma2_rn(a[jj], make_float2(u.x, u.x), acc[jj][4 * g + 0]);
+                            acc[jj][4 * g + 1] = __ffma2_rn(a[jj], make_float2(u.y, u.y), acc[jj][4 * g + 1]);
+                            acc[jj][4 * g + 2] = __ffma2_rn(a[jj], make_float2(u.z, u.z), acc[jj][4 * g + 2]);
+                            acc[jj][4 * g + 3] = __ffma2_rn(a[jj], make_float2(u.w, u.w), acc[jj][4 * g + 3]);
                         }
                     }
                 }
