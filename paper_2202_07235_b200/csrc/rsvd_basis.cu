@@ -31,6 +31,10 @@ constexpr int KA = 8, KBB = 4; // per-thread register tile: rows ty + 8a (a < 8)
 // ramp (row f2, may be NULL): [S][R][Q] fp64 complex factors exp(-i k_r (dx_s cos psi_j + dy_s sin psi_j));
 // every template then contributes its S translated copies (the discrete translation average of
 // Eq. eq_Image_single_cost_with_translations).
+__device__ __forceinline__ void kp_cp_async16(void *smem, const void *gmem, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
+}
 __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__restrict__ tmpl,
                                                                int64_t T, int R, int Q,
                                                                double *__restrict__ partials,
@@ -52,67 +56,86 @@ __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__r
 
     const int64_t t_begin = c * KCHUNK;
     const int64_t t_end = min(T, t_begin + KCHUNK);
-    for (int64_t ts = t_begin * S; ts < t_end * S; ++ts) {
-        const int64_t t = ts / S;
-        const double2 *rp = ramp ? ramp + (ts % S) * (int64_t)R * Q : nullptr;
+    // slabs k = (translated template ts, samples j0 .. j0 + JB) in order; the raw fp32 samples of slab
+    // k + 1 stream into shared memory (cp.async, zero-filled outside the grid) while slab k is
+    // multiplied, so the global-load latency hides behind the DFMA loop
+    const int nslab_t = (Q + JB - 1) / JB;
+    const int64_t ts0 = t_begin * S, nslab = (t_end * S - ts0) * nslab_t;
+    float2 *rawi = reinterpret_cast<float2 *>(kp_smem + 2 * BT * (JB + 1));      // [BT][JB]
+    float2 *rawj = rawi + BT * JB;
+    auto issue = [&](int64_t k) {
+        const int64_t t = (ts0 + k / nslab_t) / S;
+        const int j0 = (int)(k % nslab_t) * JB;
         const float2 *bt = tmpl + t * (int64_t)R * Q;
-        if (tid < BT) { si[tid][0] = si[tid][1] = 0.0; sj[tid][0] = sj[tid][1] = 0.0; }
-        for (int j0 = 0; j0 < Q; j0 += JB) {
-            __syncthreads();
-            // load 64 rows x JB samples for both row tiles, widened to fp64
-            for (int idx = tid; idx < BT * JB; idx += NTHR) {
-                const int rr = idx / JB, jj = idx % JB;
-                const int r1 = ti * BT + rr, r2 = tj * BT + rr;
-                const int j = j0 + jj;
-                const float2 z = make_float2(0.f, 0.f);
-                const float2 u = (r1 < R && j < Q) ? __ldg(bt + (int64_t)r1 * Q + j) : z;
-                const float2 v = (r2 < R && j < Q) ? __ldg(bt + (int64_t)r2 * Q + j) : z;
-                double2 du = make_double2((double)u.x, (double)u.y), dv = make_double2((double)v.x, (double)v.y);
-                if (rp) {                                  // translated copy: exact fp64 complex product
-                    const double2 a = (r1 < R && j < Q) ? rp[(int64_t)r1 * Q + j] : make_double2(1.0, 0.0);
-                    const double2 b = (r2 < R && j < Q) ? rp[(int64_t)r2 * Q + j] : make_double2(1.0, 0.0);
-                    du = make_double2(du.x * a.x - du.y * a.y, du.x * a.y + du.y * a.x);
-                    dv = make_double2(dv.x * b.x - dv.y * b.y, dv.x * b.y + dv.y * b.x);
-                }
-                xi[rr][jj] = du;
-                xj[rr][jj] = dv;
-            }
-            __syncthreads();
-            // row sums (fp64, fixed order)
-            if (tid < BT) {
-                double sr = 0, sim = 0, tr = 0, tim = 0;
-                for (int jj = 0; jj < JB; ++jj) {
-                    sr += xi[tid][jj].x; sim += xi[tid][jj].y;
-                    tr += xj[tid][jj].x; tim += xj[tid][jj].y;
-                }
-                si[tid][0] += sr; si[tid][1] += sim;
-                sj[tid][0] += tr; sj[tid][1] += tim;
-            }
-            // Gram: Re(x_r conj(x_r')) = xr xr' + xi xi'
-#pragma unroll 4
-            for (int jj = 0; jj < JB; ++jj) {
-                double2 av[KA], bv[KBB];
-#pragma unroll
-                for (int a = 0; a < KA; ++a) av[a] = xi[ty + 8 * a][jj];
-#pragma unroll
-                for (int b = 0; b < KBB; ++b) bv[b] = xj[tx + 16 * b][jj];
-#pragma unroll
-                for (int a = 0; a < KA; ++a)
-#pragma unroll
-                    for (int b = 0; b < KBB; ++b) acc[a][b] = fma(av[a].x, bv[b].x, fma(av[a].y, bv[b].y, acc[a][b]));
-            }
+        for (int idx = tid; idx < BT * JB / 2; idx += NTHR) {    // 16-B chunks of 2 samples
+            const int rr = idx / (JB / 2), j = j0 + 2 * (idx % (JB / 2));
+            const int r1 = ti * BT + rr, r2 = tj * BT + rr;
+            kp_cp_async16(rawi + rr * JB + (j - j0), (r1 < R && j < Q) ? bt + (int64_t)r1 * Q + j : bt, (r1 < R && j < Q));
+            kp_cp_async16(rawj + rr * JB + (j - j0), (r2 < R && j < Q) ? bt + (int64_t)r2 * Q + j : bt, (r2 < R && j < Q));
         }
-        __syncthreads();
-        // remove the angular mean: - (1/Q) Re(S_r conj(S_r'))
-        const double invQ = 1.0 / (double)Q;
-#pragma unroll
-        for (int a = 0; a < KA; ++a)
-#pragma unroll
-            for (int b = 0; b < KBB; ++b) {
-                const double re = si[ty + 8 * a][0] * sj[tx + 16 * b][0] + si[ty + 8 * a][1] * sj[tx + 16 * b][1];
-                acc[a][b] -= re * invQ;
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    if (nslab > 0) issue(0);
+    for (int64_t k = 0; k < nslab; ++k) {
+        const int64_t ts = ts0 + k / nslab_t;
+        const int sl = (int)(k % nslab_t), j0 = sl * JB;
+        const double2 *rp = ramp ? ramp + (ts % S) * (int64_t)R * Q : nullptr;
+        if (sl == 0 && tid < BT) { si[tid][0] = si[tid][1] = 0.0; sj[tid][0] = sj[tid][1] = 0.0; }
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();                                   // slab k landed; slab k - 1 fully consumed
+        // widen to fp64 (products of fp32 values are then exact)
+        for (int idx = tid; idx < BT * JB; idx += NTHR) {
+            const int rr = idx / JB, jj = idx % JB;
+            const float2 u = rawi[idx], v = rawj[idx];
+            double2 du = make_double2((double)u.x, (double)u.y), dv = make_double2((double)v.x, (double)v.y);
+            if (rp) {                                  // translated copy: exact fp64 complex product
+                const int r1 = ti * BT + rr, r2 = tj * BT + rr, j = j0 + jj;
+                const double2 a = (r1 < R && j < Q) ? rp[(int64_t)r1 * Q + j] : make_double2(1.0, 0.0);
+                const double2 b = (r2 < R && j < Q) ? rp[(int64_t)r2 * Q + j] : make_double2(1.0, 0.0);
+                du = make_double2(du.x * a.x - du.y * a.y, du.x * a.y + du.y * a.x);
+                dv = make_double2(dv.x * b.x - dv.y * b.y, dv.x * b.y + dv.y * b.x);
             }
-        __syncthreads();           // every thread has read si/sj before the next template zeroes them
+            xi[rr][jj] = du;
+            xj[rr][jj] = dv;
+        }
+        __syncthreads();                                   // fp64 slab ready, raw buffer free
+        if (k + 1 < nslab) issue(k + 1);
+        // row sums (fp64, fixed order)
+        if (tid < BT) {
+            double sr = 0, sim = 0, tr = 0, tim = 0;
+            for (int jj = 0; jj < JB; ++jj) {
+                sr += xi[tid][jj].x; sim += xi[tid][jj].y;
+                tr += xj[tid][jj].x; tim += xj[tid][jj].y;
+            }
+            si[tid][0] += sr; si[tid][1] += sim;
+            sj[tid][0] += tr; sj[tid][1] += tim;
+        }
+        // Gram: Re(x_r conj(x_r')) = xr xr' + xi xi'
+#pragma unroll 4
+        for (int jj = 0; jj < JB; ++jj) {
+            double2 av[KA], bv[KBB];
+#pragma unroll
+            for (int a = 0; a < KA; ++a) av[a] = xi[ty + 8 * a][jj];
+#pragma unroll
+            for (int b = 0; b < KBB; ++b) bv[b] = xj[tx + 16 * b][jj];
+#pragma unroll
+            for (int a = 0; a < KA; ++a)
+#pragma unroll
+                for (int b = 0; b < KBB; ++b) acc[a][b] = fma(av[a].x, bv[b].x, fma(av[a].y, bv[b].y, acc[a][b]));
+        }
+        if (sl == nslab_t - 1) {
+            __syncthreads();                               // every row sum of this template is complete
+            // remove the angular mean: - (1/Q) Re(S_r conj(S_r'))
+            const double invQ = 1.0 / (double)Q;
+#pragma unroll
+            for (int a = 0; a < KA; ++a)
+#pragma unroll
+                for (int b = 0; b < KBB; ++b) {
+                    const double re = si[ty + 8 * a][0] * sj[tx + 16 * b][0] + si[ty + 8 * a][1] * sj[tx + 16 * b][1];
+                    acc[a][b] -= re * invQ;
+                }
+            __syncthreads();       // every thread has read si/sj before the next template zeroes them
+        }
     }
     double *out = partials + c * (int64_t)R * R;
 #pragma unroll
@@ -123,7 +146,7 @@ __global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__r
             if (r1 < R && r2 < R) out[(int64_t)r1 * R + r2] = acc[a][b];
         }
 }
-constexpr size_t KP_SMEM = 2 * (size_t)BT * (JB + 1) * sizeof(double2);
+constexpr size_t KP_SMEM = 2 * (size_t)BT * (JB + 1) * sizeof(double2) + 2 * (size_t)BT * JB * sizeof(float2);
 
 // C[r][r'] = sqrt(w_r w_r') / (T Q) * sum_c P_c[max(r,r')][min(r,r')] (lower triangle is the
 // computed one; reading it for both halves makes C exactly symmetric).
