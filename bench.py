@@ -339,6 +339,24 @@ def run_ours(args):
             "avg_launch_ms": round(k_ms / max(k_n, 1), 4), "launches": k_n,
             "timing": f"CUDA events around every launch on its stream over a second {timing_steps}-step region",
             "algorithmic_flops_per_pair": fpp, "contraction_path": "tc" if path == api.PATH_TC else "simt"}
+    # The contraction against the L2 it actually saturates: per launch it writes the chunk's spectrum
+    # (pairs x Q/2 slots x 8 B) and reads the fp16 hi/lo operand rows ((Q/2 + 1) x KB x 2 B per pair for
+    # 128 x 256 pair tiles); bound t = writes / BW_w + reads / BW_r with the L2 write / read bandwidths
+    # measured by tools/l2_bw_probe.cu on this pool's B200s (profiles/r01s3_l2_bw_probe.txt).
+    contr_l2 = None
+    if path == api.PATH_TC and c_n > 0 and c_ms > 0:
+        L2_W, L2_R = 7300.0, 15500.0                       # GB/s
+        pairs_launch = n_pairs_timed / c_n
+        kb = (H + 7) // 8
+        w_b = pairs_launch * (Q // 2) * 8
+        r_b = pairs_launch * (Q // 2 + 1) * kb * 2
+        t_launch = c_ms / c_n / 1e3
+        t_min = w_b / (L2_W * 1e9) + r_b / (L2_R * 1e9)
+        contr_l2 = {"bound": "l2", "kernel": "contract_tc_kernel", "achieved": round((w_b + r_b) / t_launch / 1e9, 1),
+                    "peak": round((w_b + r_b) / t_min / 1e9, 1), "unit": "GB/s", "frac": round(t_min / t_launch, 4),
+                    "bytes_per_launch": {"spectrum_write": int(w_b), "operand_read": int(r_b)},
+                    "peak_note": f"time-weighted L2 ceiling: write {L2_W:.0f} / read {L2_R:.0f} GB/s measured by "
+                                 "tools/l2_bw_probe.cu (profiles/r01s3_l2_bw_probe.txt)"}
     pi_c = f16_peak / 3.0 if path == api.PATH_TC else fp32_peak
     t_roof = pairs * (f_contr / pi_c + f_fft / fp32_peak) / 1e12 / world
     ts = max(timing_steps, 1)
@@ -414,7 +432,7 @@ def run_ours(args):
                        "workspace_mb": round(wbytes / 2**20, 1), "parallelism": f"template-sharded x{world} (NCCL all-gather of winners)",
                        "l2": "inputs larger than L2 (rings %.1f GB per step)" % ((images.numel() + T * R * Q) * 8 / 1e9),
                        "seed": 220207235},
-            "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "roofline": roof, "contraction_l2": contr_l2, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches_all, "phases_ms_last_step": {k: round(v, 3) for k, v in phase.items()},
             "gen_seconds": round(gen_s, 1),
         }
