@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--work-mb", type=int, default=None, help="align workspace (default: library recommendation)")
     p.add_argument("--path", default=None, choices=["auto", "simt", "tc"], help="contraction path override")
+    p.add_argument("--shard", default="2d", choices=["2d", "templates"],
+                   help="rank grid: image x template shards (dist.grid_shape) or templates only")
     return p.parse_args()
 
 
@@ -199,22 +201,30 @@ def run_ours(args):
     H = args.H or cfg["H"][0]
     Q, R = cfg["Q"], cfg["R"]
     chunk = api.kernel_chunk()
-    T = cfg["T"]
-    t0, t1 = pdist.shard_range(T, world, rank, chunk)
+    T, M = cfg["T"], cfg["M"] * cfg.get("shifts", 1)
+    # rank grid: GI image shards x GT template shards (dist.grid_shape); --shard templates = 1 x world
+    GI, GT = pdist.grid_shape(world, M, T) if args.shard == "2d" else (1, world)
+    ri, rt = pdist.grid_coords(rank, GI)
+    t0, t1 = pdist.shard_range(T, GT, rt, chunk)
+    b0, b1 = pdist.basis_range(T, world, rank, chunk, GI)
     tg0 = time.perf_counter()
     ds = make_dataset(args.config, device=dev, t_range=(t0, t1))
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - tg0
-    images, tmpl = ds.images, ds.templates
-    M = images.shape[0]
+    assert ds.images.shape[0] == M, (ds.images.shape, M)
+    m0, m1 = pdist.image_range(M, GI, ri)
+    images = ds.images[m0:m1].contiguous() if GI > 1 else ds.images
+    tmpl = ds.templates
+    tmpl_basis = tmpl[b0 - t0:b1 - t0]
+    M_loc = images.shape[0]
     T_loc = tmpl.shape[0]
     w_dev = ds.w.contiguous()
     if args.path:
         api.set_path({"simt": api.PATH_SIMT, "tc": api.PATH_TC, "auto": api.PATH_AUTO}[args.path])
     path = api.path_for(Q, H)
-    ib = torch.empty(api.block_bytes(M, Q, H, api.SIDE_IMAGE) // 4, dtype=torch.float32, device=dev)
+    ib = torch.empty(max(api.block_bytes(M_loc, Q, H, api.SIDE_IMAGE), 16) // 4, dtype=torch.float32, device=dev)
     tb = torch.empty(max(api.block_bytes(T_loc, Q, H, api.SIDE_TEMPLATE), 16) // 4, dtype=torch.float32, device=dev)
-    wbytes = args.work_mb * (1 << 20) if args.work_mb else api.align_workspace_bytes(M, T_loc, Q, H)
+    wbytes = args.work_mb * (1 << 20) if args.work_mb else api.align_workspace_bytes(M_loc, T_loc, Q, H)
     work = torch.empty(wbytes // 4, dtype=torch.float32, device=dev)
     keys = torch.zeros(M, dtype=torch.int64, device=dev)
     U_dev = torch.zeros((R, H), dtype=torch.float64, device=dev)
@@ -229,18 +239,19 @@ def run_ours(args):
     def step(imgs, tmps, record=False):
         if record:
             mark("start")
-        U, lam = pdist.basis_from_shards(tmps, T, w_dev, H)         # a0 (syncs for the host solve)
+        U, lam = pdist.basis_from_shards(tmps[b0 - t0:b1 - t0], T, w_dev, H, GI=GI)   # a0 (syncs for the host solve)
         U_dev.copy_(torch.from_numpy(U), non_blocking=False)
         if record:
             mark("basis")
-        api.compress(imgs, w_dev, U_dev, api.SIDE_IMAGE, out=ib)      # a1
+        if M_loc:
+            api.compress(imgs, w_dev, U_dev, api.SIDE_IMAGE, out=ib)  # a1
         if T_loc:
             api.compress(tmps, w_dev, U_dev, api.SIDE_TEMPLATE, out=tb)
         if record:
             mark("compress")
         api.winners_reset(keys)                                       # a2-a4
-        if T_loc:
-            api.align_argmax(ib, M, tb, T_loc, Q, H, api.PER_IMAGE, work, best_key=keys, t_offset=t0)
+        if T_loc and M_loc:
+            api.align_argmax(ib, M_loc, tb, T_loc, Q, H, api.PER_IMAGE, work, best_key=keys[m0:m1], t_offset=t0)
         if record:
             mark("align")
         out = pdist.combine_keys(keys, Q)                             # all-gather + combine
@@ -303,7 +314,7 @@ def run_ours(args):
     f_contr, f_fft = flops_per_pair(H, Q)
     c_ms, c_n = ktime["contract"]
     f_ms, f_n = ktime["fft_reduce"]
-    n_pairs_timed = max(timing_steps, 1) * M * T_loc
+    n_pairs_timed = max(timing_steps, 1) * M_loc * T_loc
     traffic_all = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -381,7 +392,9 @@ def run_ours(args):
             d_tmp = torch.empty_like(tmpl)
             h_out = [torch.empty(M, dtype=x, pin_memory=True) for x in (torch.float32, torch.int32, torch.int32)]
             # one untimed pass: allocator growth for the per-block buffers, first-touch of the pinned pages
-            pdist.align_from_host(h_img, h_tmp, T, t0, w_dev, H, d_img, d_tmp, work=work, img_block=args.e2e_img_block)
+            e2e_kw = dict(work=work, img_block=args.e2e_img_block, M_total=M, m_offset=m0,
+                          basis_sub=(b0 - t0, b1 - t0), GI=GI)
+            pdist.align_from_host(h_img, h_tmp, T, t0, w_dev, H, d_img, d_tmp, **e2e_kw)
             torch.cuda.synchronize()
             barrier(world)
             e0 = torch.cuda.Event(enable_timing=True)
@@ -389,8 +402,7 @@ def run_ours(args):
             e0.record(stream)
             for _ in range(args.e2e_steps):
                 # public streamed path: copies of template / image blocks overlap partials, compress, align
-                (kk, val, tt, k), _ = pdist.align_from_host(h_img, h_tmp, T, t0, w_dev, H, d_img, d_tmp, work=work,
-                                                            img_block=args.e2e_img_block)
+                (kk, val, tt, k), _ = pdist.align_from_host(h_img, h_tmp, T, t0, w_dev, H, d_img, d_tmp, **e2e_kw)
                 for h, d in zip(h_out, (val, tt, k)):
                     h.copy_(d, non_blocking=True)
             e1.record(stream)
@@ -429,7 +441,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "M": M, "T": T, "R": R, "Q": Q, "H": H, "mode": "per_image",
-                       "workspace_mb": round(wbytes / 2**20, 1), "parallelism": f"template-sharded x{world} (NCCL all-gather of winners)",
+                       "workspace_mb": round(wbytes / 2**20, 1), "parallelism": f"{GI} image x {GT} template shards on {world} GPU(s) (NCCL all-gather of winners)",
                        "l2": "inputs larger than L2 (rings %.1f GB per step)" % ((images.numel() + T * R * Q) * 8 / 1e9),
                        "seed": 220207235},
             "roofline": roof, "contraction_l2": contr_l2, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
