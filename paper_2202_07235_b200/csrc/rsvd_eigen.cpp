@@ -6,7 +6,10 @@
 //
 // Algorithm: Householder reduction to tridiagonal form with accumulated orthogonal factor, then
 // implicit symmetric QR steps with Wilkinson shifts and deflation (the textbook symmetric QR
-// algorithm), all in fp64 with a fixed operation order, so the result is deterministic.  Output:
+// algorithm), all in fp64 with a fixed operation order, so the result is deterministic.  For
+// H <= R/2 the QR steps run without accumulating vectors and the H leading eigenvectors come from
+// inverse iteration on the tridiagonal form (each pair checked by its residual, else the full QR
+// path), which drops the O(R^3) rotation updates and the accumulation of the Householder factor.  Output:
 // eigenvalues descending (stable order), eigenvectors normalised with the sign rule "largest-|.|
 // entry positive" (first such entry on ties).
 #include <cmath>
@@ -24,11 +27,13 @@ rsvd_status fail(rsvd_status st, const std::string &msg);
 
 namespace {
 
-// A (n x n, row-major, symmetric) -> tridiagonal (d, e) with A = Z T Z^T.
-void householder_tridiag(int n, std::vector<double> &A, std::vector<double> &Z,
-                         std::vector<double> &d, std::vector<double> &e) {
-    Z.assign((size_t)n * n, 0.0);
-    for (int i = 0; i < n; ++i) Z[(size_t)i * n + i] = 1.0;
+// A (n x n, row-major, symmetric) -> tridiagonal (d, e) with A = Z T Z^T, Z = H_0 H_1 ... H_{n-3},
+// H_k = I - beta_k v_k v_k^T acting on indices k+1..n-1.  The reflectors are kept in refl (row k:
+// v_k at offsets k+1.., beta_k in betas[k], 0 = identity); accumulate_z forms Z from them.
+void householder_tridiag(int n, std::vector<double> &A, std::vector<double> &d, std::vector<double> &e,
+                         std::vector<double> &refl, std::vector<double> &betas) {
+    refl.assign((size_t)n * n, 0.0);
+    betas.assign(n, 0.0);
     std::vector<double> v(n), p(n), q(n);
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1;                 // length of x = A[k+1..n-1][k]
@@ -65,14 +70,8 @@ void householder_tridiag(int n, std::vector<double> &A, std::vector<double> &Z,
             A[(size_t)(k + 1 + i) * n + k] = 0.0;
             A[(size_t)k * n + (k + 1 + i)] = 0.0;
         }
-        // Z <- Z H on columns k+1..n-1
-        for (int r = 0; r < n; ++r) {
-            double *zr = &Z[(size_t)r * n + (k + 1)];
-            double s = 0.0;
-            for (int j = 0; j < m; ++j) s += zr[j] * v[j];
-            s *= beta;
-            for (int j = 0; j < m; ++j) zr[j] -= s * v[j];
-        }
+        betas[k] = beta;
+        for (int j = 0; j < m; ++j) refl[(size_t)k * n + k + 1 + j] = v[j];
     }
     d.resize(n);
     e.assign(n > 1 ? n - 1 : 0, 0.0);
@@ -80,9 +79,27 @@ void householder_tridiag(int n, std::vector<double> &A, std::vector<double> &Z,
     for (int i = 0; i + 1 < n; ++i) e[i] = A[(size_t)(i + 1) * n + i];
 }
 
+// Z = H_0 H_1 ... H_{n-3} (Z <- Z H_k on columns k+1..n-1, k ascending)
+void accumulate_z(int n, const std::vector<double> &refl, const std::vector<double> &betas, std::vector<double> &Z) {
+    Z.assign((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i) Z[(size_t)i * n + i] = 1.0;
+    for (int k = 0; k + 2 < n; ++k) {
+        if (betas[k] == 0.0) continue;
+        const int m = n - k - 1;
+        const double *vk = &refl[(size_t)k * n + k + 1];
+        for (int r = 0; r < n; ++r) {
+            double *zr = &Z[(size_t)r * n + (k + 1)];
+            double s = 0.0;
+            for (int j = 0; j < m; ++j) s += zr[j] * vk[j];
+            s *= betas[k];
+            for (int j = 0; j < m; ++j) zr[j] -= s * vk[j];
+        }
+    }
+}
+
 // Implicit symmetric QR on the tridiagonal (d, e), accumulating rotations into the columns of Z,
 // held transposed (Zt[col][row]) so that each rotation updates two contiguous vectors.
-bool tridiag_qr(int n, std::vector<double> &d, std::vector<double> &e, std::vector<double> &Zt) {
+bool tridiag_qr(int n, std::vector<double> &d, std::vector<double> &e, std::vector<double> *Zt) {
     if (n <= 1) return true;
     const double eps = 2.220446049250313e-16;
     double anorm = 0.0;
@@ -122,13 +139,104 @@ bool tridiag_qr(int n, std::vector<double> &d, std::vector<double> &e, std::vect
                 bulge = -s * e[k + 1];
                 e[k + 1] = c * e[k + 1];
             }
-            double *__restrict__ zk = &Zt[(size_t)k * n];
-            double *__restrict__ zk1 = &Zt[(size_t)(k + 1) * n];
+            if (!Zt) continue;                   // eigenvalues only
+            double *__restrict__ zk = &(*Zt)[(size_t)k * n];
+            double *__restrict__ zk1 = &(*Zt)[(size_t)(k + 1) * n];
             for (int row = 0; row < n; ++row) {
                 const double a = zk[row], b = zk1[row];
                 zk[row] = c * a - s * b;
                 zk1[row] = s * a + c * b;
             }
+        }
+    }
+    return true;
+}
+
+
+// Top-H eigenvectors of the tridiagonal T = (d, e) by inverse iteration (tridiagonal LU with partial
+// pivoting, fixed start vector, 3 steps) with modified Gram-Schmidt against the vectors already found
+// (which keeps clusters -- e.g. the numerical null space of a low-rank kernel -- orthonormal), then
+// back-transformed with the Householder reflectors.  Every pair is checked a posteriori:
+// ||T y - lambda y|| <= 64 n eps ||T||, else false and the caller runs the QR algorithm with
+// accumulated vectors.
+bool top_vectors_inverse_iteration(int n, const std::vector<double> &d, const std::vector<double> &e,
+                                   const std::vector<double> &lam_sorted, int H, const std::vector<double> &refl,
+                                   const std::vector<double> &betas, std::vector<double> &V /* [H][n] */) {
+    const double eps = 2.220446049250313e-16;
+    double tnorm = 0.0;
+    for (int i = 0; i < n; ++i) tnorm = std::fmax(tnorm, std::fabs(d[i]) + (i < n - 1 ? std::fabs(e[i]) : 0.0) + (i > 0 ? std::fabs(e[i - 1]) : 0.0));
+    std::vector<double> Y((size_t)H * n);
+    std::vector<double> a(n), b(n), c(n), c2(n), x(n);
+    std::vector<char> swp(n);
+    for (int h = 0; h < H; ++h) {
+        const double sigma = lam_sorted[h];
+        // LU of T - sigma I with partial pivoting: rows hold (a_i, b_i, c2_i) = (diag, super, super^2)
+        for (int i = 0; i < n; ++i) { a[i] = d[i] - sigma; b[i] = i + 1 < n ? e[i] : 0.0; c2[i] = 0.0; }
+        for (int i = 0; i + 1 < n; ++i) {
+            const double sub = e[i];
+            if (std::fabs(sub) > std::fabs(a[i])) {          // swap rows i and i+1
+                swp[i] = 1;
+                const double na = sub, nb = a[i + 1], nc = i + 2 < n ? e[i + 1] : 0.0;
+                const double m = a[i] / sub;
+                const double oa1 = b[i], oc = c2[i];
+                a[i] = na; b[i] = nb; c2[i] = nc;
+                c[i] = m;
+                a[i + 1] = oa1 - m * nb;
+                b[i + 1] = oc - m * nc;
+            } else {
+                swp[i] = 0;
+                const double m = a[i] != 0.0 ? sub / a[i] : 0.0;
+                c[i] = m;
+                a[i + 1] -= m * b[i];
+            }
+        }
+        for (int i = 0; i < n; ++i)
+            if (std::fabs(a[i]) < eps * tnorm) a[i] = (a[i] < 0 ? -1.0 : 1.0) * eps * tnorm;
+        for (int i = 0; i < n; ++i) x[i] = 1.0 + 1e-3 * (double)((i * 7 + h * 3) % 11);
+        for (int it = 0; it < 3; ++it) {
+            for (int i = 0; i + 1 < n; ++i) {                 // forward: apply L^{-1} P
+                if (swp[i]) { const double t = x[i]; x[i] = x[i + 1]; x[i + 1] = t; }
+                x[i + 1] -= c[i] * x[i];
+            }
+            for (int i = n - 1; i >= 0; --i) {                // back: U^{-1}
+                double v = x[i];
+                if (i + 1 < n) v -= b[i] * x[i + 1];
+                if (i + 2 < n) v -= c2[i] * x[i + 2];
+                x[i] = v / a[i];
+            }
+            for (int g = 0; g < h; ++g) {                     // modified Gram-Schmidt
+                const double *y = &Y[(size_t)g * n];
+                double dot = 0.0;
+                for (int i = 0; i < n; ++i) dot += y[i] * x[i];
+                for (int i = 0; i < n; ++i) x[i] -= dot * y[i];
+            }
+            double nrm = 0.0;
+            for (int i = 0; i < n; ++i) nrm += x[i] * x[i];
+            nrm = std::sqrt(nrm);
+            if (!(nrm > 0.0) || !std::isfinite(nrm)) return false;
+            for (int i = 0; i < n; ++i) x[i] /= nrm;
+        }
+        double r2 = 0.0;                                      // a-posteriori residual on T
+        for (int i = 0; i < n; ++i) {
+            double t = d[i] * x[i] - sigma * x[i];
+            if (i > 0) t += e[i - 1] * x[i - 1];
+            if (i + 1 < n) t += e[i] * x[i + 1];
+            r2 += t * t;
+        }
+        if (!(std::sqrt(r2) <= 64.0 * n * eps * tnorm)) return false;
+        std::copy(x.begin(), x.end(), Y.begin() + (size_t)h * n);
+    }
+    // back-transform: v_h = Z y_h = H_0 (H_1 (... (H_{n-3} y_h)))
+    V = Y;
+    for (int h = 0; h < H; ++h) {
+        double *v = &V[(size_t)h * n];
+        for (int k = n - 3; k >= 0; --k) {
+            if (betas[k] == 0.0) continue;
+            const double *vk = &refl[(size_t)k * n];
+            double s = 0.0;
+            for (int j = k + 1; j < n; ++j) s += vk[j] * v[j];
+            s *= betas[k];
+            for (int j = k + 1; j < n; ++j) v[j] -= s * vk[j];
         }
     }
     return true;
@@ -149,12 +257,45 @@ extern "C" rsvd_status rsvd_eigen_basis(const double *C, int32_t R, int32_t H, d
             if (!std::isfinite(a)) return fail(RSVD_ERR_NUMERIC, "kernel matrix has non-finite entries");
             A[(size_t)i * n + j] = 0.5 * (a + b);
         }
-    std::vector<double> Z, d, e;
-    householder_tridiag(n, A, Z, d, e);
+    std::vector<double> Z, d, e, refl, betas;
+    const bool fast = 2 * H <= n;
+    householder_tridiag(n, A, d, e, refl, betas);
+    auto emit = [&](const double *vec, int h) {      // normalise + sign rule into column h of U
+        double nrm = 0.0, amax = -1.0;
+        int imax = 0;
+        for (int r = 0; r < n; ++r) {
+            nrm += vec[r] * vec[r];
+            if (std::fabs(vec[r]) > amax) { amax = std::fabs(vec[r]); imax = r; }
+        }
+        nrm = std::sqrt(nrm);
+        const double sgn = (vec[imax] < 0) ? -1.0 : 1.0;
+        for (int r = 0; r < n; ++r) U[(size_t)r * H + h] = sgn * vec[r] / nrm;
+    };
+    if (fast) {
+        // top-H fast path: eigenvalues by QR without vectors (the same d/e arithmetic as below, so
+        // bitwise the same eigenvalues), vectors by inverse iteration when they are well separated
+        std::vector<double> d2 = d, e2 = e;
+        if (!tridiag_qr(n, d2, e2, nullptr)) return fail(RSVD_ERR_NUMERIC, "eigen-solver did not converge");
+        std::vector<double> ls = d2;
+        for (int i = 1; i < n; ++i) {                 // stable descending insertion sort
+            const double v = ls[i];
+            int j = i - 1;
+            while (j >= 0 && ls[j] < v) { ls[j + 1] = ls[j]; --j; }
+            ls[j + 1] = v;
+        }
+        std::vector<double> V;
+        if (top_vectors_inverse_iteration(n, d, e, ls, H, refl, betas, V)) {
+            for (int h = 0; h < H; ++h) emit(&V[(size_t)h * n], h);
+            if (lambda)
+                for (int i = 0; i < n; ++i) lambda[i] = ls[i];
+            return RSVD_OK;
+        }
+    }
+    accumulate_z(n, refl, betas, Z);
     std::vector<double> Zt((size_t)n * n);
     for (int r = 0; r < n; ++r)
         for (int c = 0; c < n; ++c) Zt[(size_t)c * n + r] = Z[(size_t)r * n + c];
-    if (!tridiag_qr(n, d, e, Zt)) return fail(RSVD_ERR_NUMERIC, "eigen-solver did not converge");
+    if (!tridiag_qr(n, d, e, &Zt)) return fail(RSVD_ERR_NUMERIC, "eigen-solver did not converge");
     std::vector<int> order(n);
     std::iota(order.begin(), order.end(), 0);
     // stable descending sort (insertion sort: n <= 256, deterministic)
@@ -164,20 +305,7 @@ extern "C" rsvd_status rsvd_eigen_basis(const double *C, int32_t R, int32_t H, d
         while (j >= 0 && d[order[j]] < d[v]) { order[j + 1] = order[j]; --j; }
         order[j + 1] = v;
     }
-    for (int h = 0; h < H; ++h) {
-        const int col = order[h];
-        double nrm = 0.0;
-        int imax = 0;
-        double amax = -1.0;
-        for (int r = 0; r < n; ++r) {
-            const double z = Zt[(size_t)col * n + r];
-            nrm += z * z;
-            if (std::fabs(z) > amax) { amax = std::fabs(z); imax = r; }
-        }
-        nrm = std::sqrt(nrm);
-        const double sgn = (Zt[(size_t)col * n + imax] < 0) ? -1.0 : 1.0;
-        for (int r = 0; r < n; ++r) U[(size_t)r * H + h] = sgn * Zt[(size_t)col * n + r] / nrm;
-    }
+    for (int h = 0; h < H; ++h) emit(&Zt[(size_t)order[h] * n], h);
     if (lambda)
         for (int i = 0; i < n; ++i) lambda[i] = d[order[i]];
     return RSVD_OK;
