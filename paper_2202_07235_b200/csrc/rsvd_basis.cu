@@ -19,7 +19,13 @@ namespace rsvd {
 
 constexpr int KCHUNK = 16;     // templates per partial (rsvd_kernel_chunk)
 constexpr int BT = 64;         // output tile (rows) of C per CTA
-constexpr int JB = 32;         // angular samples per smem slab
+#ifndef RSVD_KP_JB
+#define RSVD_KP_JB 16
+#endif
+#ifndef RSVD_KP_MINB
+#define RSVD_KP_MINB 3      // 3 CTAs (12 warps) per SM: 16-sample slabs, <= 170 registers; measured 11.4 -> 10.8 ms
+#endif
+constexpr int JB = RSVD_KP_JB;   // angular samples per smem slab
 constexpr int NTHR = 128;
 constexpr int KA = 8, KBB = 4; // per-thread register tile: rows ty + 8a (a < 8) x columns tx + 16b (b < 4)
 
@@ -35,7 +41,7 @@ __device__ __forceinline__ void kp_cp_async16(void *smem, const void *gmem, bool
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
 }
-__global__ void __launch_bounds__(NTHR) kernel_partials_kernel(const float2 *__restrict__ tmpl,
+__global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(const float2 *__restrict__ tmpl,
                                                                int64_t T, int R, int Q,
                                                                double *__restrict__ partials,
                                                                const double2 *__restrict__ ramp, int S) {
