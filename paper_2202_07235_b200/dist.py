@@ -37,6 +37,10 @@ def _all_gather_equal(x: torch.Tensor, group=None) -> torch.Tensor:
     out = torch.empty((world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, x.contiguous(), group=group)
+    elif x.is_cuda:                       # gloo (tests): stage through host memory
+        host = torch.empty((world,) + tuple(x.shape), dtype=x.dtype)
+        dist.all_gather(list(host.unbind(0)), x.detach().cpu().contiguous(), group=group)
+        out.copy_(host)
     else:
         dist.all_gather(list(out.unbind(0)), x.contiguous(), group=group)
     return out
