@@ -55,8 +55,8 @@ typedef enum { RSVD_PER_PAIR = 0, RSVD_PER_IMAGE = 1 } rsvd_reduce;
 
 /* Thread-local message describing the last non-OK status returned on this thread. */
 const char *rsvd_last_error(void);
-/* ABI version of this header (bumped when a signature or the block layout changes): 5 (5 adds the
- * f4 volume entry points of rsvd_vol.h). */
+/* ABI version of this header (bumped when a signature or the block layout changes): 6 (5 adds the
+ * f4 volume entry points of rsvd_vol.h, 6 rsvd_kernel_translated_sh). */
 int32_t rsvd_abi_version(void);
 
 /* ------------------------------------------------------------------ sizes */
@@ -149,15 +149,30 @@ rsvd_status rsvd_blocks_unpack(const void *blocks, int64_t n, int32_t Q, int32_t
 /* rsvd_build_basis_translated: as rsvd_build_basis, for the translation-averaged objective of
  * Eq. eq_Image_single_cost_with_translations with a discrete distribution of S
  * equally weighted shifts: C is averaged over the T x S translated templates (each angularly
- * centred), C = (1/(T S Q)) sqrt(w w') sum_{t,s} Re sum_j W_ts W_ts^H.  The paper's closed form for a
- * Gaussian shift distribution (:1152-1166) needs the molecule's spherical-harmonic coefficients,
- * which a template set does not provide; this is the exact finite-sum kernel.  Host inputs: w, k
+ * centred), C = (1/(T S Q)) sqrt(w w') sum_{t,s} Re sum_j W_ts W_ts^H (the exact finite-sum kernel;
+ * the paper's closed form for a Gaussian shift distribution, :1152-1166, is rsvd_kernel_translated_sh,
+ * which needs the volume's spherical-harmonic coefficients instead of templates).  Host inputs: w, k
  * [R] fp64 (weights, radial wavenumbers), shifts [S][2] fp64 (dx, dy).  The ramps are built in fp64
  * on the device.  Synchronises; allocates scratch (S*R*Q complex fp64 + partials). */
 rsvd_status rsvd_build_basis_translated(const void *templates, int64_t T, int32_t R, int32_t Q,
                                         const double *w_host, const double *k_host,
                                         const double *shifts_host, int32_t S, int32_t H,
                                         double *U_host, double *lambda_host, rsvd_stream_t stream);
+/* rsvd_kernel_translated_sh: the closed-form kernel of Eq. template_cost_with_translations
+ * -- targets = projections of one volume at uniformly distributed views, shifted
+ * by an isotropic Gaussian translation of standard deviation sigma (per axis) -- from the volume's
+ * spherical-harmonic coefficients:
+ *   C[r][r'] = sqrt(w_r w_r') Re[ (sum_{l,m} conj(B_l^m(k_r)) B_l^m(k_r')) E+(k_r, k_r')
+ *                                 - conj(B_0^0(k_r)) B_0^0(k_r') E-(k_r) E-(k_r') ],
+ *   E+ = exp(-sigma^2 (k_r - k_r')^2 / 2) (= the printed product form),
+ *   E- = exp(-k^2 sigma^2 / 2) (= the printed Bessel form, I_{-1/2} - I_{1/2} in closed form),
+ * up to the paper's constant factor (the same C the paper's Rayleigh quotient uses; DESIGN.md reading
+ * T1: the printed mean term keeps l = 0 only, an approximation of the view average).  Feed C to
+ * rsvd_eigen_basis for U.  Bsh: device complex128 [R][(L+1)^2], index l*l + l + m, 16-B aligned;
+ * k, w: device fp64 [R] (radial nodes of the image grid and their weights); C: device fp64 [R][R].
+ * sigma >= 0 (0: no translations).  Asynchronous on `stream`; deterministic (fixed reduction order). */
+rsvd_status rsvd_kernel_translated_sh(const void *Bsh, int32_t R, int32_t L, const double *k, const double *w,
+                                      double sigma, double *C, rsvd_stream_t stream);
 rsvd_status rsvd_compress_translated(const void *rings, int64_t n_base, int32_t R, int32_t Q,
                                      const double *w, const double *k, const double *U, int32_t H,
                                      const double *shifts, int32_t S, rsvd_side side, void *blocks,

@@ -34,6 +34,12 @@ F2 translate           a exp(-i k_r (dx cos psi_j + dy sin psi_j)), the Fourier 
                        kernel of Eq. eq_Image_single_cost_with_translations (:1146-1150) for a discrete
                        shift distribution is kernel_C of the translated templates.
 
+T1 kernel_translated_sh  the closed-form target-averaged kernel with Gaussian translations (sigma_d)
+                       and uniform views, Eq. template_cost_with_translations, from
+                       the target volume's spherical-harmonic coefficients B_l^m(k_r), with E+ and E-
+                       written exactly as printed (E- via the modified Bessel functions I_{-1/2}, I_{1/2});
+                       times sqrt(w_r w_r'), real part (readings G6, T1 in DESIGN.md).
+
 Parity pins for every function live in tests/test_oracle_pins.py.
 """
 from __future__ import annotations
@@ -298,3 +304,40 @@ def backward_fraction(approx, full) -> np.ndarray:
     ke = argmax_first(approx)
     xe = np.take_along_axis(full, ke[..., None], axis=-1)
     return (full <= xe).sum(axis=-1) / full.shape[-1]
+
+
+# ------------------------------------------------------------------------------------ T1
+def E_plus(k, kp, sigma: float) -> np.ndarray:
+    """E+(k_r, k_r') = exp(-sigma^2/2 [k_r^2 + k_r'^2]) exp(k_r k_r' sigma^2), as
+    printed: the outer product over the radial nodes."""
+    k = np.asarray(k, np.float64)[:, None]
+    kp = np.asarray(kp, np.float64)[None, :]
+    return np.exp(-0.5 * sigma ** 2 * (k ** 2 + kp ** 2)) * np.exp(k * kp * sigma ** 2)
+
+
+def E_minus(k, sigma: float) -> np.ndarray:
+    """E-(k_r) = kt sqrt(pi/2) exp(-kt^2) (I_{-1/2}(kt^2) - I_{+1/2}(kt^2)), kt = k sigma / 2
+    (PAPER.md:1164-1166), as printed; E-(k) -> 1 as sigma -> 0 (the limit is taken at kt = 0)."""
+    import scipy.special
+    k = np.asarray(k, np.float64)
+    kt = k * sigma / 2.0
+    out = np.ones_like(kt)
+    nz = kt > 0
+    x = kt[nz] ** 2
+    out[nz] = kt[nz] * np.sqrt(np.pi / 2.0) * np.exp(-x) * (scipy.special.iv(-0.5, x) - scipy.special.iv(0.5, x))
+    return out
+
+
+def kernel_translated_sh(Bsh, k, w, sigma: float) -> np.ndarray:
+    """T1: C_{rr'} = sqrt(w_r w_r') Re[ (sum_{l,m} conj(B_l^m(k_r)) B_l^m(k_r')) E+(k_r, k_r')
+                                          - conj(B_0^0(k_r)) B_0^0(k_r') E-(k_r) E-(k_r') ]
+    Eq. template_cost_with_translations, up to the paper's constant factor.
+    Bsh [R, (L+1)^2] complex (index l*l + l + m), k [R] radial nodes, w [R] radial weights."""
+    B = _c128(Bsh)
+    S = np.einsum("rl,sl->rs", np.conj(B), B)
+    b0 = B[:, 0]
+    Em = E_minus(k, sigma)
+    C = (S * E_plus(k, k, sigma) - np.outer(np.conj(b0), b0) * np.outer(Em, Em)).real
+    sw = np.sqrt(np.asarray(w, np.float64))
+    C = sw[:, None] * C * sw[None, :]
+    return 0.5 * (C + C.T)

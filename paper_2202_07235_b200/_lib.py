@@ -34,6 +34,7 @@ SIGNATURES = [
     ("rsvd_eigen_basis_ctf", _I32, [_P, _I32, _P, _I32, _P, _P, _P]),
     ("rsvd_build_basis", _I32, [_P, _I64, _I32, _I32, _P, _I32, _P, _P, _P]),
     ("rsvd_build_basis_translated", _I32, [_P, _I64, _I32, _I32, _P, _P, _P, _I32, _I32, _P, _P, _P]),
+    ("rsvd_kernel_translated_sh", _I32, [_P, _I32, _I32, _P, _P, ctypes.c_double, _P, _P]),
     ("rsvd_compress", _I32, [_P, _I64, _I32, _I32, _P, _P, _I32, _I32, _P, _P]),
     ("rsvd_blocks_unpack", _I32, [_P, _I64, _I32, _I32, _I32, _P, _P]),
     ("rsvd_compress_translated", _I32, [_P, _I64, _I32, _I32, _P, _P, _P, _I32, _P, _I32, _I32, _P, _P]),

@@ -136,6 +136,21 @@ def build_basis_translated(templates: torch.Tensor, w, k, shifts, H: int, stream
     return U, lam
 
 
+def kernel_translated_sh(Bsh: torch.Tensor, k: torch.Tensor, w: torch.Tensor, sigma: float, stream=None) -> torch.Tensor:
+    """rsvd_kernel_translated_sh: the closed-form translation- and view-averaged kernel (PAPER.md:1156-1166,
+    row f2) from a volume's spherical-harmonic coefficients Bsh [R, (L+1)^2] complex128 (device);
+    k, w: device fp64 [R].  Returns C [R, R] fp64 (device); U from eigen_basis(C)."""
+    require_cuda(Bsh, k, w)
+    R, nlm = Bsh.shape
+    L = int(round(nlm ** 0.5)) - 1
+    if (L + 1) ** 2 != nlm or Bsh.dtype != torch.complex128:
+        raise RsvdError(1, "Bsh must be complex128 [R, (L+1)^2]")
+    C = torch.empty((R, R), dtype=torch.float64, device=Bsh.device)
+    check(_lib.lib().rsvd_kernel_translated_sh(ptr(Bsh.contiguous()), R, L, ptr(k.contiguous()), ptr(w.contiguous()),
+                                               float(sigma), ptr(C), stream_handle(stream)))
+    return C
+
+
 # ------------------------------------------------------------------ row a1
 def compress(rings: torch.Tensor, w: torch.Tensor, U: torch.Tensor, side: int, out=None, stream=None):
     """rsvd_compress -> opaque block buffer (float32 tensor of block_bytes/4 elements)."""

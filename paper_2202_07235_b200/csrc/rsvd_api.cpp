@@ -97,4 +97,4 @@ extern "C" rsvd_status rsvd_timing_read(double *ms, int64_t *count, int32_t nkin
 }
 
 extern "C" const char *rsvd_last_error(void) { return rsvd::g_last_error.c_str(); }
-extern "C" int32_t rsvd_abi_version(void) { return 5; }
+extern "C" int32_t rsvd_abi_version(void) { return 6; }

@@ -182,6 +182,38 @@ __global__ void ramp_kernel(const double *__restrict__ k, const double *__restri
     ramp[idx] = make_double2(pc, ps);
 }
 
+// ------------------------------------------------------------------ row f2: closed-form translation kernel
+// Eq. template_cost_with_translations: from the target volume's spherical-harmonic
+// coefficients B_l^m(k_r), one warp per entry (r, r' <= r), fixed lane-strided order over the
+// (L+1)^2 coefficients and a fixed shuffle tree (deterministic):
+//   C[r][r'] = sqrt(w_r w_r') Re[ S(r, r') E+(k_r, k_r') - conj(B_0^0(k_r)) B_0^0(k_r') E-(k_r) E-(k_r') ],
+//   S(r, r') = sum_{l,m} conj(B_l^m(k_r)) B_l^m(k_r'),
+// with the printed E+ = exp(-s^2 (k^2 + k'^2)/2) exp(k k' s^2) evaluated as exp(-s^2 (k - k')^2 / 2)
+// and the printed Bessel-form E- as its closed form exp(-k^2 s^2 / 2) (I_{-1/2}(x) - I_{1/2}(x) =
+// sqrt(2/(pi x)) e^{-x}; pinned by tests/test_oracle_pins.py::test_T1_E_minus_is_a_gaussian).
+__global__ void kernel_translated_sh_kernel(const double2 *__restrict__ Bsh, int R, int nlm,
+                                            const double *__restrict__ k, const double *__restrict__ w,
+                                            double sigma, double *__restrict__ C) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= (int64_t)R * R) return;
+    const int r = (int)(warp / R), c = (int)(warp % R);
+    if (c > r) return;
+    const double2 *a = Bsh + (int64_t)r * nlm, *b = Bsh + (int64_t)c * nlm;
+    double re = 0.0;
+    for (int i = lane; i < nlm; i += 32) re += a[i].x * b[i].x + a[i].y * b[i].y;      // Re conj(a) b
+    for (int off = 16; off >= 1; off >>= 1) re += __shfl_xor_sync(0xffffffffu, re, off);
+    if (lane == 0) {
+        const double kr = k[r], kc = k[c], s2 = sigma * sigma;
+        const double ep = exp(-0.5 * s2 * (kr - kc) * (kr - kc));
+        const double em = exp(-0.5 * s2 * kr * kr) * exp(-0.5 * s2 * kc * kc);
+        const double b0 = a[0].x * b[0].x + a[0].y * b[0].y;
+        const double v = sqrt(w[r]) * sqrt(w[c]) * (re * ep - b0 * em);
+        C[(int64_t)r * R + c] = v;
+        C[(int64_t)c * R + r] = v;
+    }
+}
+
 }  // namespace rsvd
 
 using namespace rsvd;
@@ -243,6 +275,21 @@ extern "C" rsvd_status rsvd_kernel_reduce(const double *partials, int64_t nchunk
         partials, nchunks, R, scale, w, C);
     count_launches(1);
     return cuda_check(cudaGetLastError(), "kernel_reduce launch");
+}
+
+extern "C" rsvd_status rsvd_kernel_translated_sh(const void *Bsh, int32_t R, int32_t L, const double *k,
+                                                 const double *w, double sigma, double *C, rsvd_stream_t stream) {
+    if (R < 1 || R > 256) return fail(RSVD_ERR_UNSUPPORTED, "R must be in [1, 256]");
+    if (L < 0 || L > 1023) return fail(RSVD_ERR_UNSUPPORTED, "L must be in [0, 1023]");
+    if (!(sigma >= 0.0) || !std::isfinite(sigma)) return fail(RSVD_ERR_ARG, "sigma must be finite and >= 0");
+    if (!Bsh || !k || !w || !C) return fail(RSVD_ERR_ARG, "NULL pointer");
+    if (!aligned16(Bsh)) return fail(RSVD_ERR_ARG, "misaligned pointer");
+    const int nlm = (L + 1) * (L + 1);
+    const int64_t threads = (int64_t)R * R * 32;
+    kernel_translated_sh_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const double2 *>(Bsh), R, nlm, k, w, sigma, C);
+    count_launches(1);
+    return cuda_check(cudaGetLastError(), "kernel_translated_sh launch");
 }
 
 extern "C" rsvd_status rsvd_build_basis_translated(const void *templates, int64_t T, int32_t R, int32_t Q,

@@ -59,7 +59,7 @@ def test_sizes(lib):
     assert api.kernel_chunk() == 16
     assert api.kernel_partials_bytes(8192, 128) == 512 * 128 * 128 * 8
     assert api.align_min_workspace_bytes(512) == 128 * 256 * 256 * 8
-    assert lib.rsvd_abi_version() == 5
+    assert lib.rsvd_abi_version() == 6
 
 
 def test_eigen_solver_matches_lapack(lib):

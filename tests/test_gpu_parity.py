@@ -429,3 +429,32 @@ def test_ctf_group_bases_end_to_end():
         Bg = (B.astype(np.complex128) * ctfs[g][None, :, None])
         X_ref = ref.landscape_rank(to_np(imgs), Bg, to_np(w), U, m, t).real
         assert np.abs(X[m, t] - X_ref).max() <= TOL_FP32 * np.abs(X_ref).max()
+
+
+def test_closed_form_translation_kernel_matches_oracle():
+    """Row f2, closed form: rsvd_kernel_translated_sh vs the oracle T1 at several
+    translation widths, then the basis from it through rsvd_eigen_basis vs the oracle's on the
+    leading (well-separated) eigenspace."""
+    from synth.volumes import ball_points, sh_coefficients
+    from synth import radial_grid
+    rng = np.random.default_rng(21)
+    atoms = ball_points(rng, 40, 0.3)
+    R, L = 32, 40
+    kk, ww = radial_grid(R)
+    B = sh_coefficients(atoms, kk, L, sigma=0.05)
+    Bd = torch.tensor(B, dtype=torch.complex128, device="cuda")
+    kd, wd = cuda(kk, torch.float64), cuda(ww, torch.float64)
+    for sig in [0.0, 0.01, 0.03]:
+        C = api.kernel_translated_sh(Bd, kd, wd, sig).cpu().numpy()
+        C_ref = ref.kernel_translated_sh(B, kk, ww, sig)
+        assert np.abs(C - C_ref).max() <= 1e-12 * np.abs(C_ref).max(), sig
+        assert np.array_equal(C, C.T)
+        C2 = api.kernel_translated_sh(Bd, kd, wd, sig).cpu().numpy()
+        assert np.array_equal(C, C2)                                   # deterministic
+        U, lam = api.eigen_basis(C, 8)
+        Ur, lr = ref.basis(C_ref, 8)
+        assert np.abs(lam[:8] - lr[:8]).max() <= 1e-10 * lr[0]
+        h = 4
+        assert np.abs(U[:, :h] @ U[:, :h].T - Ur[:, :h] @ Ur[:, :h].T).max() <= 1e-8
+    with pytest.raises(api.RsvdError):
+        api.kernel_translated_sh(Bd, kd, wd, -1.0)

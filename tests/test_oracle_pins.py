@@ -513,3 +513,70 @@ def test_F3_library_ctf_basis_matches_oracle(lib_built=None):
     assert np.abs(lam - lr).max() <= 1e-12 * lr[0]
     assert np.linalg.norm(U @ U.T - Ur @ Ur.T, 2) <= 1e-9 / ((lr[H - 1] - lr[H]) / lr[0])
     np.testing.assert_allclose(Ut, c[:, None] * U, rtol=0, atol=1e-15)
+
+
+# ------------------------------------------------------------------------------ T1 (row f2, closed form)
+def _slices_analytic(atoms, k, Q, views, shifts, sig_a):
+    """Central slices of sum_a exp(-sig^2 k^2/2) exp(-i kvec . c_a) on the polar grid, viewing direction
+    v, translated in-plane by (dx, dy) (Fourier shift theorem), evaluated directly (test helper)."""
+    psi = 2 * np.pi * np.arange(Q) / Q
+    out = np.empty((len(views), len(k), Q), np.complex128)
+    for i, (v, (dx, dy)) in enumerate(zip(views, shifts)):
+        v = v / np.linalg.norm(v)
+        a = np.cross(v, [0.3, 0.5, 0.8])
+        a /= np.linalg.norm(a)
+        b = np.cross(v, a)
+        dirs = np.cos(psi)[:, None] * a + np.sin(psi)[:, None] * b
+        kv = k[:, None, None] * dirs[None]
+        F = np.exp(-0.5 * sig_a ** 2 * k ** 2)[:, None] * np.exp(-1j * (kv @ atoms.T)).sum(-1)
+        out[i] = F * np.exp(-1j * k[:, None] * (dx * np.cos(psi) + dy * np.sin(psi))[None])
+    return out
+
+
+def test_T1_E_minus_is_a_gaussian():
+    """The printed E-(k) (modified Bessel functions of order -+1/2) equals exp(-k^2 sigma^2 / 2):
+    I_{-1/2}(x) - I_{1/2}(x) = sqrt(2/(pi x)) e^{-x} (textbook closed forms of the half-order I)."""
+    k = np.linspace(0.0, 60.0, 41)
+    for sig in [0.005, 0.02, 0.05]:
+        assert np.allclose(ref.E_minus(k, sig), np.exp(-0.5 * (k * sig) ** 2), rtol=1e-12, atol=1e-300)
+    assert np.array_equal(ref.E_minus(k, 0.0), np.ones_like(k))
+
+
+def test_T1_E_plus_is_the_translation_average_along_a_ray():
+    """E+(k, k') = E_delta[exp(-i (k - k') u . delta)] for an isotropic Gaussian delta (std sigma per
+    axis) and any unit u: u . delta ~ N(0, sigma^2), evaluated here by Gauss-Hermite quadrature."""
+    x, wq = np.polynomial.hermite_e.hermegauss(80)
+    wq = wq / wq.sum()
+    k = np.linspace(1.0, 40.0, 9)
+    for sig in [0.01, 0.03]:
+        avg = np.array([[np.sum(wq * np.exp(-1j * (a - b) * sig * x)) for b in k] for a in k])
+        assert np.abs(avg.imag).max() < 1e-14
+        assert np.allclose(ref.E_plus(k, k, sig), avg.real, rtol=1e-12, atol=1e-15)
+
+
+def test_T1_closed_form_against_the_view_average():
+    """sigma_d = 0: the O3 kernel of central slices at uniform random views converges (as the views
+    are averaged) to (1/4 pi) sum_lm conj(B_lm) B_lm' minus the view average of the ring
+    mean, which by Funk-Hecke is (1/4 pi) sum_{even l} P_l(0)^2 sum_m conj(B_lm) B_lm'.  T1 keeps the l = 0
+    mean term only (as printed), so T1 plus the even l >= 2 terms (computed here independently) must
+    match the Monte-Carlo kernel; the printed form alone misses by the size of those terms (reading T1)."""
+    from scipy.special import eval_legendre
+    from synth.volumes import ball_points, sh_coefficients
+    rng = np.random.default_rng(11)
+    atoms = ball_points(rng, 20, 0.3)
+    R, Q, L, nt = 12, 64, 30, 3000
+    k = np.linspace(2.0, 40.0, R)
+    w = np.linspace(0.5, 2.0, R)
+    B = sh_coefficients(atoms, k, L, sigma=0.05)
+    views = rng.standard_normal((nt, 3))
+    C_mc = ref.kernel_C(_slices_analytic(atoms, k, Q, views, np.zeros((nt, 2)), 0.05), w)
+    C_t1 = ref.kernel_translated_sh(B, k, w, 0.0) / (4 * np.pi)
+    even = np.zeros((R, R))
+    for l in range(2, L + 1, 2):
+        c = B[:, l * l:(l + 1) * (l + 1)]
+        even += eval_legendre(l, 0.0) ** 2 * np.einsum("rm,sm->rs", np.conj(c), c).real
+    even *= np.sqrt(np.outer(w, w)) / (4 * np.pi)
+    err_exact = np.linalg.norm(C_mc - (C_t1 - even)) / np.linalg.norm(C_mc)
+    err_printed = np.linalg.norm(C_mc - C_t1) / np.linalg.norm(C_mc)
+    assert err_exact < 0.02                       # Monte-Carlo error ~ 1/sqrt(nt)
+    assert err_printed > 3 * err_exact            # the printed mean term is an approximation (reading T1)
