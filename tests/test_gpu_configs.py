@@ -139,3 +139,27 @@ def test_translations_streamed_landscape_and_argmax():
             err = np.abs(got - X_ref[sel]).max()
             assert err <= tol_abs, err / np.abs(X_ref).max()
     torch.cuda.synchronize()
+
+
+def test_large_per_image_winners_against_all_templates():
+    """Bench configuration (Large, PER_IMAGE, 128 MB workspace): for two images the per-image winner
+    is checked against the oracle's rank-H landscape over ALL 8192 templates x 512 angles (O2 direct
+    sums, ~5e10 complex MACs per image on the host cores): value within the tolerance of the global
+    max, and (t, k) inside the oracle's near-tie set."""
+    d = make_dataset("large", device="cuda")
+    M, T, Q, H = d.images.shape[0], d.templates.shape[0], d.Q, 24
+    w = to_np(d.w)
+    U, _ = api.build_basis(d.templates, w, H)
+    ib, tb = _blocks(d, U, H)
+    work = torch.empty(WORK // 4, dtype=torch.float32, device="cuda")
+    keys = api.winners_reset(torch.zeros(M, dtype=torch.int64, device="cuda"))
+    api.align_argmax(ib, M, tb, T, Q, H, api.PER_IMAGE, work, best_key=keys)
+    val, tw, kw = (to_np(x) for x in api.winners_unpack(keys, Q))
+    B = d.templates.cpu().numpy()
+    for m in [5, 12345]:
+        A = _rows(d.images, [m])
+        X = ref.landscape_rank(A, B, w, U, np.zeros(T, np.int64), np.arange(T)).real      # [T, Q]
+        v_ref, t_ref, k_ref = ref.per_image_winner(X)
+        tol_abs = TOL_FP32 * np.abs(X).max()
+        assert abs(float(val[m]) - v_ref) <= tol_abs, (m, float(val[m]), v_ref)
+        assert X[tw[m], kw[m]] >= v_ref - tol_abs, (m, tw[m], kw[m], t_ref, k_ref)
