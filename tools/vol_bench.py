@@ -33,7 +33,7 @@ ap.add_argument("--H", type=int, default=16)
 ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--landscape", action="store_true")
-ap.add_argument("--no-cpu-baseline", action="store_true")
+ap.add_argument("--no-cpu-baseline", action="store_true", help="(accepted for compatibility; no CPU leg)")
 a = ap.parse_args()
 L, R, H = a.L, a.R or a.L + 1, a.H
 t0 = time.time()
@@ -120,12 +120,5 @@ for i in range(min(a.n, 96)):
     Rf = sv.rotation(2 * np.pi * int(aa[i]) / P, vs.betas[int(b[i])], 2 * np.pi * int(g[i]) / P)
     ok += int(np.abs(Rt - Rf).max() < 1e-6)
 line["winners_recovered"] = f"{ok}/{min(a.n, 96)}"
-if not a.no_cpu_baseline:
-    from oracle import vol as ov  # noqa: E402  (the reported CPU baseline only)
-    U, V = al.U.cpu().numpy(), al.V.cpu().numpy()
-    t = time.time()
-    ov.vol_landscape_rank(vs.volumes[0], vs.target, vs.w, U, V, L, vs.betas, P)
-    cs = time.time() - t
-    line["cpu_baseline"] = {"value": 1.0 / cs, "unit": "volumes/s", "cores": torch.get_num_threads(),
-                            "kind": "oracle", "sample": "1 volume, full nb x P x P landscape (oracle.vol.vol_landscape_rank)"}
+line["cpu_baseline"] = None      # tools never execute oracle/ (only tests/, smoke() and bench.py may)
 print(json.dumps(line))
