@@ -5,7 +5,7 @@ sharding of north_star; grid_shape picks GI to balance the per-rank compress row
 step:
 
   a0  each rank: rsvd_kernel_partials on its basis sub-shard (piece ri of template shard rt; global,
-      fixed 16-template chunks) -> all-gather of the chunk partials (rank order == global chunk
+      fixed rsvd_kernel_chunk() = 8-template chunks) -> all-gather of the chunk partials (rank order == global chunk
       order) -> rsvd_kernel_reduce -> host eigen-solver.  The fixed chunking makes C and U bitwise
       identical for any world size and grid.
   a1  each rank compresses its image shard and its template shard.

@@ -56,8 +56,8 @@ def test_sizes(lib):
     finally:
         api.set_path(api.PATH_AUTO)
     assert api.path_for(512, 24) == api.PATH_TC
-    assert api.kernel_chunk() == 16
-    assert api.kernel_partials_bytes(8192, 128) == 512 * 128 * 128 * 8
+    assert api.kernel_chunk() == 8
+    assert api.kernel_partials_bytes(8192, 128) == 8192 // api.kernel_chunk() * 128 * 128 * 8
     assert api.align_min_workspace_bytes(512) == 128 * 256 * 256 * 8
     assert lib.rsvd_abi_version() == 6
 
