@@ -44,7 +44,7 @@ struct Fft2Cfg {
     static constexpr int SLOT = ((UBYTES > ZBYTES ? UBYTES : ZBYTES) + 1023) / 1024 * 1024;
     static constexpr int P2_PER = TB * N2 / GT;       // pass-2 tasks per thread
     static constexpr int NSLOT = G + 1;               // one slot in flight beyond the G being processed
-    static constexpr size_t smem_bytes() { return 1024 + (size_t)NSLOT * SLOT + (size_t)N * 8 + (size_t)(N / 2) * 8 + NSLOT * 12 + 64; }
+    static constexpr size_t smem_bytes() { return 1024 + (size_t)NSLOT * SLOT + (size_t)N * 8 + (size_t)(N / 2) * 8 + NSLOT * 20 + 64; }
 };
 
 // Z_r and Z_{N-r} from a = U_r, b = U_{N-r} (0 < r < N/2), w = W_Q^r.
@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
     // tag[s] = local index of the item whose load was last issued into slot s.  A group may reach
     // its wait for item i while slot i % NSLOT still holds (or is loading) item i - NSLOT: the parity
     // wait alone would then pass one phase early, so it first waits for the tag.
-    volatile int *tag = reinterpret_cast<volatile int *>(full + C::NSLOT);   // [NSLOT]
+    uint64_t *empty = full + C::NSLOT;                                // [NSLOT] slot read out (TASKS warps)
+    volatile int *tag = reinterpret_cast<volatile int *>(empty + C::NSLOT);   // [NSLOT]
 
     const int tid = threadIdx.x;
     const int g = tid / GT, gt = tid - g * GT;
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
     if (tid == 0) {
         for (int sl = 0; sl < C::NSLOT; ++sl) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fr_smem(full + sl)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(fr_smem(empty + sl)), "r"(C::TASKS));
             tag[sl] = -1;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -213,8 +215,13 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
 #pragma unroll
             for (int i = 0; i < N1; ++i) w[j][i] = yr[i];
         }
-        gbar();                                                // (C) slot free: refill it NSLOT items ahead
+        // (C) this warp's reads of the slot are done: one arrival per warp (release); only the group's
+        // issuing thread waits for all TASKS warps before refilling the slot NSLOT items ahead, the
+        // other warps go straight on to pass 2
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fr_smem(empty + sl)) : "memory");
         if (gt == 0 && item_of(i + C::NSLOT) < nitems) {
+            fr_mbar_wait(empty + sl, (uint32_t)(i / C::NSLOT) & 1u);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(i + C::NSLOT);
         }
