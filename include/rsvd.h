@@ -95,11 +95,14 @@ int64_t rsvd_align_min_workspace_bytes(int32_t Q);
  *   S_t[r] = sum_j b_t[r,j], in fp64 to partials [ceil(T/chunk)][R][R] (device).  A rank holding
  *   templates [t0, t0+T) with t0 % chunk == 0 produces exactly the global chunks t0/chunk... so that
  *   the concatenation over ranks is independent of the sharding.
- * rsvd_kernel_reduce: device.  Sums partials[0..nchunks) in index order (fixed order => bitwise
+ * rsvd_kernel_reduce: device.  Sums partials[0..nchunks) in a fixed tree over the chunk index (chunk c into
+ *   partial sum c mod 8 in ascending c, then the 8 partial sums in order; fixed order => bitwise
  *   identical for any sharding) and writes C (device fp64 [R][R], exactly symmetric) using the
  *   device weights w[R] and the global template count T_total.
  * rsvd_eigen_basis: host only.  Householder tridiagonalisation + implicit QL/QR with Wilkinson
- *   shifts, fp64, deterministic.  U (host [R][H] row-major), lambda (host [R], may be NULL).
+ *   shifts, fp64, deterministic; for H <= R/2 the H leading vectors come from inverse iteration on the
+ *   tridiagonal form (residual-checked, else the full QR path).  U (host [R][H] row-major), lambda
+ *   (host [R], may be NULL).
  * rsvd_build_basis: single-device convenience = partials + reduce + D2H + eigen.  Synchronises. */
 rsvd_status rsvd_kernel_partials(const void *templates, int64_t T, int32_t R, int32_t Q,
                                  double *partials, rsvd_stream_t stream);

@@ -158,17 +158,31 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
 constexpr size_t KP_SMEM = 2 * (size_t)BT * (JB + 1) * sizeof(double2) + 2 * (size_t)BT * JB * sizeof(float2);
 
 // C[r][r'] = sqrt(w_r w_r') / (T Q) * sum_c P_c[max(r,r')][min(r,r')] (lower triangle is the
-// computed one; reading it for both halves makes C exactly symmetric).
-__global__ void kernel_reduce_kernel(const double *__restrict__ partials, int64_t nchunks, int R,
-                                     double scale, const double *__restrict__ w, double *__restrict__ C) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)R * R) return;
-    const int r = (int)(idx / R), s = (int)(idx % R);
+// computed one; reading it for both halves makes C exactly symmetric).  The chunk sum is a fixed
+// two-level tree (chunk c into partial sum c mod 8 in ascending c, then the 8 partial sums in order),
+// so C is bitwise the same for any sharding of the chunks over ranks.
+constexpr int KR_WARPS = 8;    // chunk-parallel reduce: warp w sums chunks w, w + 8, ... of 32 entries
+__global__ void __launch_bounds__(KR_WARPS * 32) kernel_reduce_kernel(const double *__restrict__ partials, int64_t nchunks,
+                                                                       int R, double scale, const double *__restrict__ w,
+                                                                       double *__restrict__ C) {
+    __shared__ double part[KR_WARPS][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t idx = (int64_t)blockIdx.x * 32 + lane;
+    const bool ok = idx < (int64_t)R * R;
+    const int r = ok ? (int)(idx / R) : 0, s = ok ? (int)(idx % R) : 0;
     const int hi = r > s ? r : s, lo = r > s ? s : r;
     // tiles with ti < tj were skipped: the element (hi, lo) always lies in a computed tile
     double acc = 0.0;
-    for (int64_t c = 0; c < nchunks; ++c) acc += partials[c * (int64_t)R * R + (int64_t)hi * R + lo];
-    C[idx] = acc * scale * sqrt(w[r]) * sqrt(w[s]);
+    if (ok)
+        for (int64_t c = warp; c < nchunks; c += KR_WARPS) acc += partials[c * (int64_t)R * R + (int64_t)hi * R + lo];
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && ok) {
+        double t = part[0][lane];                           // fixed order over the warps: deterministic
+#pragma unroll
+        for (int i = 1; i < KR_WARPS; ++i) t += part[i][lane];
+        C[idx] = t * scale * sqrt(w[r]) * sqrt(w[s]);
+    }
 }
 
 // ramp[s][r][j] = exp(-i k_r (dx_s cos psi_j + dy_s sin psi_j)), fp64 (row f2; reading G15)
@@ -274,7 +288,7 @@ extern "C" rsvd_status rsvd_kernel_reduce(const double *partials, int64_t nchunk
     if (!partials || !w || !C) return fail(RSVD_ERR_ARG, "NULL pointer");
     const double scale = 1.0 / ((double)T_total * (double)Q);
     const int64_t n = (int64_t)R * R;
-    kernel_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+    kernel_reduce_kernel<<<(unsigned)((n + 31) / 32), KR_WARPS * 32, 0, (cudaStream_t)stream>>>(
         partials, nchunks, R, scale, w, C);
     count_launches(1);
     return cuda_check(cudaGetLastError(), "kernel_reduce launch");
