@@ -27,7 +27,8 @@ rsvd_status fail(rsvd_status st, const std::string &msg);
 
 namespace {
 
-// A (n x n, row-major, symmetric) -> tridiagonal (d, e) with A = Z T Z^T, Z = H_0 H_1 ... H_{n-3},
+// A (n x n, row-major, symmetric; only the lower triangle is read after the first step) -> tridiagonal
+// (d, e) with A = Z T Z^T, Z = H_0 H_1 ... H_{n-3},
 // H_k = I - beta_k v_k v_k^T acting on indices k+1..n-1.  The reflectors are kept in refl (row k:
 // v_k at offsets k+1.., beta_k in betas[k], 0 = identity); accumulate_z forms Z from them.
 void householder_tridiag(int n, std::vector<double> &A, std::vector<double> &d, std::vector<double> &e,
@@ -49,20 +50,29 @@ void householder_tridiag(int n, std::vector<double> &A, std::vector<double> &d, 
         for (int i = 0; i < m; ++i) vv += v[i] * v[i];
         if (vv == 0.0) continue;
         const double beta = 2.0 / vv;
-        // trailing block B = A[k+1.., k+1..]:  B <- H B H = B - v q^T - q v^T
+        // trailing block B = A[k+1.., k+1..] (only its lower triangle is kept up to date):
+        // p = beta B v by the symmetric matvec over row prefixes (a dot and an axpy, both contiguous),
+        // then B <- H B H = B - v q^T - q v^T on the lower triangle
+        for (int i = 0; i < m; ++i) p[i] = 0.0;
         for (int i = 0; i < m; ++i) {
-            double s = 0.0;
             const double *row = &A[(size_t)(k + 1 + i) * n + (k + 1)];
-            for (int j = 0; j < m; ++j) s += row[j] * v[j];
-            p[i] = beta * s;
+            double s = row[i] * v[i];
+            const double vi = v[i];
+            for (int j = 0; j < i; ++j) {
+                s += row[j] * v[j];
+                p[j] += row[j] * vi;
+            }
+            p[i] += s;
         }
+        for (int i = 0; i < m; ++i) p[i] *= beta;
         double vp = 0.0;
         for (int i = 0; i < m; ++i) vp += v[i] * p[i];
         const double K = 0.5 * beta * vp;
         for (int i = 0; i < m; ++i) q[i] = p[i] - K * v[i];
         for (int i = 0; i < m; ++i) {
             double *row = &A[(size_t)(k + 1 + i) * n + (k + 1)];
-            for (int j = 0; j < m; ++j) row[j] -= v[i] * q[j] + q[i] * v[j];
+            const double vi = v[i], qi = q[i];
+            for (int j = 0; j <= i; ++j) row[j] -= vi * q[j] + qi * v[j];
         }
         A[(size_t)(k + 1) * n + k] = alpha;
         A[(size_t)k * n + (k + 1)] = alpha;
