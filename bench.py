@@ -509,11 +509,12 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": args.config, "M": M, "T": T, "R": R, "Q": Q, "H": H, "mode": "per_pair argmax sample",
-                   "seed": 220207235},
+        "config": {"workload": args.config, "M": M, "T": T, "R": R, "Q": Q, "H": H, "mode": "per_image",
+                   "parallelism": "host cores (OpenMP over pairs)", "seed": 220207235},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
-                         "sample": f"{n_step} seeded random (m,t) pairs per step; O2 rank-{H} fp64 direct sum + "
-                                   f"argmax, oracle basis (eigh of C from {nb} templates)"},
+                         "sample": f"{n_step} seeded random (m,t) pairs of the workload per step: O2 rank-{H} fp64 "
+                                   f"direct-sum landscape over all {Q} angles + argmax per pair (the per-image "
+                                   f"winner is the max of these), oracle basis (eigh of C from {nb} templates)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
