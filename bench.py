@@ -56,8 +56,9 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--work-mb", type=int, default=None, help="align workspace (default: library recommendation)")
     p.add_argument("--path", default=None, choices=["auto", "simt", "tc"], help="contraction path override")
-    p.add_argument("--shard", default="2d", choices=["2d", "templates"],
-                   help="rank grid: image x template shards (dist.grid_shape) or templates only")
+    p.add_argument("--shard", default="templates", choices=["2d", "templates"],
+                   help="rank grid: templates only (north_star: templates sharded over the GPUs, default) or "
+                        "image x template shards (dist.grid_shape)")
     return p.parse_args()
 
 
@@ -520,8 +521,28 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` without a torchrun environment: re-launch this script as N ranks
+    (one process per GPU) through torch.distributed.run on 127.0.0.1 and return its exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=dict(os.environ, BENCH_SPAWNED="1"))
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

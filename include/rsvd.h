@@ -92,7 +92,9 @@ int64_t rsvd_align_min_workspace_bytes(int32_t Q);
  * rsvd_kernel_partials: device, deterministic.  For each fixed chunk c of rsvd_kernel_chunk()
  *   consecutive templates (the last may be short) writes the un-normalised, unweighted partial
  *   P_c[r][r'] = sum_{t in c} Re( sum_j b_t[r,j] conj(b_t[r',j]) - (1/Q) S_t[r] conj(S_t[r']) ),
- *   S_t[r] = sum_j b_t[r,j], in fp64 to partials [ceil(T/chunk)][R][R] (device).  A rank holding
+ *   S_t[r] = sum_j b_t[r,j], in fp64 to partials [ceil(T/chunk)][R][R] (device).  P_c is symmetric and
+ *   only its lower triangle (entries r >= r') is written; the upper-triangle entries of the buffer are
+ *   left as the caller allocated them (rsvd_kernel_reduce reads the lower triangle only).  A rank holding
  *   templates [t0, t0+T) with t0 % chunk == 0 produces exactly the global chunks t0/chunk... so that
  *   the concatenation over ranks is independent of the sharding.
  * rsvd_kernel_reduce: device.  Sums partials[0..nchunks) in a fixed tree over the chunk index (chunk c into
@@ -247,10 +249,17 @@ rsvd_status rsvd_combine_winners(const uint64_t *keys, int32_t G, int64_t M, int
  *   launch is bracketed by CUDA events recorded on its own stream (process-global, thread-safe).
  * rsvd_timing_read: synchronises on the recorded events, returns per-kind total milliseconds and
  *   launch counts (kinds: 0 contraction, 1 fft_reduce, 2 compress, 3 kernel partials) for the
- *   spans recorded since the previous read, and recycles the events. */
+ *   spans recorded since the previous read, and recycles the events.
+ * rsvd_probe_fp32: the measured FP32 peak of the current device (roofline denominator Pi_fp32 of
+ *   SURVEY.md 8(d)): one launch of register-only dependency chains on every SM (4 x 256 threads per
+ *   SM, 8 chains per thread, `iters` x 32 instructions per chain), timed with CUDA events on `stream`
+ *   after a short warm-up launch; synchronises.  kind 0 = FFMA, 1 = FFMA2 (packed fp32x2, sm_100),
+ *   2 = FADD2.  *tflops = flops / elapsed (FFMA 2, FFMA2 4, FADD2 2 flops per lane and instruction).
+ *   Not part of the method; allocates a 1 KB scratch buffer. */
 int64_t rsvd_launch_count(void);
 void rsvd_timing_enable(int32_t on);
 rsvd_status rsvd_timing_read(double *ms, int64_t *count, int32_t nkinds);
+rsvd_status rsvd_probe_fp32(int32_t kind, int32_t iters, double *tflops, rsvd_stream_t stream);
 
 #ifdef __cplusplus
 }

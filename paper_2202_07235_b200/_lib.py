@@ -48,6 +48,7 @@ SIGNATURES = [
     ("rsvd_launch_count", _I64, []),
     ("rsvd_timing_enable", None, [_I32]),
     ("rsvd_timing_read", _I32, [_P, _P, _I32]),
+    ("rsvd_probe_fp32", _I32, [_I32, _I32, _P, _P]),
     # row f4 (include/rsvd_vol.h)
     ("rsvd_vol_ncoef", _I64, [_I32]),
     ("rsvd_vol_kernels", _I32, [_P, _I64, _I32, _I32, _P, _P, _P, _P]),
@@ -98,6 +99,8 @@ def ptr(t) -> int | None:
 
 
 def stream_handle(stream=None) -> int:
+    """The caller's stream, else the current device's current stream (require_cuda has checked that
+    the tensors live on the current device, so the work lands on the tensors' device)."""
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
 
@@ -110,3 +113,6 @@ def require_cuda(*tensors):
             raise RsvdError(1, "expected a CUDA tensor")
         if t is not None and not t.is_contiguous():
             raise RsvdError(1, "expected a contiguous tensor")
+        if t is not None and t.device.index != torch.cuda.current_device():
+            raise RsvdError(1, f"tensor on {t.device} but the current device is cuda:{torch.cuda.current_device()} "
+                               "(library work goes to the current device's stream: torch.cuda.set_device first)")

@@ -33,7 +33,7 @@ PATH_AUTO, PATH_SIMT, PATH_TC = 0, 1, 2
 
 
 def path_for(Q: int, H: int) -> int:
-    """1 = FP32 SIMT contraction, 2 = tcgen05 3xTF32 contraction (include/rsvd.h)."""
+    """1 = FP32 SIMT contraction, 2 = tcgen05 contraction, fp16 hi/lo split x3 MMAs (include/rsvd.h)."""
     return int(_lib.lib().rsvd_path_for(Q, H))
 
 
@@ -304,6 +304,17 @@ def timing_read():
     cnt = np.zeros(len(TIMING_KINDS), dtype=np.int64)
     check(_lib.lib().rsvd_timing_read(ptr(ms), ptr(cnt), len(TIMING_KINDS)))
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(TIMING_KINDS)}
+
+
+PROBE_KINDS = {"ffma": 0, "ffma2": 1, "fadd2": 2}
+
+
+def probe_fp32(kind: str = "ffma2", iters: int = 200000, stream=None) -> float:
+    """Measured sustained FP32 TFLOP/s of the current device (rsvd_probe_fp32): the Pi_fp32 roofline
+    denominator of SURVEY.md 8(d)."""
+    out = np.zeros(1, dtype=np.float64)
+    check(_lib.lib().rsvd_probe_fp32(PROBE_KINDS[kind], iters, ptr(out), stream_handle(stream)))
+    return float(out[0])
 
 
 # ------------------------------------------------------------------ the full path

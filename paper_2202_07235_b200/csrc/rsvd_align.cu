@@ -232,6 +232,7 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     CUtensorMap tmap;
     if ((e = make_tmap_any(LOGN, &tmap, Upk, Mc, Tc)) != cudaSuccess) return cuda_check(e, "spectrum tensor map");
     const bool timed = timing_enabled();
+    bool first = true;
     for (int64_t t0 = 0; t0 < Tpad; t0 += Tc) {
         const int64_t tc_ = std::min(Tc, Tpad - t0);
         const int64_t tcv = std::min(tc_, a.T - t0);
@@ -240,7 +241,8 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
             const int64_t mcv = std::min(mc, a.M - m0);
             cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
             if (tc) {
-                e = launch_contract_tc(tmA, tmB, a.H, N, Nout, m0, t0, mc, tc_, Mc, Tc, Upk, num_sms(), s);
+                e = launch_contract_tc(tmA, tmB, a.H, N, Nout, m0, t0, mc, tc_, Mc, Tc, Upk, num_sms(), first, s);
+                first = false;
                 if (e != cudaSuccess) return cuda_check(e, "contract (tcgen05) launch");
             } else {
                 dim3 g1((unsigned)(tc_ / CT_TILE), (unsigned)(mc / CT_TILE), (unsigned)((N + 1 + CT_QB - 1) / CT_QB));

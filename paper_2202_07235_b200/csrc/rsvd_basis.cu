@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
         }
 }
 constexpr size_t KP_SMEM = 2 * (size_t)BT * (JB + 1) * sizeof(double2) + 2 * (size_t)BT * JB * sizeof(float2);
+static std::atomic<uint64_t> g_partials_attr{0};   // per-device max-smem attribute of kernel_partials_kernel
 
 // C[r][r'] = sqrt(w_r w_r') / (T Q) * sum_c P_c[max(r,r')][min(r,r')] (lower triangle is the
 // computed one; reading it for both halves makes C exactly symmetric).  The chunk sum is a fixed
@@ -266,11 +267,9 @@ extern "C" rsvd_status rsvd_kernel_partials(const void *templates, int64_t T, in
     dim3 grid(nt, nt, (unsigned)nchunks);
     const bool timed = timing_enabled();
     cudaEvent_t ev0 = timed ? timing_event((cudaStream_t)stream) : nullptr;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kernel_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KP_SMEM);
+    {
+        const cudaError_t e = smem_attr_once((const void *)kernel_partials_kernel, (int)KP_SMEM, g_partials_attr);
         if (e != cudaSuccess) return cuda_check(e, "kernel_partials attribute");
-        attr = true;
     }
     kernel_partials_kernel<<<grid, NTHR, KP_SMEM, (cudaStream_t)stream>>>(
         reinterpret_cast<const float2 *>(templates), T, R, Q, partials, nullptr, 1);
@@ -355,12 +354,8 @@ extern "C" rsvd_status rsvd_build_basis_translated(const void *templates, int64_
         st = cuda_check(cudaGetLastError(), "ramp launch");
     }
     if (st == RSVD_OK) {
-        static bool attr = false;
-        if (!attr) {
-            e = cudaFuncSetAttribute(kernel_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KP_SMEM);
-            if (e != cudaSuccess) st = cuda_check(e, "kernel_partials attribute");
-            attr = (e == cudaSuccess);
-        }
+        e = smem_attr_once((const void *)kernel_partials_kernel, (int)KP_SMEM, g_partials_attr);
+        if (e != cudaSuccess) st = cuda_check(e, "kernel_partials attribute");
     }
     if (st == RSVD_OK) {
         const int nt = (R + BT - 1) / BT;

@@ -322,17 +322,6 @@ __global__ void __launch_bounds__(FR_THREADS, 2) fft_reduce_kernel(const __grid_
     }
 }
 
-inline int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
-
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency).
 typedef CUresult (*PFN_encodeTiled_fr)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                        const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
@@ -370,14 +359,12 @@ static cudaError_t launch_fft_mode(cudaStream_t s, const CUtensorMap &tm, int64_
                                    int64_t t0, int64_t mcv, int64_t tcv, const FftOut &out) {
     using C = FftCfg<LOGN>;
     const size_t smem = C::smem_bytes();
-    static int occ = 0;
-    if (!occ) {
-        cudaError_t e = cudaFuncSetAttribute(fft_reduce_kernel<LOGN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fft_reduce_kernel<LOGN, MODE>, FR_THREADS, smem);
-        if (e != cudaSuccess || occ < 1) occ = 1;
-    }
+    static std::atomic<uint64_t> attr{0};
+    cudaError_t e = smem_attr_once((const void *)fft_reduce_kernel<LOGN, MODE>, (int)smem, attr);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fft_reduce_kernel<LOGN, MODE>, FR_THREADS, smem);
+    if (e != cudaSuccess || occ < 1) occ = 1;
     const int64_t nitems = tcv * ((mcv + C::TB - 1) / C::TB);
     const int64_t grid = std::min<int64_t>(nitems, (int64_t)num_sms() * occ);
     fft_reduce_kernel<LOGN, MODE><<<(unsigned)grid, FR_THREADS, smem, s>>>(tm, Mc, Tc, m0, t0, mcv, tcv, out);

@@ -308,13 +308,9 @@ static cudaError_t launch_fft2_mode(cudaStream_t s, const CUtensorMap &tm, int64
                                     int64_t tcv, const FftOut &out, float *Upk, int64_t Mc, int64_t Tc) {
     using C = Fft2Cfg<LOGN>;
     const size_t smem = C::smem_bytes();
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(fft2_reduce_kernel<LOGN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    const cudaError_t e = smem_attr_once((const void *)fft2_reduce_kernel<LOGN, MODE>, (int)smem, attr);
+    if (e != cudaSuccess) return e;
     const int64_t nitems = tcv * ((mcv + C::TB - 1) / C::TB);
     const int64_t grid = std::min<int64_t>((nitems + C::G - 1) / C::G, (int64_t)num_sms());
     cudaLaunchConfig_t cfg = {};

@@ -1,0 +1,85 @@
+// rsvd_probe.cu -- measured FP32 peak of this GPU for the roofline denominators (SURVEY.md 8(d):
+// "Pi_fp32 is measured on the box (sustained FFMA microbenchmark)").  Not part of the method.
+//
+// Every thread runs NCH independent dependency chains of the probed instruction on register operands
+// (no memory traffic inside the loop), on 4 resident CTAs x 256 threads per SM.  The sustained rate is
+// flops / elapsed time over a launch long enough (~100 ms) to settle under the power cap.
+//   kind 0  FFMA  (scalar, 3-register form)        2 flops per lane per instruction
+//   kind 1  FFMA2 (sm_100 packed fp32x2)           4 flops per lane per instruction
+//   kind 2  FADD2 (sm_100 packed fp32x2 add)        2 flops per lane per instruction
+#include <cuda_runtime.h>
+
+#include "rsvd_common.cuh"
+
+namespace rsvd {
+
+constexpr int PR_THREADS = 256;
+constexpr int PR_NCH = 8;
+
+template <int KIND>
+__global__ void __launch_bounds__(PR_THREADS) fp32_probe_kernel(int iters, float seed, float *__restrict__ sink) {
+    float2 acc[PR_NCH];
+    const float2 a = make_float2(seed * 1e-3f + 0.999f, 1.0001f - seed * 1e-3f);
+    const float2 b = make_float2(seed * 1e-7f, -seed * 1e-7f);
+#pragma unroll
+    for (int c = 0; c < PR_NCH; ++c) acc[c] = make_float2((float)(threadIdx.x + c), (float)(blockIdx.x - c));
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int c = 0; c < PR_NCH; ++c) {
+                if constexpr (KIND == 0) {
+                    acc[c].x = fmaf(acc[c].x, a.x, b.x);
+                    acc[c].y = fmaf(acc[c].y, a.y, b.y);
+                } else if constexpr (KIND == 1) {
+                    acc[c] = __ffma2_rn(acc[c], a, b);
+                } else {
+                    acc[c] = __fadd2_rn(acc[c], b);
+                }
+            }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < PR_NCH; ++c) s += acc[c].x + acc[c].y;
+    if (s == 1234.5678f) sink[threadIdx.x] = s;      // never true in practice; keeps the chains live
+}
+
+template <int KIND>
+static cudaError_t run_probe(int iters, cudaStream_t st, float *sink, float *ms) {
+    const int grid = num_sms() * 4;
+    cudaEvent_t e0, e1;
+    cudaError_t e = cudaEventCreate(&e0);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventCreate(&e1)) != cudaSuccess) { cudaEventDestroy(e0); return e; }
+    fp32_probe_kernel<KIND><<<grid, PR_THREADS, 0, st>>>(iters / 16, 0.5f, sink);      // warm-up
+    cudaEventRecord(e0, st);
+    fp32_probe_kernel<KIND><<<grid, PR_THREADS, 0, st>>>(iters, 0.5f, sink);
+    cudaEventRecord(e1, st);
+    e = cudaEventSynchronize(e1);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(ms, e0, e1);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return e;
+}
+
+}  // namespace rsvd
+
+extern "C" rsvd_status rsvd_probe_fp32(int32_t kind, int32_t iters, double *tflops, rsvd_stream_t stream) {
+    using namespace rsvd;
+    if (kind < 0 || kind > 2 || iters < 16 || !tflops) return fail(RSVD_ERR_ARG, "bad probe arguments");
+    float *sink = nullptr;
+    cudaError_t e = cudaMalloc(&sink, PR_THREADS * sizeof(float));
+    if (e != cudaSuccess) return cuda_check(e, "probe sink");
+    float ms = 0.f;
+    cudaStream_t s = (cudaStream_t)stream;
+    e = kind == 0 ? run_probe<0>(iters, s, sink, &ms) : kind == 1 ? run_probe<1>(iters, s, sink, &ms)
+                                                                  : run_probe<2>(iters, s, sink, &ms);
+    cudaFree(sink);
+    if (e != cudaSuccess) return cuda_check(e, "fp32 probe");
+    const double lanes = (double)num_sms() * 4 * PR_THREADS;
+    const double per_iter = 4.0 * PR_NCH * (kind == 0 ? 4.0 : (kind == 1 ? 4.0 : 2.0));   // flops per thread per iter
+    *tflops = lanes * (double)iters * per_iter / (ms * 1e-3) / 1e12;
+    count_launches(2);
+    return RSVD_OK;
+}

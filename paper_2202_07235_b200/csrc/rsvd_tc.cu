@@ -181,7 +181,7 @@ __device__ __forceinline__ void st_spectrum(float *p, float v, uint64_t pol) {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int steps, int KB, int N,
     int mtl, int ntl, int mt0, int nt0, int qg, int nqg, int nitems, int64_t Mc, int64_t Tc,
-    float *__restrict__ Upk, int Nout) {
+    float *__restrict__ Upk, int Nout, int operands_fresh) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint64_t *bars = reinterpret_cast<uint64_t *>(base + TC_STAGES * TC_STAGE_BYTES);
@@ -214,6 +214,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+            // PDL: the operand rows may have just been written by the kernel before us on the stream
+            // (Step 1, compress): then the first TMA must wait for that grid.  Later chunks of one align
+            // call follow the library's own Step-3 kernel, which does not write operands, so their
+            // loads may overlap its tail.
+            if (operands_fresh) asm volatile("griddepcontrol.wait;" ::: "memory");
             // chunks run template-tile outer / image inner: a chunk's template operands are re-read by
             // every following chunk of the same template tile, image operands by none of them
             uint64_t pol_stream, pol_keep;
@@ -795,12 +800,11 @@ cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t ro
 // One chunk: images [m0, m0 + mc) (multiples of 128), templates [t0, t0 + tc) (multiples of 256).
 cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int Nout, int64_t m0,
                                int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms,
-                               cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(contract_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
+                               bool operands_fresh, cudaStream_t s) {
+    static std::atomic<uint64_t> attr{0};
+    {
+        const cudaError_t e = smem_attr_once((const void *)contract_tc_kernel, (int)TC_SMEM, attr);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     const int mtl = (int)(mc / TC_PIMG), ntl = (int)(tc / TC_TT);
     const int ntiles = mtl * ntl;
@@ -822,7 +826,8 @@ cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, i
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, contract_tc_kernel, tmA, tmB, tc_steps(H), tc_kb(H), N, mtl, ntl,
-                                       (int)(m0 / TC_PIMG), (int)(t0 / TC_TT), qg, nqg, nitems, Mc, Tc, Upk, Nout);
+                                       (int)(m0 / TC_PIMG), (int)(t0 / TC_TT), qg, nqg, nitems, Mc, Tc, Upk, Nout,
+                                       operands_fresh ? 1 : 0);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

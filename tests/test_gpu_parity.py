@@ -16,7 +16,7 @@ api = pytest.importorskip("paper_2202_07235_b200.api")
 
 @pytest.fixture(autouse=True, params=["simt", "tc"])
 def contraction_path(request):
-    """Every parity test runs on both contraction paths (FP32 SIMT and tcgen05 3xTF32)."""
+    """Every parity test runs on both contraction paths (FP32 SIMT and tcgen05 with the error-compensated fp16 hi/lo split)."""
     api.set_path(api.PATH_SIMT if request.param == "simt" else api.PATH_TC)
     yield request.param
     api.set_path(api.PATH_AUTO)
