@@ -248,7 +248,7 @@ rsvd_status rsvd_combine_winners(const uint64_t *keys, int32_t G, int64_t M, int
  * rsvd_timing_enable(1): from now on every contraction / FFT-reduce / compress / kernel-partials
  *   launch is bracketed by CUDA events recorded on its own stream (process-global, thread-safe).
  * rsvd_timing_read: synchronises on the recorded events, returns per-kind total milliseconds and
- *   launch counts (kinds: 0 contraction, 1 fft_reduce, 2 compress, 3 kernel partials) for the
+ *   launch counts (kinds: 0 contraction, 1 fft_reduce, 2 compress, 3 kernel partials, 4 fused align) for the
  *   spans recorded since the previous read, and recycles the events.
  * rsvd_probe_fp32: the measured FP32 peak of the current device (roofline denominator Pi_fp32 of
  *   SURVEY.md 8(d)): one launch of register-only dependency chains on every SM (4 x 256 threads per

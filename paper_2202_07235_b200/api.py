@@ -287,7 +287,7 @@ def combine_winners(keys_g: torch.Tensor, Q: int, stream=None):
 
 
 # ------------------------------------------------------------------ instrumentation
-TIMING_KINDS = ("contract", "fft_reduce", "compress", "kernel_partials")
+TIMING_KINDS = ("contract", "fft_reduce", "compress", "kernel_partials", "align_fused")
 
 
 def launch_count() -> int:

@@ -141,15 +141,21 @@ struct AlignArgs {
     float *best_gamma;     // PER_PAIR, optional: parabolic-refined angle
 };
 
-// Steps 3-4 kernel: fft2 (rsvd_fft2.cuh) for N = Q/2 <= 256, the original schedule (rsvd_fft.cuh)
-// for N = 512 or when RSVD_FFT_V1=1 (kept for comparison).
-static bool use_fft2(int LOGN) {
-    static const int v1 = [] { const char *e = getenv("RSVD_FFT_V1"); return e ? atoi(e) : 0; }();
-    return LOGN <= 8 && !v1;
+// Steps 3-4 kernel: fft2 (rsvd_fft2.cuh) for N = Q/2 <= 256; the original schedule (rsvd_fft.cuh)
+// for N = 512 or when RSVD_FFT=1 / RSVD_FFT_V1=1 (kept for comparison).
+static int fft_version(int LOGN) {
+    static const int v = [] {
+        const char *e = getenv("RSVD_FFT");
+        const char *e1 = getenv("RSVD_FFT_V1");
+        if (e1 && atoi(e1)) return 1;
+        return e ? atoi(e) : 2;
+    }();
+    if (LOGN > 8) return 1;
+    return v == 1 ? 1 : 2;
 }
 
 static cudaError_t make_tmap_any(int LOGN, CUtensorMap *tm, const float *Upk, int64_t Mc, int64_t Tc) {
-    if (use_fft2(LOGN)) {
+    if (fft_version(LOGN) >= 2) {
         switch (LOGN) {
             case 4: return make_spectrum_tmap2<4>(tm, Upk, Mc, Tc);
             case 5: return make_spectrum_tmap2<5>(tm, Upk, Mc, Tc);
@@ -172,7 +178,8 @@ static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const CUte
                                   int64_t m0, int64_t t0, int64_t mcv, int64_t tcv, const FftOut &o, float *Upk) {
     static const bool discard = [] { const char *e = getenv("RSVD_NO_DISCARD"); return !(e && atoi(e)); }();
     float *dU = discard ? Upk : nullptr;
-    if (use_fft2(LOGN)) {
+    const int v = fft_version(LOGN);
+    if (v == 2) {
         switch (LOGN) {
             case 4: return launch_fft2<4>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
             case 5: return launch_fft2<5>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
@@ -190,6 +197,9 @@ static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const CUte
         default: return launch_fft<9>(mode, s, tm, Mc, Tc, m0, t0, mcv, tcv, o);
     }
 }
+
+cudaError_t launch_align_fused(const void *alpha, int64_t M, const void *beta, int64_t T, int Q, int H, int mode,
+                               void *work, int64_t work_bytes, const FftOut &out, cudaStream_t s, bool *launched);
 
 static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const int N = a.Q / 2;
@@ -222,6 +232,20 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const FftOut o{a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t, a.T, a.t_offset,
                    tc ? tc_scales(a.alpha, a.M, a.Q, a.H, RSVD_SIDE_IMAGE) : nullptr,
                    tc ? tc_scales(a.beta, a.T, a.Q, a.H, RSVD_SIDE_TEMPLATE) : nullptr, a.best_gamma};
+    if (tc && Nout == N) {
+        // one persistent launch: contraction and transform roles over an L2-sized spectrum ring
+        // (rsvd_fused.cu); falls through to the two-kernel chunk loop where it does not apply
+        cudaEvent_t ev0 = timing_enabled() ? timing_event(s) : nullptr;
+        bool launched = false;
+        cudaError_t ef = launch_align_fused(a.alpha, a.M, a.beta, a.T, a.Q, a.H, a.mode, a.work, a.work_bytes, o, s,
+                                            &launched);
+        if (ef != cudaSuccess) return cuda_check(ef, "fused align launch");
+        if (launched) {
+            count_launches(1);
+            if (ev0) timing_span(ev0, timing_event(s), TK_FUSED);
+            return RSVD_OK;
+        }
+    }
     if (Nout > N) {
         // rows the contraction never writes (im row 0, rows N..Nout-1 except re row N) must read as 0;
         // they are written here once per call and never discarded from L2 (no discard when padded)

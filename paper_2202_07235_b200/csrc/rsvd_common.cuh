@@ -33,7 +33,7 @@ void count_launches(int n);
 bool timing_enabled();
 cudaEvent_t timing_event(cudaStream_t s);
 void timing_span(cudaEvent_t a, cudaEvent_t b, int kind);
-enum { TK_CONTRACT = 0, TK_FFT = 1, TK_COMPRESS = 2, TK_BASIS = 3 };
+enum { TK_CONTRACT = 0, TK_FFT = 1, TK_COMPRESS = 2, TK_BASIS = 3, TK_FUSED = 4 };
 
 // contraction path: FP32 SIMT (block layout "simt") or tcgen05 fp16 hi/lo split on CTA pairs (layout "tc").
 // resolve_path(Q, H) is the single source of truth used by block sizing, compress and align.
@@ -47,7 +47,8 @@ int64_t tc_block_bytes(int64_t rows, int Q, int H, int side);
 cudaError_t launch_compress_tc(const float2 *rings, int64_t n, int R, int Q, const double *w, const double *U, int H,
                                int side, float *blocks, const double *kr, const double *shifts, int S, cudaStream_t s);
 cudaError_t launch_unpack_tc(const float *blocks, int64_t n, int Q, int H, int side, float2 *coeffs, cudaStream_t s);
-cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t rows, int Q, int H, int side);
+cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t rows, int Q, int H, int side,
+                                 int box_rows = 128);
 const float *tc_scales(const void *blocks, int64_t rows, int Q, int H, int side);
 cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int Nout, int64_t m0,
                                int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms,

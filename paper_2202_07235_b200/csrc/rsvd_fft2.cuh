@@ -56,6 +56,186 @@ __device__ __forceinline__ void z_pair(float2 a, float2 b, float2 w, float2 &zr,
     zm = c_add(make_float2(sv.x, -sv.y), make_float2(p.y, p.x));   // conj(s) + i conj(p)
 }
 
+// One work item (one template x 32 images) of a warp group: pass 1 straight from the item's landed
+// slot U, pass 2 and the fused output.  `release()` is called by every thread once the slot has been
+// read for the last time (its warps may then let the slot be refilled).  Images m_first + p,
+// p < n_valid, are real; t is the template index within the call (out.T columns, out.t_offset).
+template <int LOGN, int MODE, class Release>
+__device__ __forceinline__ void fft2_item(float *U, int gt, int warp, int lane, int gbar_id, const float2 *Wn,
+                                          const float2 *Wq, int64_t m_first, int n_valid, int64_t t, float st,
+                                          const uint32_t (&stale)[Fft2Cfg<LOGN>::P2_PER],
+                                          const float (&smv)[Fft2Cfg<LOGN>::P2_PER], const FftOut &out,
+                                          Release release) {
+    using C = Fft2Cfg<LOGN>;
+    constexpr int N = C::N, Q = C::Q, N1 = C::N1, N2 = C::N2, TB = C::TB, SZ = C::SZ, GT = C::GT;
+    float2 *ZY = reinterpret_cast<float2 *>(U);                           // [TB][SZ], in place after pass-1 reads
+    auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(gbar_id), "n"(GT) : "memory"); };
+    const float PI = 3.14159265358979323846f;
+    const int ca = warp == 0 ? 0 : warp;
+    const int cb = warp == 0 ? N1 / 2 : N1 - warp;
+
+    // ---- pass 1: Z from the ring, two DFTs of length N2
+    float2 za[N2], zb[N2];
+    auto ld = [&](int n) { return make_float2(U[n * TB + lane], U[(N + n) * TB + lane]); };
+    if (warp == 0) {
+        // column 0: rows N1*n2; pairs (n2, N2 - n2); n2 = 0 -> Z_0, n2 = N2/2 -> Z_{N/2}
+        {
+            const float2 u0 = ld(0);                                  // (U_0, U_N) packed
+            za[0] = make_float2(u0.x + u0.y, u0.x - u0.y);
+            const float2 uh = ld(N / 2);
+            za[N2 / 2] = make_float2(2.f * uh.x, 2.f * uh.y);
+#pragma unroll
+            for (int n2 = 1; n2 < N2 / 2; ++n2) z_pair(ld(N1 * n2), ld(N1 * (N2 - n2)), Wq[N1 * n2], za[n2], za[N2 - n2]);
+        }
+        // column N1/2: rows N1/2 + N1 n2; pairs (n2, N2 - 1 - n2)
+#pragma unroll
+        for (int n2 = 0; n2 < N2 / 2; ++n2) {
+            const int r = N1 / 2 + N1 * n2;
+            z_pair(ld(r), ld(N - r), Wq[r], zb[n2], zb[N2 - 1 - n2]);
+        }
+    } else {
+        // columns c and N1 - c: (c, n2) <-> (N1 - c, N2 - 1 - n2)
+#pragma unroll
+        for (int n2 = 0; n2 < N2 / 2; ++n2) {
+            const int ra = ca + N1 * n2, rb = cb + N1 * n2;
+            z_pair(ld(ra), ld(N - ra), Wq[ra], za[n2], zb[N2 - 1 - n2]);
+            z_pair(ld(rb), ld(N - rb), Wq[rb], zb[n2], za[N2 - 1 - n2]);
+        }
+    }
+    gbar();                                                // (A) every U read: slot becomes ZY
+    dif4<N2>(za);
+    dif4<N2>(zb);
+    {
+        float2 *ywa = ZY + lane * SZ + ca, *ywb = ZY + lane * SZ + cb;
+        const float2 *twa = Wn + ca * N2, *twb = Wn + cb * N2;
+#pragma unroll
+        for (int k1 = 0; k1 < N2; ++k1) {
+            float2 xa = za[dpos4<N2>(k1)], xb = zb[dpos4<N2>(k1)];
+            if (k1) {
+                xa = c_mul(xa, twa[k1]);
+                xb = c_mul(xb, twb[k1]);
+            }
+            ywa[k1 * C::SK] = xa;
+            ywb[k1 * C::SK] = xb;
+        }
+    }
+    gbar();                                                // (B) ZY complete
+
+    // ---- pass 2
+    float2 w[C::P2_PER][N1];
+#pragma unroll
+    for (int j = 0; j < C::P2_PER; ++j) {
+        const int task = gt + GT * j;
+        const int p = task / N2, k1 = task % N2;
+        const float2 *yr = ZY + p * SZ + k1 * C::SK;
+#pragma unroll
+        for (int i = 0; i < N1; ++i) w[j][i] = yr[i];
+    }
+    release();                                             // (C) this thread's reads of the slot are done
+#pragma unroll
+    for (int j = 0; j < C::P2_PER; ++j) dif4<N1>(w[j]);   // w[dpos4(k2)] = z[k1 + N2 k2]
+    if constexpr (MODE == MODE_LANDSCAPE) {
+#pragma unroll
+        for (int j = 0; j < C::P2_PER; ++j) {
+            const int task = gt + GT * j;
+            const int p = task / N2, k1 = task % N2;
+            if (p < n_valid) {
+                const float mul = PI / (smv[j] * st);
+                float2 *dst = reinterpret_cast<float2 *>(out.X + (m_first + p) * out.ld_m + t * out.ld_t);
+#pragma unroll
+                for (int k2 = 0; k2 < N1; ++k2) dst[k1 + N2 * k2] = c_scale(w[j][dpos4<N1>(k2)], mul);
+            }
+        }
+    } else {
+        // max over the pair: a balanced tree per task (short dependency chains), then the N2-lane
+        // butterfly with the tasks' shuffles interleaved
+        const unsigned gmask = N2 >= 32 ? 0xffffffffu
+                                        : (((1u << (N2 & 31)) - 1u) << ((threadIdx.x & 31) & ~(N2 - 1)));
+        float mx[C::P2_PER];
+#pragma unroll
+        for (int j = 0; j < C::P2_PER; ++j) {
+            float r[N1];
+#pragma unroll
+            for (int k2 = 0; k2 < N1; ++k2) r[k2] = fmaxf(w[j][k2].x, w[j][k2].y);
+#pragma unroll
+            for (int h = N1 / 2; h >= 1; h >>= 1)
+#pragma unroll
+                for (int k2 = 0; k2 < h; ++k2) r[k2] = fmaxf(r[k2], r[k2 + h]);
+            mx[j] = r[0];
+        }
+#pragma unroll
+        for (int off = N2 / 2; off >= 1; off >>= 1)
+#pragma unroll
+            for (int j = 0; j < C::P2_PER; ++j) mx[j] = fmaxf(mx[j], __shfl_xor_sync(gmask, mx[j], off));
+#pragma unroll
+        for (int j = 0; j < C::P2_PER; ++j) {
+            const int task = gt + GT * j;
+            const int p = task / N2, k1 = task % N2;
+            const bool valid = p < n_valid;
+            const int64_t m = m_first + p;
+            const float bv = (PI / (smv[j] * st)) * mx[j];
+            bool go = valid;
+            if constexpr (MODE == MODE_IMAGE) go = valid && ord_f32(bv) >= stale[j];
+            if (go) {                                      // uniform over the pair's lanes
+                int bk = 0x7fffffff;
+#pragma unroll
+                for (int k2 = N1 - 1; k2 >= 0; --k2) {     // descending: the smallest index wins
+                    const float2 z = w[j][dpos4<N1>(k2)];
+                    const int kx = 2 * (k1 + N2 * k2);
+                    if (z.y == mx[j]) bk = kx + 1;
+                    if (z.x == mx[j]) bk = kx;
+                }
+#pragma unroll
+                for (int off = N2 / 2; off >= 1; off >>= 1) bk = min(bk, __shfl_xor_sync(gmask, bk, off));
+                float gam = 0.f;
+                if constexpr (MODE == MODE_PAIR) {
+                    if (out.best_gamma) gam = parabolic_gamma<N1, N2, true>(w[j], k1, bk, mx[j], gmask);
+                }
+                if (k1 == 0) {
+                    if constexpr (MODE == MODE_PAIR) {
+                        out.best_val[m * out.T + t] = bv;
+                        out.best_k[m * out.T + t] = bk;
+                        if (out.best_gamma) out.best_gamma[m * out.T + t] = gam;
+                    } else {
+                        const uint32_t idx = (uint32_t)((out.t_offset + t) * Q + bk);
+                        const unsigned long long key =
+                            ((unsigned long long)ord_f32(bv) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
+                        atomicMax(out.best_key + m, key);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// per-image side data of an item's pass-2 tasks (image scale; MODE_IMAGE: the image's current key),
+// fetched before the item's data wait so its latency hides behind it
+template <int LOGN, int MODE>
+__device__ __forceinline__ void fft2_side(int gt, int64_t m_first, int n_valid, const FftOut &out,
+                                          uint32_t (&stale)[Fft2Cfg<LOGN>::P2_PER], float (&smv)[Fft2Cfg<LOGN>::P2_PER]) {
+    using C = Fft2Cfg<LOGN>;
+#pragma unroll
+    for (int j = 0; j < C::P2_PER; ++j) {
+        const int p = (gt + C::GT * j) / C::N2;
+        const bool ok = p < n_valid;
+        smv[j] = (ok && out.sc_m) ? __ldg(out.sc_m + m_first + p) : 1.f;
+        stale[j] = 0u;
+        if constexpr (MODE == MODE_IMAGE) stale[j] = ok ? (uint32_t)(__ldcg(out.best_key + m_first + p) >> 32) : 0u;
+    }
+}
+
+// shared tables of the transform: Wn[c][k1] = W_N^{c k1}, Wq[r] = W_Q^r (r < N/2)
+template <int LOGN>
+__device__ __forceinline__ void fft2_tables(float2 *Wn, float2 *Wq, int tid, int nthreads) {
+    using C = Fft2Cfg<LOGN>;
+    for (int i = tid; i < C::N; i += nthreads) Wn[i] = twiddle_N(i / C::N2, i % C::N2, C::N);
+    for (int i = tid; i < C::N / 2; i += nthreads) {
+        float sn, cs;
+        sincospif(2.0f * (float)i / (float)C::Q, &sn, &cs);
+        Wq[i] = make_float2(cs, -sn);
+    }
+}
+
 template <int LOGN, int MODE>
 __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                                int64_t m0, int64_t t0, int64_t mcv,
@@ -63,7 +243,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
                                                                                float *__restrict__ Upk, int64_t Mc,
                                                                                int64_t Tc) {
     using C = Fft2Cfg<LOGN>;
-    constexpr int N = C::N, Q = C::Q, N1 = C::N1, N2 = C::N2, TB = C::TB, SZ = C::SZ, G = C::G, GT = C::GT;
+    constexpr int N = C::N, TB = C::TB, G = C::G, GT = C::GT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // pointer arithmetic on the __shared__ array (not an integer round trip) keeps LDS/STS addressing
     unsigned char *base = smem_raw + ((1024u - (fr_smem(smem_raw) & 1023u)) & 1023u);
@@ -101,7 +281,6 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
                 : "memory");
         }
     };
-    auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(GT) : "memory"); };
 
     // PDL: the next chunk's contraction may be scheduled as SMs free up (it waits for us before
     // writing the workspace); our own input is the previous kernel's output, so wait for it first.
@@ -114,176 +293,53 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = tid; i < N; i += C::THREADS) Wn[i] = twiddle_N(i / N2, i % N2, N);
-    for (int i = tid; i < N / 2; i += C::THREADS) {
-        float sn, cs;
-        sincospif(2.0f * (float)i / (float)Q, &sn, &cs);
-        Wq[i] = make_float2(cs, -sn);
-    }
+    fft2_tables<LOGN>(Wn, Wq, tid, C::THREADS);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (tid == 0)
         for (int i = 0; i < C::NSLOT; ++i)
             if (item_of(i) < nitems) issue(i);
     __syncthreads();
 
-    const float PI = 3.14159265358979323846f;
-    // pass-1 columns of this warp
-    const int ca = warp == 0 ? 0 : warp;
-    const int cb = warp == 0 ? N1 / 2 : N1 - warp;
-    for (int i = g; item_of(i) < nitems; i += G) {
-        const int item = item_of(i), sl = i % C::NSLOT;
+    // item coordinates advance by G * grid items per iteration: carry instead of a division per item
+    const int step = G * grid, dtl = step / nmb, dmb = step - dtl * nmb;
+    int tl = item_of(g) / nmb, mbi = item_of(g) - tl * nmb;
+    // this thread's discard rows r = gt, gt + GT, ... (row stride Tc * Mc floats)
+    float *const dbase = Upk ? Upk + (int64_t)gt * Tc * Mc : nullptr;
+    const int64_t dstride = (int64_t)GT * Tc * Mc;
+    for (int i = g; item_of(i) < nitems; i += G, tl += dtl, mbi += dmb) {
+        if (mbi >= nmb) { mbi -= nmb; ++tl; }
+        const int sl = i % C::NSLOT;
         float *U = reinterpret_cast<float *>(base + (size_t)sl * C::SLOT);    // [ROWS][TB]
-        float2 *ZY = reinterpret_cast<float2 *>(U);                           // [TB][SZ], in place after pass-1 reads
-        const int tl = item / nmb, mb0 = (item - tl * nmb) * TB;
+        const int mb0 = mbi * TB;
         const int64_t t = t0 + tl;
         const float st = out.sc_t ? __ldg(out.sc_t + t) : 1.f;
-        // per-image side data of this item's pass-2 tasks, fetched now so its latency hides behind pass 1
-        uint32_t stale[C::P2_PER];                             // MODE_IMAGE: the image's current key
-        float smv[C::P2_PER];                                  // image operand scale (TC path)
-#pragma unroll
-        for (int j = 0; j < C::P2_PER; ++j) {
-            const int ml = mb0 + (gt + GT * j) / N2;
-            const bool ok = ml < mcv;
-            smv[j] = (ok && out.sc_m) ? __ldg(out.sc_m + m0 + ml) : 1.f;
-            stale[j] = 0u;
-            if constexpr (MODE == MODE_IMAGE) stale[j] = ok ? (uint32_t)(__ldcg(out.best_key + m0 + ml) >> 32) : 0u;
-        }
+        const int n_valid = (int)(mcv - mb0 < TB ? mcv - mb0 : TB);
+        uint32_t stale[C::P2_PER];
+        float smv[C::P2_PER];
+        fft2_side<LOGN, MODE>(gt, m0 + mb0, n_valid, out, stale, smv);
         while (tag[sl] != i) {}
         fr_mbar_wait(full + sl, (uint32_t)(i / C::NSLOT) & 1u);
         // the item's 2N spectrum rows (one 128-B line each: 32 images x fp32) are now in shared memory
         // and dead in HBM terms: drop them from L2 without write-back (the next chunk's contraction
         // rewrites every line before it is read again)
-        if (Upk) {
-            for (int r = gt; r < C::ROWS; r += GT)
-                asm volatile("discard.global.L2 [%0], 128;" ::"l"(Upk + ((int64_t)r * Tc + tl) * Mc + mb0) : "memory");
-        }
-
-        // ---- pass 1: Z from the ring, two DFTs of length N2
-        float2 za[N2], zb[N2];
-        auto ld = [&](int n) { return make_float2(U[n * TB + lane], U[(N + n) * TB + lane]); };
-        if (warp == 0) {
-            // column 0: rows N1*n2; pairs (n2, N2 - n2); n2 = 0 -> Z_0, n2 = N2/2 -> Z_{N/2}
-            {
-                const float2 u0 = ld(0);                                  // (U_0, U_N) packed
-                za[0] = make_float2(u0.x + u0.y, u0.x - u0.y);
-                const float2 uh = ld(N / 2);
-                za[N2 / 2] = make_float2(2.f * uh.x, 2.f * uh.y);
+        if (dbase) {
+            const float *pd = dbase + (int64_t)tl * Mc + mb0;
 #pragma unroll
-                for (int n2 = 1; n2 < N2 / 2; ++n2) z_pair(ld(N1 * n2), ld(N1 * (N2 - n2)), Wq[N1 * n2], za[n2], za[N2 - n2]);
+            for (int r = gt; r < C::ROWS; r += GT, pd += dstride)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(pd) : "memory");
+        }
+        // (C) one arrival per warp once its reads are done (release); only the group's issuing thread
+        // waits for all TASKS warps before refilling the slot NSLOT items ahead
+        auto release = [&]() {
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fr_smem(empty + sl)) : "memory");
+            if (gt == 0 && item_of(i + C::NSLOT) < nitems) {
+                fr_mbar_wait(empty + sl, (uint32_t)(i / C::NSLOT) & 1u);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(i + C::NSLOT);
             }
-            // column N1/2: rows N1/2 + N1 n2; pairs (n2, N2 - 1 - n2)
-#pragma unroll
-            for (int n2 = 0; n2 < N2 / 2; ++n2) {
-                const int r = N1 / 2 + N1 * n2;
-                z_pair(ld(r), ld(N - r), Wq[r], zb[n2], zb[N2 - 1 - n2]);
-            }
-        } else {
-            // columns c and N1 - c: (c, n2) <-> (N1 - c, N2 - 1 - n2)
-#pragma unroll
-            for (int n2 = 0; n2 < N2 / 2; ++n2) {
-                const int ra = ca + N1 * n2, rb = cb + N1 * n2;
-                z_pair(ld(ra), ld(N - ra), Wq[ra], za[n2], zb[N2 - 1 - n2]);
-                z_pair(ld(rb), ld(N - rb), Wq[rb], zb[n2], za[N2 - 1 - n2]);
-            }
-        }
-        gbar();                                                // (A) every U read: slot becomes ZY
-        dif4<N2>(za);
-        dif4<N2>(zb);
-        {
-            float2 *ywa = ZY + lane * SZ + ca, *ywb = ZY + lane * SZ + cb;
-            const float2 *twa = Wn + ca * N2, *twb = Wn + cb * N2;
-#pragma unroll
-            for (int k1 = 0; k1 < N2; ++k1) {
-                float2 xa = za[dpos4<N2>(k1)], xb = zb[dpos4<N2>(k1)];
-                if (k1) {
-                    xa = c_mul(xa, twa[k1]);
-                    xb = c_mul(xb, twb[k1]);
-                }
-                ywa[k1 * C::SK] = xa;
-                ywb[k1 * C::SK] = xb;
-            }
-        }
-        gbar();                                                // (B) ZY complete
-
-        // ---- pass 2
-        float2 w[C::P2_PER][N1];
-#pragma unroll
-        for (int j = 0; j < C::P2_PER; ++j) {
-            const int task = gt + GT * j;
-            const int p = task / N2, k1 = task % N2;
-            const float2 *yr = ZY + p * SZ + k1 * C::SK;
-#pragma unroll
-            for (int i = 0; i < N1; ++i) w[j][i] = yr[i];
-        }
-        // (C) this warp's reads of the slot are done: one arrival per warp (release); only the group's
-        // issuing thread waits for all TASKS warps before refilling the slot NSLOT items ahead, the
-        // other warps go straight on to pass 2
-        __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fr_smem(empty + sl)) : "memory");
-        if (gt == 0 && item_of(i + C::NSLOT) < nitems) {
-            fr_mbar_wait(empty + sl, (uint32_t)(i / C::NSLOT) & 1u);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(i + C::NSLOT);
-        }
-#pragma unroll
-        for (int j = 0; j < C::P2_PER; ++j) {
-            const int task = gt + GT * j;
-            const int p = task / N2, k1 = task % N2;
-            dif4<N1>(w[j]);                                    // w[dpos4(k2)] = z[k1 + N2 k2]
-            const int64_t ml = mb0 + p;
-            const bool valid = ml < mcv;
-            const int64_t m = m0 + ml;
-            const float mul = PI / (smv[j] * st);
-            if constexpr (MODE == MODE_LANDSCAPE) {
-                if (valid) {
-                    float2 *dst = reinterpret_cast<float2 *>(out.X + m * out.ld_m + t * out.ld_t);
-#pragma unroll
-                    for (int k2 = 0; k2 < N1; ++k2) {
-                        const float2 z = w[j][dpos4<N1>(k2)];
-                        dst[k1 + N2 * k2] = c_scale(z, mul);
-                    }
-                }
-            } else {
-                const unsigned gmask = N2 >= 32 ? 0xffffffffu
-                                                : (((1u << (N2 & 31)) - 1u) << ((threadIdx.x & 31) & ~(N2 - 1)));
-                float mx = -INFINITY;
-#pragma unroll
-                for (int k2 = 0; k2 < N1; ++k2) mx = fmaxf(mx, fmaxf(w[j][k2].x, w[j][k2].y));
-#pragma unroll
-                for (int off = N2 / 2; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, off));
-                const float bv = mul * mx;
-                bool go = valid;
-                if constexpr (MODE == MODE_IMAGE) go = valid && ord_f32(bv) >= stale[j];
-                if (go) {                                      // uniform over the pair's lanes
-                    int bk = 0x7fffffff;
-#pragma unroll
-                    for (int k2 = N1 - 1; k2 >= 0; --k2) {     // descending: the smallest index wins
-                        const float2 z = w[j][dpos4<N1>(k2)];
-                        const int kx = 2 * (k1 + N2 * k2);
-                        if (z.y == mx) bk = kx + 1;
-                        if (z.x == mx) bk = kx;
-                    }
-#pragma unroll
-                    for (int off = N2 / 2; off >= 1; off >>= 1) bk = min(bk, __shfl_xor_sync(gmask, bk, off));
-                    float gam = 0.f;
-                    if constexpr (MODE == MODE_PAIR) {
-                        if (out.best_gamma) gam = parabolic_gamma<N1, N2, true>(w[j], k1, bk, mx, gmask);
-                    }
-                    if (k1 == 0) {
-                        if constexpr (MODE == MODE_PAIR) {
-                            out.best_val[m * out.T + t] = bv;
-                            out.best_k[m * out.T + t] = bk;
-                            if (out.best_gamma) out.best_gamma[m * out.T + t] = gam;
-                        } else {
-                            const uint32_t idx = (uint32_t)((out.t_offset + t) * Q + bk);
-                            const unsigned long long key =
-                                ((unsigned long long)ord_f32(bv) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
-                            atomicMax(out.best_key + m, key);
-                        }
-                    }
-                }
-            }
-        }
+        };
+        fft2_item<LOGN, MODE>(U, gt, warp, lane, 1 + g, Wn, Wq, m0 + mb0, n_valid, t, st, stale, smv, out, release);
     }
 }
 

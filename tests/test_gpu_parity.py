@@ -94,7 +94,7 @@ def test_basis_parity_and_determinism():
         C_ref = ref.kernel_C(B, w)
         Ur, lr = ref.basis(C_ref, R)
         assert np.abs(lam - lr).max() <= 1e-12 * lr[0]
-        assert np.linalg.norm(C_ref @ U - U * lam[None, :]) <= 1e-11 * lr[0]
+        assert np.linalg.norm(C_ref @ U - U * lam[None, :]) <= 1e-12 * lr[0]
         # projector agreement on the non-null eigenspace up to each well-separated gap
         nz = int((lr > 1e-9 * lr[0]).sum())
         for h in range(1, nz):
@@ -103,7 +103,7 @@ def test_basis_parity_and_determinism():
                 continue
             P = U[:, :h] @ U[:, :h].T
             Pr = Ur[:, :h] @ Ur[:, :h].T
-            assert np.linalg.norm(P - Pr, 2) <= 1e-9 / relgap, (name, h, relgap)
+            assert np.linalg.norm(P - Pr, 2) <= 1e-10 / relgap, (name, h, relgap)
 
 
 def test_compress_parity():
@@ -390,7 +390,7 @@ def test_translation_averaged_basis():
     C_ref = ref.kernel_C(ref.translate(B, k, shifts), w)
     Ur, lr = ref.basis(C_ref, R)
     assert np.abs(lam - lr).max() <= 1e-12 * lr[0]
-    assert np.linalg.norm(C_ref @ U - U * lam[None, :]) <= 1e-11 * lr[0]
+    assert np.linalg.norm(C_ref @ U - U * lam[None, :]) <= 1e-12 * lr[0]
     nz = int((lr > 1e-9 * lr[0]).sum())
     for h in range(1, nz):
         relgap = (lr[h - 1] - lr[h]) / lr[0]
