@@ -43,11 +43,18 @@ UNIT = "pairs/s"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="large", choices=list(CONFIGS))
     p.add_argument("--H", type=int, default=None)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--mode", default=None, choices=["per_image", "per_pair", "landscape"],
+                   help="Step-4 output (default: the config's BASELINE mode -- per_image for Large, per_pair otherwise)")
+    p.add_argument("--traffic", default="auto", choices=["auto", "off"],
+                   help="measure the dominant kernel's DRAM bytes per launch with an ncu child run of the same "
+                        "workload (rank 0, N = 1)")
+    p.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
+    p.add_argument("--landscape-gb", type=float, default=8.0, help="landscape tile buffer (GB) for --mode landscape")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-kernel-timing", action="store_true", help="(diagnostic) no per-kernel CUDA events in the timed region")
@@ -185,11 +192,11 @@ def sum_over_ranks(x: float, world: int) -> float:
 
 
 # ------------------------------------------------------------------ oracle (cpu baseline / reference arm)
-def oracle_pairs_per_s(A, B, w, U, m, t, seconds: float):
+def oracle_pairs_per_s(A, B, w, U, m, t, seconds: float, threads: int | None = None):
     """Time the fp64 oracle (O2 direct sum, as it stands) on sampled pairs; grow the sample until
     it takes ~`seconds`.  Returns (pairs/s, pairs timed, threads, seconds)."""
     from oracle import ref
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
     n = 4
     while True:
         n = min(n, len(m))
@@ -203,6 +210,67 @@ def oracle_pairs_per_s(A, B, w, U, m, t, seconds: float):
 
 
 # ------------------------------------------------------------------ our arm
+DEFAULT_MODE = {"tiny": "per_pair", "small": "per_pair", "medium": "per_pair", "large": "per_image",
+                "translations": "per_pair"}
+TRAFFIC_KERNELS = {"fft_reduce": "fft2_reduce_kernel|fft_reduce_kernel", "contract": "contract_tc_kernel|contract_kernel"}
+
+
+def measure_traffic(args, kernel_key: str, timeout_s: int = 600):
+    """DRAM bytes per launch of one kernel family, from an ncu child run of this workload
+    (`bench.py --traffic-probe`: one warm-up step + one step, no timing).  ncu runs with
+    --cache-control none so the counts are the steady-state ones (a flushed L2 would charge every
+    spectrum read to DRAM).  Returns a dict or {"error": ...}."""
+    import csv
+    import shutil
+    import tempfile
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return {"error": "ncu not found"}
+    log = tempfile.NamedTemporaryFile(suffix=".csv", delete=False).name
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "--cache-control", "none", "-k", f"regex:{TRAFFIC_KERNELS[kernel_key]}",
+           "-s", "8", "-c", "6", "--csv", "--log-file", log,
+           sys.executable, os.path.abspath(__file__), "--traffic-probe", "--config", args.config,
+           "--mode", args.mode]
+    if args.H:
+        cmd += ["--H", str(args.H)]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s, env=env)
+        if r.returncode != 0:
+            return {"error": f"ncu exit {r.returncode}: {(r.stderr or r.stdout)[-200:]}"}
+        rows = [row for row in csv.reader(open(log)) if len(row) > 10]
+        hdr = rows[0]
+        ci = {h: i for i, h in enumerate(hdr)}
+        per = {}
+        for row in rows[1:]:
+            kid = row[ci["ID"]]
+            per.setdefault(kid, {})[row[ci["Metric Name"]]] = (float(row[ci["Metric Value"]].replace(",", "")),
+                                                                row[ci["Metric Unit"]])
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
+                 "msecond": 1e-3, "nsecond": 1e-9}
+        rd, wr, tm = [], [], []
+        for m in per.values():
+            v, u = m["dram__bytes_read.sum"]
+            rd.append(v * scale.get(u, 1))
+            v, u = m["dram__bytes_write.sum"]
+            wr.append(v * scale.get(u, 1))
+            v, u = m["gpu__time_duration.sum"]
+            tm.append(v * scale.get(u, 1e-9))
+        if not rd:
+            return {"error": "no launches profiled"}
+        return {"dram_read_per_launch": float(np.mean(rd)), "dram_write_per_launch": float(np.mean(wr)),
+                "launches": len(rd), "ncu_launch_ms": float(np.mean(tm) * 1e3),
+                "command": "ncu --metrics dram__bytes_{read,write}.sum --cache-control none (child run of this workload)"}
+    except Exception as exc:  # noqa: BLE001
+        return {"error": str(exc)[:200]}
+    finally:
+        try:
+            os.unlink(log)
+        except OSError:
+            pass
+
+
 def run_ours(args):
     from paper_2202_07235_b200 import api
     from paper_2202_07235_b200 import dist as pdist
@@ -212,6 +280,8 @@ def run_ours(args):
     cfg = CONFIGS[args.config]
     H = args.H or cfg["H"][0]
     Q, R = cfg["Q"], cfg["R"]
+    args.mode = args.mode or DEFAULT_MODE[args.config]
+    mode = args.mode
     chunk = api.kernel_chunk()
     T, M = cfg["T"], cfg["M"] * cfg.get("shifts", 1)
     # rank grid: GI image shards x GT template shards (dist.grid_shape); --shard templates = 1 x world
@@ -227,81 +297,111 @@ def run_ours(args):
     m0, m1 = pdist.image_range(M, GI, ri)
     images = ds.images[m0:m1].contiguous() if GI > 1 else ds.images
     tmpl = ds.templates
-    tmpl_basis = tmpl[b0 - t0:b1 - t0]
     M_loc = images.shape[0]
     T_loc = tmpl.shape[0]
     w_dev = ds.w.contiguous()
     if args.path:
         api.set_path({"simt": api.PATH_SIMT, "tc": api.PATH_TC, "auto": api.PATH_AUTO}[args.path])
     path = api.path_for(Q, H)
-    ib = torch.empty(max(api.block_bytes(M_loc, Q, H, api.SIDE_IMAGE), 16) // 4, dtype=torch.float32, device=dev)
     tb = torch.empty(max(api.block_bytes(T_loc, Q, H, api.SIDE_TEMPLATE), 16) // 4, dtype=torch.float32, device=dev)
-    wbytes = args.work_mb * (1 << 20) if args.work_mb else api.align_workspace_bytes(M_loc, T_loc, Q, H)
+    # landscape mode: the M x T x Q landscape is streamed to HBM in image blocks through one tile buffer
+    # (each block's rows compressed on their own: the block layout is per call)
+    if mode == "landscape":
+        per_img = max(T_loc, 1) * Q * 4
+        lblk = max(128, int(args.landscape_gb * 1e9 // per_img) // 128 * 128)
+        lblk = min(lblk, M_loc)
+        blocks = [(a, min(a + lblk, M_loc)) for a in range(0, M_loc, lblk)]
+        Xbuf = torch.empty((lblk, T_loc, Q), dtype=torch.float32, device=dev)
+    else:
+        blocks = [(0, M_loc)]
+        Xbuf = None
+    ibs = [torch.empty(max(api.block_bytes(e - a, Q, H, api.SIDE_IMAGE), 16) // 4, dtype=torch.float32, device=dev)
+           for a, e in blocks]
+    wbytes = args.work_mb * (1 << 20) if args.work_mb else api.align_workspace_bytes(blocks[0][1] - blocks[0][0], T_loc, Q, H)
     work = torch.empty(wbytes // 4, dtype=torch.float32, device=dev)
     keys = torch.zeros(M, dtype=torch.int64, device=dev)
+    if mode == "per_pair":
+        best_val = torch.empty((M_loc, T_loc), dtype=torch.float32, device=dev)
+        best_k = torch.empty((M_loc, T_loc), dtype=torch.int32, device=dev)
     U_dev = torch.zeros((R, H), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
-    ev = {}
 
-    def mark(name):
-        e = torch.cuda.Event(enable_timing=True)
-        e.record(stream)
-        ev[name] = e
-
-    def step(imgs, tmps, record=False):
-        if record:
-            mark("start")
+    def step(imgs, tmps, marks=None):
+        def mark(name):
+            if marks is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                marks.append((name, e))
+        mark("start")
         U, lam = pdist.basis_from_shards(tmps[b0 - t0:b1 - t0], T, w_dev, H, GI=GI)   # a0 (syncs for the host solve)
         U_dev.copy_(torch.from_numpy(U), non_blocking=False)
-        if record:
-            mark("basis")
-        if M_loc:
-            api.compress(imgs, w_dev, U_dev, api.SIDE_IMAGE, out=ib)  # a1
+        mark("basis")
+        for (a, e), ib in zip(blocks, ibs):                                        # a1
+            if e > a:
+                api.compress(imgs[a:e] if len(blocks) > 1 else imgs, w_dev, U_dev, api.SIDE_IMAGE, out=ib)
         if T_loc:
             api.compress(tmps, w_dev, U_dev, api.SIDE_TEMPLATE, out=tb)
-        if record:
-            mark("compress")
-        api.winners_reset(keys)                                       # a2-a4
-        if T_loc and M_loc:
-            api.align_argmax(ib, M_loc, tb, T_loc, Q, H, api.PER_IMAGE, work, best_key=keys[m0:m1], t_offset=t0)
-        if record:
+        mark("compress")
+        out = None
+        if mode == "per_image":                                                    # a2-a4
+            api.winners_reset(keys)
+            if T_loc and M_loc:
+                api.align_argmax(ibs[0], M_loc, tb, T_loc, Q, H, api.PER_IMAGE, work, best_key=keys[m0:m1], t_offset=t0)
             mark("align")
-        out = pdist.combine_keys(keys, Q)                             # all-gather + combine
-        if record:
-            mark("combine")
+            out = pdist.combine_keys(keys, Q)                                      # all-gather + combine
+        elif mode == "per_pair":
+            if T_loc and M_loc:
+                api.align_argmax(ibs[0], M_loc, tb, T_loc, Q, H, api.PER_PAIR, work, best_val=best_val, best_k=best_k)
+            mark("align")
+        else:
+            for (a, e), ib in zip(blocks, ibs):
+                if e > a and T_loc:
+                    api.align_landscape(ib, e - a, tb, T_loc, Q, H, work, X=Xbuf, ld_m=T_loc * Q, ld_t=Q)
+            mark("align")
+        mark("combine")
         return out, U
+
+    if args.traffic_probe:                      # child of measure_traffic: run under ncu, print nothing
+        step(images, tmpl)
+        step(images, tmpl)
+        torch.cuda.synchronize()
+        return
 
     for _ in range(args.warmup):
         step(images, tmpl)
     torch.cuda.synchronize()
     barrier(world)
+    # measured FP32 peak of this GPU (Pi_fp32 of SURVEY.md 8(d)), outside the timed region
+    fp32_meas = {k: api.probe_fp32(k) for k in ("ffma2", "ffma")}
 
     clocks = Clocks(local)
     clocks.start()
-    phase = {k: 0.0 for k in ["basis", "compress", "align", "combine"]}
     api.timing_read()
     api.timing_enable(False)
     n0 = api.launch_count()
     barrier(world)
     torch.cuda.synchronize()
-    # headline region: K steps, no events between launches (the align path chains its contraction /
+    # headline region: K steps, events only at step boundaries (the align path chains its contraction /
     # FFT launches with programmatic dependent launch; a per-launch event would serialise them)
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     start.record(stream)
-    last_U = None
+    step_marks = []
+    last_U, out = None, None
     for _ in range(args.steps):
-        out, last_U = step(images, tmpl, record=True)
+        mk = []
+        out, last_U = step(images, tmpl, marks=mk)
+        step_marks.append(mk)
     end.record(stream)
     torch.cuda.synchronize()
     elapsed_ms = start.elapsed_time(end)
     barrier(world)
     launches = api.launch_count() - n0
     clk = clocks.stop()
-    # per-phase of the last step
-    names = ["start", "basis", "compress", "align", "combine"]
-    for a, b in zip(names[:-1], names[1:]):
-        phase[b] = ev[a].elapsed_time(ev[b])
+    per_step = [mk[0][1].elapsed_time(nxt[0][1]) for mk, nxt in zip(step_marks[:-1], step_marks[1:])]
+    per_step.append(step_marks[-1][0][1].elapsed_time(end))
+    names = [n for n, _ in step_marks[-1]]
+    phase = {b: step_marks[-1][i][1].elapsed_time(step_marks[-1][i + 1][1]) for i, b in enumerate(names[1:])}
     # kernel-duration region: the same K steps again with a CUDA event pair on the launching stream
     # around every library launch (rsvd_timing_*), for the per-kernel roofline
     timing_steps = 0
@@ -314,6 +414,7 @@ def run_ours(args):
         timing_steps = args.steps
     ktime = api.timing_read()
     ms_step = max_over_ranks(elapsed_ms / args.steps, world)
+    ms_median = max_over_ranks(float(np.median(per_step)), world)
     launches_all = int(sum_over_ranks(launches, world))
     pairs = M * T
     value = pairs / (ms_step / 1e3)
@@ -321,20 +422,14 @@ def run_ours(args):
     # dominant-kernel roofline (the kernel with the larger measured share of the step)
     pk, pk_kind = peaks()
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-    fp32_peak = sm_count * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12      # TFLOP/s
+    fp32_nom = sm_count * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12      # TFLOP/s at max clock
+    fp32_peak = fp32_meas["ffma2"]                                                   # measured (FFMA2 probe)
     f16_peak = pk.get("bf16_tflops", 1656.1)                                        # fp16 dense = bf16 dense rate
     f_contr, f_fft = flops_per_pair(H, Q)
+    f_fft_strict = f_fft / 2.0                                                       # G18: c2r costs 2.5 Q log2 Q
     c_ms, c_n = ktime["contract"]
     f_ms, f_n = ktime["fft_reduce"]
     n_pairs_timed = max(timing_steps, 1) * M_loc * T_loc
-    traffic_all = {}
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            with open(tpath) as f:
-                traffic_all = json.load(f).get(args.config, {})
-        except Exception:
-            traffic_all = {}
     if c_ms >= f_ms:
         achieved = n_pairs_timed * f_contr / (c_ms / 1e3) / 1e12 if c_ms > 0 else None
         if path == api.PATH_TC:
@@ -345,24 +440,33 @@ def run_ours(args):
         else:
             peak, bound = fp32_peak, "alu"
             kname = "contract_kernel (Step 2, FP32 SIMT)"
-            note = (f"{sm_count} SMs x 128 FP32 lanes x 2 flop x {pk.get('sm_max_mhz', 1965.0):.0f} MHz "
-                    f"(sm_max_mhz from MEASURED_PEAKS.json, {pk_kind})")
-        k_ms, k_n, fpp, tkey = c_ms, c_n, f_contr, "contract_bytes_per_launch"
+            note = f"measured FFMA2 peak {fp32_peak:.1f} TF/s (rsvd_probe_fp32); nominal {fp32_nom:.1f} at max clock"
+        k_ms, k_n, fpp, tkey = c_ms, c_n, f_contr, "contract"
+        strict = None
     else:
         achieved = n_pairs_timed * f_fft / (f_ms / 1e3) / 1e12 if f_ms > 0 else None
         peak, bound = fp32_peak, "alu"
         kname = "fft2_reduce_kernel (Steps 3-4, FP32 SIMT)"
-        note = (f"{sm_count} SMs x 128 FP32 lanes x 2 flop x {pk.get('sm_max_mhz', 1965.0):.0f} MHz "
-                f"(sm_max_mhz from MEASURED_PEAKS.json, {pk_kind}); algorithmic 5 Q log2 Q per pair")
-        k_ms, k_n, fpp, tkey = f_ms, f_n, f_fft, "fft_bytes_per_launch"
+        note = (f"peak = measured sustained FFMA2 rate {fp32_peak:.2f} TF/s of this GPU (rsvd_probe_fp32, scalar "
+                f"FFMA {fp32_meas['ffma']:.1f}); nominal {fp32_nom:.1f} TF/s = {sm_count} SMs x 128 lanes x 2 x "
+                f"{pk.get('sm_max_mhz', 1965.0):.0f} MHz; algorithmic 5 Q log2 Q flops per pair")
+        k_ms, k_n, fpp, tkey = f_ms, f_n, f_fft, "fft_reduce"
+        strict = round(n_pairs_timed * f_fft_strict / (f_ms / 1e3) / 1e12 / fp32_peak, 4) if f_ms > 0 else None
+    traffic = None
+    if rank == 0 and world == 1 and args.traffic == "auto" and k_n > 0:
+        traffic = measure_traffic(args, tkey)
     roof = {"bound": bound, "kernel": kname,
             "achieved": round(achieved, 3) if achieved else None, "peak": round(peak, 2),
             "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if achieved else None,
-            "traffic": traffic_all.get(tkey), "peak_note": note,
+            "frac_nominal_peak": round(achieved / fp32_nom, 4) if (achieved and bound == "alu") else None,
+            "frac_strict_c2r": strict,
+            "traffic": (traffic["dram_read_per_launch"] + traffic["dram_write_per_launch"])
+            if traffic and "dram_read_per_launch" in traffic else None,
+            "traffic_detail": traffic, "peak_note": note,
             "avg_launch_ms": round(k_ms / max(k_n, 1), 4), "launches": k_n,
             "timing": f"CUDA events around every launch on its stream over a second {timing_steps}-step region",
             "algorithmic_flops_per_pair": fpp, "contraction_path": "tc" if path == api.PATH_TC else "simt"}
-    # The contraction against the L2 it actually saturates: per launch it writes the chunk's spectrum
+    # The contraction against the L2 it saturates: per launch it writes the chunk's spectrum
     # (pairs x Q/2 slots x 8 B) and reads the fp16 hi/lo operand rows ((Q/2 + 1) x KB x 2 B per pair for
     # 128 x 256 pair tiles); bound t = writes / BW_w + reads / BW_r with the L2 write / read bandwidths
     # measured by tools/l2_bw_probe.cu on this pool's B200s (profiles/r01s3_l2_bw_probe.txt).
@@ -381,20 +485,22 @@ def run_ours(args):
                     "peak_note": f"time-weighted L2 ceiling: write {L2_W:.0f} / read {L2_R:.0f} GB/s measured by "
                                  "tools/l2_bw_probe.cu (profiles/r01s3_l2_bw_probe.txt)"}
     pi_c = f16_peak / 3.0 if path == api.PATH_TC else fp32_peak
-    t_roof = pairs * (f_contr / pi_c + f_fft / fp32_peak) / 1e12 / world
+    land_bytes = float(M) * T * Q * 4 if mode == "landscape" else 0.0
+    hbm = pk.get("hbm_gbs", 6539.9) * 1e9
+    t_flop = pairs * (f_contr / pi_c + f_fft / fp32_peak) / 1e12 / world
+    t_roof = max(t_flop, land_bytes / hbm / world)
     ts = max(timing_steps, 1)
     step_roof = {"t_roof_ms": round(t_roof * 1e3, 3), "frac": round(t_roof * 1e3 / ms_step, 4),
-                 "definition": ("M*T*(8HQ/Pi_contr + 5Q log2 Q/Pi_fp32) / G vs the measured step, Pi_contr = "
-                                + ("fp16 dense/3 (3 MMAs per MAC)" if path == api.PATH_TC else "FP32 SIMT")
-                                + " (SURVEY.md 8(d))"),
-                 "kernel_ms_per_step": {"contract": round(c_ms / ts, 3),
-                                        "fft_reduce": round(f_ms / ts, 3),
-                                        "compress": round(ktime["compress"][0] / ts, 3),
-                                        "kernel_partials": round(ktime["kernel_partials"][0] / ts, 3)}}
+                 "frac_align_only": round(t_roof * 1e3 / max(phase.get("align", 0.0), 1e-9), 4),
+                 "definition": ("max(M*T*(8HQ/Pi_contr + 5Q log2 Q/Pi_fp32), landscape bytes/BW_HBM) / G vs the "
+                                "measured step, Pi_contr = " + ("fp16 dense/3 (3 MMAs per MAC)" if path == api.PATH_TC
+                                                                 else "Pi_fp32")
+                                + ", Pi_fp32 = measured FFMA2 peak (SURVEY.md 8(d))"),
+                 "kernel_ms_per_step": {k: round(v[0] / ts, 3) for k, v in ktime.items()}}
 
-    # e2e: host (pinned) rings -> device -> step -> winners back, through the public API
+    # e2e: host (pinned) rings -> device -> step -> winners back, through the public API (per-image mode)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and mode == "per_image":
         try:
             h_img = torch.empty(images.shape, dtype=images.dtype, pin_memory=True)
             h_tmp = torch.empty(tmpl.shape, dtype=tmpl.dtype, pin_memory=True)
@@ -433,8 +539,11 @@ def run_ours(args):
             del h_img, h_tmp, d_img, d_tmp
         except Exception as exc:  # host memory etc.
             e2e = {"value": None, "unit": UNIT, "error": str(exc)[:200]}
+    elif mode != "per_image":
+        e2e = {"value": None, "unit": UNIT, "reason": f"end-to-end line is measured for the per-image mode only "
+                                                      f"({mode} outputs are M x T{' x Q' if mode == 'landscape' else ''})"}
 
-    # cpu baseline: the oracle as it stands, rank 0 at N = 1 only
+    # cpu baseline: the oracle as it stands, rank 0 at N = 1 only, on all host cores and on one core
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         m, t = sample_pairs(args.config, M, T, 2048, 0)
@@ -442,21 +551,27 @@ def run_ours(args):
         rows_t, inv_t = np.unique(t, return_inverse=True)
         A = images[torch.as_tensor(rows_m, device=dev)].cpu().numpy()
         B = tmpl[torch.as_tensor(rows_t, device=dev)].cpu().numpy()
-        rate, n, thr, secs = oracle_pairs_per_s(A, B, ds.w.cpu().numpy(), last_U, inv_m, inv_t, args.cpu_seconds)
+        wn = ds.w.cpu().numpy()
+        rate, n, thr, secs = oracle_pairs_per_s(A, B, wn, last_U, inv_m, inv_t, args.cpu_seconds)
+        rate1, n1, _, secs1 = oracle_pairs_per_s(A, B, wn, last_U, inv_m, inv_t, max(2.0, args.cpu_seconds / 4), threads=1)
         cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "oracle",
                "sample": f"{n} seeded random (m,t) pairs of the {args.config} workload, O2 rank-{H} fp64 direct "
-                         f"sum (oracle/direct.c, OpenMP) + argmax, library U; {secs:.1f} s"}
+                         f"sum (oracle/direct.c, OpenMP) + argmax, library U; {secs:.1f} s",
+               "one_core": {"value": rate1, "unit": UNIT, "cores": 1, "sample": f"{n1} pairs, {secs1:.1f} s"}}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.config, "M": M, "T": T, "R": R, "Q": Q, "H": H, "mode": "per_image",
-                       "workspace_mb": round(wbytes / 2**20, 1), "parallelism": f"{GI} image x {GT} template shards on {world} GPU(s) (NCCL all-gather of winners)",
-                       "l2": "inputs larger than L2 (rings %.1f GB per step)" % ((images.numel() + T * R * Q) * 8 / 1e9),
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "ms_per_step_median": round(ms_median, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.config, "M": M, "T": T, "R": R, "Q": Q, "H": H, "mode": mode,
+                       "workspace_mb": round(wbytes / 2**20, 1),
+                       "parallelism": f"{GI} image x {GT} template shards on {world} GPU(s)"
+                                      + (" (NCCL all-gather of winners)" if mode == "per_image" else ""),
+                       "l2": "inputs larger than L2 (rings %.1f GB per step)" % ((images.numel() + T_loc * R * Q) * 8 / 1e9),
                        "seed": 220207235},
-            "roofline": roof, "contraction_l2": contr_l2, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "roofline": roof, "contraction_l2": contr_l2, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clk, "fp32_peak_measured_tflops": {k: round(v, 2) for k, v in fp32_meas.items()},
             "gpu_launches": launches_all, "phases_ms_last_step": {k: round(v, 3) for k, v in phase.items()},
             "gen_seconds": round(gen_s, 1),
         }
@@ -510,7 +625,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": args.config, "M": M, "T": T, "R": R, "Q": Q, "H": H, "mode": "per_image",
+        "config": {"workload": args.config, "M": M, "T": T, "R": R, "Q": Q, "H": H,
+                   "mode": args.mode or DEFAULT_MODE[args.config],
                    "parallelism": "host cores (OpenMP over pairs)", "seed": 220207235},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
                          "sample": f"{n_step} seeded random (m,t) pairs of the workload per step: O2 rank-{H} fp64 "
