@@ -715,8 +715,10 @@ cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, i
     }
     const int mtl = (int)(mc / TC_PIMG), ntl = (int)(tc / TC_TT);
     const int ntiles = mtl * ntl;
+    // q-groups per tile: as many as fit the CTA pairs of one wave (floor, so that every pair gets at
+    // most one (tile, q-group) item -- a ceiling here gave a few pairs two items and doubled the launch)
     const int target = std::max(1, nsms / 2);
-    int nqg = std::max(1, (target + ntiles - 1) / ntiles);
+    int nqg = std::max(1, target / std::max(1, ntiles));
     nqg = std::min(nqg, N + 1);
     const int qg = (N + 1 + nqg - 1) / nqg;
     nqg = (N + 1 + qg - 1) / qg;
