@@ -55,6 +55,9 @@ def parse():
                         "workload (rank 0, N = 1)")
     p.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     p.add_argument("--landscape-gb", type=float, default=8.0, help="landscape tile buffer (GB) for --mode landscape")
+    p.add_argument("--ctf-groups", type=int, default=0,
+                   help="row f3: split the images into G CTF groups (toy radial CTFs), one basis per group from "
+                        "one kernel pass, templates compressed per group, one grouped align call (per-image mode)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-kernel-timing", action="store_true", help="(diagnostic) no per-kernel CUDA events in the timed region")
@@ -326,7 +329,51 @@ def run_ours(args):
     U_dev = torch.zeros((R, H), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
 
+    G_ctf = args.ctf_groups if mode == "per_image" else 0
+    if G_ctf:
+        # row f3 input model: images of group g carry the toy CTF c_g (applied once, outside the timed
+        # region -- it is the data, not the method); group g = images [gb[g], gb[g+1])
+        from synth import toy_ctf
+        kk = ds.k.cpu().numpy()
+        ctfs = np.stack([toy_ctf(kk, 0.01 + 0.01 * g) for g in range(G_ctf)])
+        gb = [(M_loc * g // G_ctf) // 128 * 128 for g in range(G_ctf)] + [M_loc]
+        images = images.clone()
+        for g in range(G_ctf):
+            images[gb[g]:gb[g + 1]] *= torch.tensor(ctfs[g], dtype=images.dtype, device=dev)[None, :, None]
+        ibs_g = [torch.empty(max(api.block_bytes(gb[g + 1] - gb[g], Q, H, api.SIDE_IMAGE), 16) // 4,
+                             dtype=torch.float32, device=dev) for g in range(G_ctf)]
+        tbs_g = [torch.empty(max(api.block_bytes(T_loc, Q, H, api.SIDE_TEMPLATE), 16) // 4, dtype=torch.float32,
+                             device=dev) for g in range(G_ctf)]
+
+    def step_grouped(imgs, tmps, marks=None):
+        def mark(name):
+            if marks is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                marks.append((name, e))
+        mark("start")
+        C = pdist.kernel_from_shards(tmps[b0 - t0:b1 - t0], T, w_dev, GI=GI).cpu().numpy()      # one kernel pass
+        bases = [api.eigen_basis_ctf(C, ctfs[g], H) for g in range(G_ctf)]
+        mark("basis")
+        groups = []
+        for g, (Ug, Utg, _) in enumerate(bases):
+            a, e = gb[g], gb[g + 1]
+            api.compress(imgs[a:e], w_dev, torch.as_tensor(Ug, device=dev), api.SIDE_IMAGE, out=ibs_g[g])
+            api.compress(tmps, w_dev, torch.as_tensor(Utg, device=dev), api.SIDE_TEMPLATE, out=tbs_g[g])
+            groups.append(dict(img_blocks=ibs_g[g], M=e - a, tmpl_blocks=tbs_g[g], T=T_loc, t_offset=t0,
+                               best_key=keys[m0 + a:m0 + e]))
+        mark("compress")
+        api.winners_reset(keys)
+        api.align_argmax_grouped(groups, Q, H, api.PER_IMAGE, work)
+        mark("align")
+        out = pdist.combine_keys(keys, Q)
+        mark("combine")
+        return out, bases[0][0]
+
     def step(imgs, tmps, marks=None):
+        if G_ctf:
+            return step_grouped(imgs, tmps, marks)
+
         def mark(name):
             if marks is not None:
                 e = torch.cuda.Event(enable_timing=True)
@@ -500,7 +547,7 @@ def run_ours(args):
 
     # e2e: host (pinned) rings -> device -> step -> winners back, through the public API (per-image mode)
     e2e = None
-    if not args.no_e2e and mode == "per_image":
+    if not args.no_e2e and mode == "per_image" and not G_ctf:
         try:
             h_img = torch.empty(images.shape, dtype=images.dtype, pin_memory=True)
             h_tmp = torch.empty(tmpl.shape, dtype=tmpl.dtype, pin_memory=True)
@@ -539,13 +586,15 @@ def run_ours(args):
             del h_img, h_tmp, d_img, d_tmp
         except Exception as exc:  # host memory etc.
             e2e = {"value": None, "unit": UNIT, "error": str(exc)[:200]}
+    elif G_ctf:
+        e2e = {"value": None, "unit": UNIT, "reason": "end-to-end line is measured for the plain per-image path"}
     elif mode != "per_image":
         e2e = {"value": None, "unit": UNIT, "reason": f"end-to-end line is measured for the per-image mode only "
                                                       f"({mode} outputs are M x T{' x Q' if mode == 'landscape' else ''})"}
 
     # cpu baseline: the oracle as it stands, rank 0 at N = 1 only, on all host cores and on one core
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not G_ctf:
         m, t = sample_pairs(args.config, M, T, 2048, 0)
         rows_m, inv_m = np.unique(m, return_inverse=True)
         rows_t, inv_t = np.unique(t, return_inverse=True)
@@ -564,7 +613,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "ms_per_step_median": round(ms_median, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.config, "M": M, "T": T, "R": R, "Q": Q, "H": H, "mode": mode,
+            "config": {"workload": args.config + (f"+ctf{G_ctf}" if G_ctf else ""), "M": M, "T": T, "R": R, "Q": Q,
+                       "H": H, "mode": mode, "ctf_groups": G_ctf or None,
                        "workspace_mb": round(wbytes / 2**20, 1),
                        "parallelism": f"{GI} image x {GT} template shards on {world} GPU(s)"
                                       + (" (NCCL all-gather of winners)" if mode == "per_image" else ""),

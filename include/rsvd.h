@@ -207,6 +207,28 @@ rsvd_status rsvd_align_landscape(const void *img_blocks, int64_t M, const void *
                                  int64_t T, int32_t Q, int32_t H, void *work, int64_t work_bytes,
                                  float *X, int64_t ld_m, int64_t ld_t, rsvd_stream_t stream);
 
+/* ------------------------------------------------------------------ row f3: CTF-grouped align
+ * The paper builds "the objective-function and kernel for each CTF separately" over the
+ * micrograph groups of its example (:715) and repeats precompute steps 1-3 per CTF (:781).  One call
+ * aligns G independent groups g: the group's images (compressed with its basis U_g from
+ * rsvd_eigen_basis_ctf) against its CTF-corrected targets (the raw templates compressed with
+ * diag(c_g) U_g), with exactly the semantics, outputs and errors of rsvd_align_argmax per group
+ * (PER_PAIR: best_val/best_k [M_g][T_g]; PER_IMAGE: best_key [M_g], t_offset per group).  Every group
+ * descriptor is validated before any work is enqueued; the groups run back to back on `stream` and
+ * share `work`.  groups: HOST array of G descriptors (device pointers inside). */
+typedef struct {
+    const void *img_blocks;   /* rsvd_compress(side=IMAGE, n=M) with the group's U_g */
+    int64_t M;
+    const void *tmpl_blocks;  /* rsvd_compress(side=TEMPLATE, n=T) with diag(c_g) U_g */
+    int64_t T;
+    int64_t t_offset;         /* PER_IMAGE: global index of the group's first template */
+    float *best_val;          /* PER_PAIR outputs (device) */
+    int32_t *best_k;
+    uint64_t *best_key;       /* PER_IMAGE outputs (device, rsvd_winners_reset first) */
+} rsvd_align_group;
+rsvd_status rsvd_align_argmax_grouped(const rsvd_align_group *groups, int32_t G, int32_t Q, int32_t H,
+                                      rsvd_reduce mode, void *work, int64_t work_bytes, rsvd_stream_t stream);
+
 /* ------------------------------------------------------------------ row f1: finer gamma (NEXT)
  * "If a finer resolution in gamma is required then the array [of Fourier coefficients] can be
  * zero-padded prior to the FFT".  Same as rsvd_align_argmax / rsvd_align_landscape

@@ -41,6 +41,7 @@ SIGNATURES = [
     ("rsvd_align_argmax", _I32, [_P, _I64, _P, _I64, _I64, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P]),
     ("rsvd_align_landscape", _I32, [_P, _I64, _P, _I64, _I32, _I32, _P, _I64, _P, _I64, _I64, _P]),
     ("rsvd_align_argmax_fine", _I32, [_P, _I64, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P, _P]),
+    ("rsvd_align_argmax_grouped", _I32, [_P, _I32, _I32, _I32, _I32, _P, _I64, _P]),
     ("rsvd_align_landscape_fine", _I32, [_P, _I64, _P, _I64, _I32, _I32, _I32, _P, _I64, _P, _I64, _I64, _P]),
     ("rsvd_winners_reset", _I32, [_P, _I64, _P]),
     ("rsvd_winners_unpack", _I32, [_P, _I64, _I32, _P, _P, _P, _P]),
@@ -57,6 +58,13 @@ SIGNATURES = [
     ("rsvd_vol_degrees", _I32, [_P, _I64, _P, _I32, _I32, _P, _I32, _P, _P]),
     ("rsvd_vol_align", _I32, [_P, _I64, _P, _I32, _I32, _I32, _I32, _P, _P, _P]),
 ]
+
+
+class AlignGroup(ctypes.Structure):
+    """rsvd_align_group (include/rsvd.h, row f3)."""
+    _fields_ = [("img_blocks", ctypes.c_void_p), ("M", ctypes.c_int64), ("tmpl_blocks", ctypes.c_void_p),
+                ("T", ctypes.c_int64), ("t_offset", ctypes.c_int64), ("best_val", ctypes.c_void_p),
+                ("best_k", ctypes.c_void_p), ("best_key", ctypes.c_void_p)]
 
 
 class RsvdError(RuntimeError):

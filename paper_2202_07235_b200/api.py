@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import PER_IMAGE, PER_PAIR, SIDE_IMAGE, SIDE_TEMPLATE, RsvdError, check, ptr, require_cuda, stream_handle
 
 __all__ = ["block_bytes", "path_for", "set_path", "PATH_AUTO", "PATH_SIMT", "PATH_TC", "kernel_chunk", "kernel_partials_bytes", "align_workspace_bytes",
-           "align_min_workspace_bytes", "kernel_partials", "kernel_reduce", "eigen_basis", "eigen_basis_ctf", "ctf_group_bases", "build_basis",
+           "align_min_workspace_bytes", "kernel_partials", "kernel_reduce", "eigen_basis", "eigen_basis_ctf", "ctf_group_bases", "align_argmax_grouped", "build_basis",
            "build_basis_translated", "compress", "compress_translated", "blocks_unpack", "align_argmax", "align_landscape", "align_argmax_fine",
            "align_landscape_fine", "winners_reset",
            "winners_unpack", "combine_winners", "launch_count", "timing_enable", "timing_read", "Aligner", "RsvdError", "PER_PAIR", "PER_IMAGE",
@@ -207,6 +207,39 @@ def align_argmax(img_blocks, M: int, tmpl_blocks, T: int, Q: int, H: int, mode: 
                                        ptr(work), work.numel() * work.element_size(), ptr(best_val),
                                        ptr(best_k), ptr(best_key), stream_handle(stream)))
     return (best_val, best_k) if mode == PER_PAIR else best_key
+
+
+def align_argmax_grouped(groups, Q: int, H: int, mode: int, work, stream=None):
+    """Row f3, rsvd_align_argmax_grouped: G independent CTF groups in one call.  groups: list of dicts
+    with img_blocks, M, tmpl_blocks, T and optionally t_offset / best_val / best_k (PER_PAIR) /
+    best_key (PER_IMAGE; reset by the caller).  Missing outputs are allocated; returns the list of
+    (best_val, best_k) or best_key per group."""
+    require_cuda(work)
+    arr = (_lib.AlignGroup * max(len(groups), 1))()
+    outs = []
+    for i, g in enumerate(groups):
+        require_cuda(g["img_blocks"], g["tmpl_blocks"])
+        dev = g["img_blocks"].device
+        M, T = int(g["M"]), int(g["T"])
+        if mode == PER_PAIR:
+            bv = g.get("best_val")
+            bk = g.get("best_k")
+            bv = torch.empty((M, T), dtype=torch.float32, device=dev) if bv is None else bv
+            bk = torch.empty((M, T), dtype=torch.int32, device=dev) if bk is None else bk
+            require_cuda(bv, bk)
+            outs.append((bv, bk))
+            key = None
+        else:
+            key = g.get("best_key")
+            key = torch.zeros(M, dtype=torch.int64, device=dev) if key is None else key
+            require_cuda(key)
+            outs.append(key)
+            bv = bk = None
+        arr[i] = _lib.AlignGroup(ptr(g["img_blocks"]), M, ptr(g["tmpl_blocks"]), T, int(g.get("t_offset", 0)),
+                                 ptr(bv), ptr(bk), ptr(key))
+    check(_lib.lib().rsvd_align_argmax_grouped(ctypes.addressof(arr), len(groups), Q, H, mode, ptr(work),
+                                               work.numel() * work.element_size(), stream_handle(stream)))
+    return outs
 
 
 def align_landscape(img_blocks, M: int, tmpl_blocks, T: int, Q: int, H: int, work, X=None,

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <string>
 
 #include "rsvd_common.cuh"
 #include "rsvd_fft.cuh"
@@ -379,6 +380,40 @@ extern "C" rsvd_status rsvd_align_argmax(const void *img_blocks, int64_t M, cons
                                          rsvd_stream_t stream) {
     return rsvd_align_argmax_fine(img_blocks, M, tmpl_blocks, T, t_offset, Q, H, Q, mode, work, work_bytes, best_val,
                                   best_k, best_key, nullptr, stream);
+}
+
+// Row f3: G independent (image-group, CTF-corrected template) problems in one call.  All groups are
+// validated first (no partial enqueue on a bad descriptor), then run back to back on the stream.
+extern "C" rsvd_status rsvd_align_argmax_grouped(const rsvd_align_group *groups, int32_t G, int32_t Q, int32_t H,
+                                                 rsvd_reduce mode, void *work, int64_t work_bytes,
+                                                 rsvd_stream_t stream) {
+    if (G < 0) return fail(RSVD_ERR_ARG, "G must be >= 0");
+    if (G == 0) return RSVD_OK;
+    if (!groups) return fail(RSVD_ERR_ARG, "NULL group array");
+    if (mode != RSVD_PER_PAIR && mode != RSVD_PER_IMAGE) return fail(RSVD_ERR_ARG, "bad mode");
+    for (int g = 0; g < G; ++g) {
+        const rsvd_align_group &d = groups[g];
+        rsvd_status st = check_common(d.img_blocks, d.M, d.tmpl_blocks, d.T, Q, H, work, work_bytes);
+        if (st != RSVD_OK) return fail(st, "group " + std::to_string(g) + ": " + rsvd_last_error());
+        if (d.M == 0 || d.T == 0) continue;
+        if (mode == RSVD_PER_PAIR && (!d.best_val || !d.best_k))
+            return fail(RSVD_ERR_ARG, "group " + std::to_string(g) + ": PER_PAIR needs best_val and best_k");
+        if (mode == RSVD_PER_IMAGE) {
+            if (!d.best_key) return fail(RSVD_ERR_ARG, "group " + std::to_string(g) + ": PER_IMAGE needs best_key");
+            if (d.t_offset < 0 || (uint64_t)(d.t_offset + d.T) * (uint64_t)Q >= 0xFFFFFFFFull)
+                return fail(RSVD_ERR_UNSUPPORTED, "group " + std::to_string(g) + ": (t_offset + T) * Q must be < 2^32");
+        }
+    }
+    for (int g = 0; g < G; ++g) {
+        const rsvd_align_group &d = groups[g];
+        if (d.M == 0 || d.T == 0) continue;
+        AlignArgs a{reinterpret_cast<const float2 *>(d.img_blocks), reinterpret_cast<const float2 *>(d.tmpl_blocks),
+                    d.M, d.T, d.t_offset, Q, H, mode == RSVD_PER_PAIR ? MODE_PAIR : MODE_IMAGE, work, work_bytes,
+                    d.best_val, d.best_k, reinterpret_cast<unsigned long long *>(d.best_key), nullptr, 0, 0, Q, nullptr};
+        const rsvd_status st = run_align(a, (cudaStream_t)stream);
+        if (st != RSVD_OK) return st;
+    }
+    return RSVD_OK;
 }
 
 extern "C" rsvd_status rsvd_align_landscape_fine(const void *img_blocks, int64_t M, const void *tmpl_blocks,

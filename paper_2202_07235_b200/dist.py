@@ -99,16 +99,22 @@ def gather_keys(keys: torch.Tensor, group=None) -> torch.Tensor:
     return _all_gather_equal(keys, group)
 
 
-def basis_from_shards(tmpl_shard: torch.Tensor, T_total: int, w_dev: torch.Tensor, H: int, group=None, GI: int = 1):
-    """Rows a0 across ranks: (U [R, H], lambda [R]) identical on every rank and for any world size.
-    tmpl_shard: this rank's basis sub-shard (basis_range)."""
+def kernel_from_shards(tmpl_shard: torch.Tensor, T_total: int, w_dev: torch.Tensor, group=None, GI: int = 1):
+    """Row a0 across ranks: the kernel C (device fp64 [R, R]), bitwise identical on every rank and for
+    any world size.  tmpl_shard: this rank's basis sub-shard (basis_range)."""
     from . import api
     Q = tmpl_shard.shape[2]
     chunk = api.kernel_chunk()
     part = api.kernel_partials(tmpl_shard)
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         part = gather_chunk_partials(part, T_total, chunk, group, GI)
-    C = api.kernel_reduce(part, T_total, Q, w_dev)
+    return api.kernel_reduce(part, T_total, Q, w_dev)
+
+
+def basis_from_shards(tmpl_shard: torch.Tensor, T_total: int, w_dev: torch.Tensor, H: int, group=None, GI: int = 1):
+    """Rows a0 across ranks: (U [R, H], lambda [R]) identical on every rank and for any world size."""
+    from . import api
+    C = kernel_from_shards(tmpl_shard, T_total, w_dev, group, GI)
     return api.eigen_basis(C.cpu().numpy(), H)
 
 

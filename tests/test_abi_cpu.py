@@ -1,6 +1,7 @@
 """CPU-only checks of the C ABI: the library builds for sm_100a, loads, exports every symbol that
 include/rsvd.h declares (and the binding declares them all), and its host-only entry points
 (sizes, the fp64 eigen-solver, argument validation that fails before any launch) behave."""
+import ctypes
 import os
 import re
 
@@ -133,3 +134,17 @@ def test_eigen_solver_top_h_path(lib):
             w, V = np.linalg.eigh(C)
             V = V[:, ::-1]
             assert np.abs(U[:, :k] @ U[:, :k].T - V[:, :k] @ V[:, :k].T).max() <= 1e-9
+
+
+def test_grouped_align_validates_before_any_launch(lib):
+    """rsvd_align_argmax_grouped (row f3) rejects bad descriptors with a status code and a message
+    before enqueuing anything (no GPU needed: validation precedes every launch)."""
+    from paper_2202_07235_b200 import _lib
+    arr = (_lib.AlignGroup * 2)()
+    arr[0] = _lib.AlignGroup(None, 8, None, 8, 0, None, None, None)
+    assert lib.rsvd_align_argmax_grouped(ctypes.addressof(arr), -1, 64, 4, 0, None, 0, None) == 1
+    assert lib.rsvd_align_argmax_grouped(None, 1, 64, 4, 0, None, 0, None) == 1
+    assert lib.rsvd_align_argmax_grouped(ctypes.addressof(arr), 1, 64, 4, 0, None, 0, None) == 1
+    assert b"group 0" in lib.rsvd_last_error()
+    assert lib.rsvd_align_argmax_grouped(ctypes.addressof(arr), 1, 48, 4, 0, None, 0, None) == 2   # Q not a power of 2
+    assert lib.rsvd_align_argmax_grouped(ctypes.addressof(arr), 0, 64, 4, 0, None, 0, None) == 0

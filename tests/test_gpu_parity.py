@@ -431,6 +431,45 @@ def test_ctf_group_bases_end_to_end():
         assert np.abs(X[m, t] - X_ref).max() <= TOL_FP32 * np.abs(X_ref).max()
 
 
+def test_ctf_grouped_align_three_groups():
+    """Row f3, rsvd_align_argmax_grouped: three CTF groups (images of group g carry c_g; targets are the
+    raw templates compressed with diag(c_g) U_g) in ONE call, PER_PAIR and PER_IMAGE, against the
+    oracle's rank-H landscape of (images_g, c_g * templates) through U_g on all pairs, and bitwise
+    equal to three separate rsvd_align_argmax calls."""
+    from synth import toy_ctf
+    G, Mg = 3, 40
+    d = make_dataset("small", M=G * Mg, T=72, device="cuda")
+    H, Q = 8, d.Q
+    k = to_np(d.k)
+    ctfs = np.stack([toy_ctf(k, lam) for lam in (0.015, 0.025, 0.04)])
+    w = d.w.contiguous()
+    bases = api.ctf_group_bases(d.templates, w, ctfs, H)
+    T = d.templates.shape[0]
+    work = torch.empty(api.align_workspace_bytes(Mg, T, Q, H) // 4, dtype=torch.float32, device="cuda")
+    B = to_np(d.templates)
+    groups, refs = [], []
+    for g, (U, Ut, lam) in enumerate(bases):
+        c = torch.tensor(ctfs[g], dtype=torch.complex64, device="cuda")
+        imgs = (d.images[g * Mg:(g + 1) * Mg] * c[None, :, None]).contiguous()
+        ib = api.compress(imgs, w, cuda(U, torch.float64), api.SIDE_IMAGE)
+        tb = api.compress(d.templates, w, cuda(Ut, torch.float64), api.SIDE_TEMPLATE)
+        groups.append(dict(img_blocks=ib, M=Mg, tmpl_blocks=tb, T=T, t_offset=g * T))
+        ia, it = _all_pairs(Mg, T)
+        Bg = B.astype(np.complex128) * ctfs[g][None, :, None]
+        refs.append(ref.landscape_rank(to_np(imgs), Bg, to_np(w), U, ia, it).real.reshape(Mg, T, Q))
+    outs = api.align_argmax_grouped(groups, Q, H, api.PER_PAIR, work)
+    keys = api.align_argmax_grouped(groups, Q, H, api.PER_IMAGE, work)
+    for g, ((val, kk), key, X_ref) in enumerate(zip(outs, keys, refs)):
+        tol_abs = TOL_FP32 * np.abs(X_ref).max()
+        assert np.abs(to_np(val) - X_ref.max(-1)).max() <= tol_abs
+        assert_argmax_gated(to_np(kk).ravel(), X_ref.reshape(-1, Q), tol_abs)
+        v1, k1 = api.align_argmax(groups[g]["img_blocks"], Mg, groups[g]["tmpl_blocks"], T, Q, H, api.PER_PAIR, work)
+        assert torch.equal(v1, val) and torch.equal(k1, kk)
+        vi, ti, ki = (to_np(x) for x in api.winners_unpack(key, Q))
+        assert np.all((ti >= g * T) & (ti < (g + 1) * T))
+        assert_per_image(vi, ti - g * T, ki, X_ref, tol_abs)
+
+
 def test_closed_form_translation_kernel_matches_oracle():
     """Row f2, closed form: rsvd_kernel_translated_sh vs the oracle T1 at several
     translation widths, then the basis from it through rsvd_eigen_basis vs the oracle's on the
