@@ -497,3 +497,46 @@ def test_closed_form_translation_kernel_matches_oracle():
         assert np.abs(U[:, :h] @ U[:, :h].T - Ur[:, :h] @ Ur[:, :h].T).max() <= 1e-8
     with pytest.raises(api.RsvdError):
         api.kernel_translated_sh(Bd, kd, wd, -1.0)
+
+
+@pytest.mark.parametrize("path", ["tc", "simt", "fused"])
+def test_repeat_runs_bitwise_identical(path, monkeypatch):
+    """Race-detection proxy (compute-sanitizer is closed on this pool): the same align call repeated
+    20 times on the same inputs gives bitwise identical per-pair values/indices, landscapes and
+    per-image keys.  A shared-memory or mbarrier race in the contraction / transform pipelines shows
+    up as run-to-run differences at these sizes (several chunks, ragged tails, many CTAs per SM
+    pipeline).  "fused": the persistent one-launch kernel (RSVD_FUSED=1), which must also reproduce
+    the two-kernel TC path bit for bit (same K order per (pair, q), same transform code)."""
+    api.set_path(api.PATH_SIMT if path == "simt" else api.PATH_TC)
+    ref_out = None
+    if path == "fused":
+        monkeypatch.setenv("RSVD_FUSED", "0")
+    try:
+        d = make_dataset("small", M=300, T=260, device="cuda")
+        w = d.w.contiguous()
+        U, _ = api.build_basis(d.templates, w.cpu().numpy(), 8)
+        Ud = cuda(U, torch.float64)
+        M, T, Q = 300, 260, d.Q
+        ib = api.compress(d.images, w, Ud, api.SIDE_IMAGE)
+        tb = api.compress(d.templates, w, Ud, api.SIDE_TEMPLATE)
+        work = torch.empty(api.align_min_workspace_bytes(Q) // 4, dtype=torch.float32, device="cuda")
+        if path == "fused":
+            ref_out = (api.align_argmax(ib, M, tb, T, Q, 8, api.PER_PAIR, work),
+                       api.align_landscape(ib, M, tb, T, Q, 8, work))
+            monkeypatch.setenv("RSVD_FUSED", "1")
+            work = torch.empty(api.align_workspace_bytes(M, T, Q, 8) // 4, dtype=torch.float32, device="cuda")
+        v0, k0 = api.align_argmax(ib, M, tb, T, Q, 8, api.PER_PAIR, work)
+        X0 = api.align_landscape(ib, M, tb, T, Q, 8, work)
+        key0 = api.align_argmax(ib, M, tb, T, Q, 8, api.PER_IMAGE, work)
+        for _ in range(20):
+            v, k = api.align_argmax(ib, M, tb, T, Q, 8, api.PER_PAIR, work)
+            X = api.align_landscape(ib, M, tb, T, Q, 8, work)
+            key = api.align_argmax(ib, M, tb, T, Q, 8, api.PER_IMAGE, work)
+            assert torch.equal(v, v0) and torch.equal(k, k0)
+            assert torch.equal(X, X0)
+            assert torch.equal(key, key0)
+        if ref_out is not None:
+            assert torch.equal(ref_out[0][0], v0) and torch.equal(ref_out[0][1], k0)
+            assert torch.equal(ref_out[1], X0)
+    finally:
+        api.set_path(api.PATH_AUTO)
