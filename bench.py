@@ -66,6 +66,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--work-mb", type=int, default=None, help="align workspace (default: library recommendation)")
     p.add_argument("--path", default=None, choices=["auto", "simt", "tc"], help="contraction path override")
+    p.add_argument("--precision", default="fp32", choices=["fp32", "fast"],
+                   help="fp32: the 1e-5 path (default); fast: single fp16 MMA + fp16 spectrum, the 2e-3 tensor-core path")
     p.add_argument("--shard", default="templates", choices=["2d", "templates"],
                    help="rank grid: templates only (north_star: templates sharded over the GPUs, default) or "
                         "image x template shards (dist.grid_shape)")
@@ -305,7 +307,9 @@ def run_ours(args):
     w_dev = ds.w.contiguous()
     if args.path:
         api.set_path({"simt": api.PATH_SIMT, "tc": api.PATH_TC, "auto": api.PATH_AUTO}[args.path])
+    api.set_precision(api.PREC_FAST if args.precision == "fast" else api.PREC_FP32)
     path = api.path_for(Q, H)
+    fast = args.precision == "fast" and path == api.PATH_TC
     tb = torch.empty(max(api.block_bytes(T_loc, Q, H, api.SIDE_TEMPLATE), 16) // 4, dtype=torch.float32, device=dev)
     # landscape mode: the M x T x Q landscape is streamed to HBM in image blocks through one tile buffer
     # (each block's rows compressed on their own: the block layout is per call)
@@ -479,7 +483,11 @@ def run_ours(args):
     n_pairs_timed = max(timing_steps, 1) * M_loc * T_loc
     if c_ms >= f_ms:
         achieved = n_pairs_timed * f_contr / (c_ms / 1e3) / 1e12 if c_ms > 0 else None
-        if path == api.PATH_TC:
+        if path == api.PATH_TC and fast:
+            peak, bound = f16_peak, "tensor"
+            kname = "contract_tc_kernel (Step 2, tcgen05 kind::f16 on CTA pairs, single fp16 MMA: the 2e-3 path)"
+            note = f"fp16 dense = measured bf16 {f16_peak:.1f} TF/s ({pk_kind}, same rate), one MMA per MAC"
+        elif path == api.PATH_TC:
             peak, bound = f16_peak / 3.0, "tensor"
             kname = "contract_tc_kernel (Step 2, tcgen05 kind::f16 on CTA pairs, fp16 hi/lo split x3)"
             note = (f"fp16 dense = measured bf16 {f16_peak:.1f} TF/s ({pk_kind}, same rate); the hi/lo split "
@@ -531,7 +539,7 @@ def run_ours(args):
                     "bytes_per_launch": {"spectrum_write": int(w_b), "operand_read": int(r_b)},
                     "peak_note": f"time-weighted L2 ceiling: write {L2_W:.0f} / read {L2_R:.0f} GB/s measured by "
                                  "tools/l2_bw_probe.cu (profiles/r01s3_l2_bw_probe.txt)"}
-    pi_c = f16_peak / 3.0 if path == api.PATH_TC else fp32_peak
+    pi_c = (f16_peak if fast else f16_peak / 3.0) if path == api.PATH_TC else fp32_peak
     land_bytes = float(M) * T * Q * 4 if mode == "landscape" else 0.0
     hbm = pk.get("hbm_gbs", 6539.9) * 1e9
     t_flop = pairs * (f_contr / pi_c + f_fft / fp32_peak) / 1e12 / world
@@ -540,8 +548,9 @@ def run_ours(args):
     step_roof = {"t_roof_ms": round(t_roof * 1e3, 3), "frac": round(t_roof * 1e3 / ms_step, 4),
                  "frac_align_only": round(t_roof * 1e3 / max(phase.get("align", 0.0), 1e-9), 4),
                  "definition": ("max(M*T*(8HQ/Pi_contr + 5Q log2 Q/Pi_fp32), landscape bytes/BW_HBM) / G vs the "
-                                "measured step, Pi_contr = " + ("fp16 dense/3 (3 MMAs per MAC)" if path == api.PATH_TC
-                                                                 else "Pi_fp32")
+                                "measured step, Pi_contr = " + (("fp16 dense (1 MMA per MAC)" if fast else
+                                                                  "fp16 dense/3 (3 MMAs per MAC)")
+                                                                 if path == api.PATH_TC else "Pi_fp32")
                                 + ", Pi_fp32 = measured FFMA2 peak (SURVEY.md 8(d))"),
                  "kernel_ms_per_step": {k: round(v[0] / ts, 3) for k, v in ktime.items()}}
 
@@ -612,9 +621,11 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "ms_per_step_median": round(ms_median, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f16 MMA / f16 spectrum, f32 transform (2e-3 path)" if fast else "f32", "data": "synthetic",
             "config": {"workload": args.config + (f"+ctf{G_ctf}" if G_ctf else ""), "M": M, "T": T, "R": R, "Q": Q,
                        "H": H, "mode": mode, "ctf_groups": G_ctf or None,
+                       "precision": "fast (<= 2e-3 gate)" if fast else "fp32 (<= 1e-5 gate)",
                        "workspace_mb": round(wbytes / 2**20, 1),
                        "parallelism": f"{GI} image x {GT} template shards on {world} GPU(s)"
                                       + (" (NCCL all-gather of winners)" if mode == "per_image" else ""),

@@ -183,6 +183,19 @@ rsvd_status rsvd_compress_translated(const void *rings, int64_t n_base, int32_t 
                                      const double *shifts, int32_t S, rsvd_side side, void *blocks,
                                      rsvd_stream_t stream);
 
+/* ------------------------------------------------------------------ numeric precision of the TC path
+ * rsvd_set_precision(0) (default, also RSVD_PRECISION unset): the fp32-grade path -- every product on
+ *   the tensor cores is the error-compensated fp16 hi/lo split (3 MMAs) and the spectrum between Steps
+ *   2 and 3 is fp32; landscapes within 1e-5 max|X| of the fp64 oracle (north_star's FP32 gate).
+ * rsvd_set_precision(1) (or RSVD_PRECISION=fast): the single-pass tensor-core path north_star allows
+ *   for "any TF32/BF16 tensor-core path" -- one fp16 MMA per product (hi x hi, row-scaled fp16
+ *   operands) and an fp16 spectrum (accumulators x 2^-20), half the spectrum bytes; landscapes within
+ *   2e-3 max|X|.  Applies to rsvd_align_argmax / _landscape / _grouped on the TC layout at Q_out == Q
+ *   (Q <= 512); other calls keep the fp32-grade path.  Process-global, like rsvd_set_path.
+ * rsvd_precision: the current setting. */
+void rsvd_set_precision(int32_t precision);
+int32_t rsvd_precision(void);
+
 /* ------------------------------------------------------------------ rows a2-a4: align
  * Step 2: S_q[m,t] = sum_h conj(A_q[m,h]) B_q[t,h] for all q;
  * Step 3: X_k = 2 pi sum_q e^{-2 pi i q k/Q} S_q, k = 0..Q-1 (forward sign, G3);

@@ -15,7 +15,7 @@ import torch
 from . import _lib
 from ._lib import PER_IMAGE, PER_PAIR, SIDE_IMAGE, SIDE_TEMPLATE, RsvdError, check, ptr, require_cuda, stream_handle
 
-__all__ = ["block_bytes", "path_for", "set_path", "PATH_AUTO", "PATH_SIMT", "PATH_TC", "kernel_chunk", "kernel_partials_bytes", "align_workspace_bytes",
+__all__ = ["block_bytes", "path_for", "set_path", "set_precision", "precision", "PREC_FP32", "PREC_FAST", "PATH_AUTO", "PATH_SIMT", "PATH_TC", "kernel_chunk", "kernel_partials_bytes", "align_workspace_bytes",
            "align_min_workspace_bytes", "kernel_partials", "kernel_reduce", "eigen_basis", "eigen_basis_ctf", "ctf_group_bases", "align_argmax_grouped", "build_basis",
            "build_basis_translated", "compress", "compress_translated", "blocks_unpack", "align_argmax", "align_landscape", "align_argmax_fine",
            "align_landscape_fine", "winners_reset",
@@ -35,6 +35,19 @@ PATH_AUTO, PATH_SIMT, PATH_TC = 0, 1, 2
 def path_for(Q: int, H: int) -> int:
     """1 = FP32 SIMT contraction, 2 = tcgen05 contraction, fp16 hi/lo split x3 MMAs (include/rsvd.h)."""
     return int(_lib.lib().rsvd_path_for(Q, H))
+
+
+PREC_FP32, PREC_FAST = 0, 1
+
+
+def set_precision(precision: int):
+    """rsvd_set_precision: PREC_FP32 (default; 1e-5 gate) or PREC_FAST (single fp16 MMA + fp16 spectrum;
+    2e-3 gate) for the tensor-core align path."""
+    _lib.lib().rsvd_set_precision(int(precision))
+
+
+def precision() -> int:
+    return int(_lib.lib().rsvd_precision())
 
 
 def set_path(path: int):

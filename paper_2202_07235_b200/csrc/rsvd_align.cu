@@ -175,18 +175,29 @@ static cudaError_t make_tmap_any(int LOGN, CUtensorMap *tm, const float *Upk, in
     }
 }
 
+static cudaError_t make_spectrum_tmap2_any(int LOGN, CUtensorMap *tm, const float *Upk, int64_t Mc, int64_t Tc, int eb) {
+    switch (LOGN) {
+        case 4: return make_spectrum_tmap2<4>(tm, Upk, Mc, Tc, eb);
+        case 5: return make_spectrum_tmap2<5>(tm, Upk, Mc, Tc, eb);
+        case 6: return make_spectrum_tmap2<6>(tm, Upk, Mc, Tc, eb);
+        case 7: return make_spectrum_tmap2<7>(tm, Upk, Mc, Tc, eb);
+        default: return make_spectrum_tmap2<8>(tm, Upk, Mc, Tc, eb);
+    }
+}
+
 static cudaError_t launch_fft_any(int LOGN, int mode, cudaStream_t s, const CUtensorMap &tm, int64_t Mc, int64_t Tc,
-                                  int64_t m0, int64_t t0, int64_t mcv, int64_t tcv, const FftOut &o, float *Upk) {
+                                  int64_t m0, int64_t t0, int64_t mcv, int64_t tcv, const FftOut &o, float *Upk,
+                                  bool half = false) {
     static const bool discard = [] { const char *e = getenv("RSVD_NO_DISCARD"); return !(e && atoi(e)); }();
     float *dU = discard ? Upk : nullptr;
     const int v = fft_version(LOGN);
     if (v == 2) {
         switch (LOGN) {
-            case 4: return launch_fft2<4>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
-            case 5: return launch_fft2<5>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
-            case 6: return launch_fft2<6>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
-            case 7: return launch_fft2<7>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
-            default: return launch_fft2<8>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc);
+            case 4: return launch_fft2<4>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc, half);
+            case 5: return launch_fft2<5>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc, half);
+            case 6: return launch_fft2<6>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc, half);
+            case 7: return launch_fft2<7>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc, half);
+            default: return launch_fft2<8>(mode, s, tm, m0, t0, mcv, tcv, o, dU, Mc, Tc, half);
         }
     }
     switch (LOGN) {
@@ -207,13 +218,17 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const int Nout = a.Qout / 2;             // spectrum rows per plane (zero-padded when Qout > Q)
     const int Kpad = (int)kpad_of(a.H);
     const bool tc = resolve_path(a.Q, a.H) == PATH_TC;
+    // fast path (<= 2e-3 gate): single fp16 MMA per product and an fp16 spectrum (half the workspace
+    // bytes per pair); TC layout, fft2 transform, plain Q_out == Q grid only
+    const bool fast = tc && resolve_precision() == PREC_FAST && a.Qout == a.Q && fft_version(ilog2(a.Q / 2)) == 2;
+    const int eb = fast ? 2 : 4;
     // pair tiles: SIMT 64 x 64; TC 128 images x 256 templates (one tcgen05 CTA-pair tile)
     const int64_t TM = tc ? 128 : 64, TT = tc ? 256 : CT_TILE;
     const int64_t Mpad = tc ? tc_rows_pad_side(a.M, RSVD_SIDE_IMAGE) : rows_pad_of(a.M);
     const int64_t Tpad = tc ? tc_rows_pad_side(a.T, RSVD_SIDE_TEMPLATE) : rows_pad_of(a.T);
     // chunk: Mc x Tc pairs (multiples of the tile) with Mc * Tc * N * 8 <= work_bytes.  Chunks are
     // visited t-outer / m-inner, so a chunk's template blocks stay in L2 while image blocks stream.
-    const int64_t tile_bytes = TM * TT * Nout * (int64_t)sizeof(float2);
+    const int64_t tile_bytes = TM * TT * Nout * 2 * (int64_t)eb;
     const int64_t ntiles = a.work_bytes / tile_bytes;
     if (ntiles < 1) return fail(RSVD_ERR_ARG, "workspace smaller than rsvd_align_min_workspace_bytes(Q)");
     const int64_t tmax = Tpad / TT, mmax = Mpad / TM;
@@ -233,7 +248,7 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const FftOut o{a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t, a.T, a.t_offset,
                    tc ? tc_scales(a.alpha, a.M, a.Q, a.H, RSVD_SIDE_IMAGE) : nullptr,
                    tc ? tc_scales(a.beta, a.T, a.Q, a.H, RSVD_SIDE_TEMPLATE) : nullptr, a.best_gamma};
-    if (tc && Nout == N) {
+    if (tc && Nout == N && !fast) {
         // one persistent launch: contraction and transform roles over an L2-sized spectrum ring
         // (rsvd_fused.cu); falls through to the two-kernel chunk loop where it does not apply
         cudaEvent_t ev0 = timing_enabled() ? timing_event(s) : nullptr;
@@ -255,7 +270,9 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     }
     const int LOGN = ilog2(Nout);
     CUtensorMap tmap;
-    if ((e = make_tmap_any(LOGN, &tmap, Upk, Mc, Tc)) != cudaSuccess) return cuda_check(e, "spectrum tensor map");
+    if ((e = fast ? make_spectrum_tmap2_any(LOGN, &tmap, Upk, Mc, Tc, 2) : make_tmap_any(LOGN, &tmap, Upk, Mc, Tc)) !=
+        cudaSuccess)
+        return cuda_check(e, "spectrum tensor map");
     const bool timed = timing_enabled();
     bool first = true;
     for (int64_t t0 = 0; t0 < Tpad; t0 += Tc) {
@@ -266,7 +283,7 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
             const int64_t mcv = std::min(mc, a.M - m0);
             cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
             if (tc) {
-                e = launch_contract_tc(tmA, tmB, a.H, N, Nout, m0, t0, mc, tc_, Mc, Tc, Upk, num_sms(), first, s);
+                e = launch_contract_tc(tmA, tmB, a.H, N, Nout, m0, t0, mc, tc_, Mc, Tc, Upk, num_sms(), first, fast, s);
                 first = false;
                 if (e != cudaSuccess) return cuda_check(e, "contract (tcgen05) launch");
             } else {
@@ -275,7 +292,7 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
                 if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "contract launch");
             }
             cudaEvent_t ev1 = timed ? timing_event(s) : nullptr;
-            e = launch_fft_any(LOGN, a.mode, s, tmap, Mc, Tc, m0, t0, mcv, tcv, o, Nout > N ? nullptr : Upk);
+            e = launch_fft_any(LOGN, a.mode, s, tmap, Mc, Tc, m0, t0, mcv, tcv, o, Nout > N ? nullptr : Upk, fast);
             if (e != cudaSuccess) return cuda_check(e, "fft_reduce launch");
             count_launches(2);
             if (timed) {

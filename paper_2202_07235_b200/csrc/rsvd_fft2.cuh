@@ -19,11 +19,13 @@
 //              item's TMA is issued as soon as the slot has been read.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "rsvd_fft.cuh"
 
 namespace rsvd {
 
-template <int LOGN>
+template <int LOGN, int EB = 4>          // EB: bytes per spectrum element (4 = fp32, 2 = fp16 fast path)
 struct Fft2Cfg {
     static constexpr int N = 1 << LOGN;
     static constexpr int Q = 2 * N;
@@ -37,7 +39,7 @@ struct Fft2Cfg {
     static constexpr int ROWS = 2 * N;                // re plane rows, then im plane rows
     static constexpr int BOXR = ROWS < 256 ? ROWS : 256;
     static constexpr int NBOX = ROWS / BOXR;
-    static constexpr int UBYTES = ROWS * TB * 4;
+    static constexpr int UBYTES = ROWS * TB * EB;
     static constexpr int SK = N1 + 1;                 // ZY stride of one k1 block (float2)
     static constexpr int SZ = N2 * SK + 1;            // ZY stride of one image (odd)
     static constexpr int ZBYTES = TB * SZ * 8;
@@ -60,7 +62,15 @@ __device__ __forceinline__ void z_pair(float2 a, float2 b, float2 w, float2 &zr,
 // slot U, pass 2 and the fused output.  `release()` is called by every thread once the slot has been
 // read for the last time (its warps may then let the slot be refilled).  Images m_first + p,
 // p < n_valid, are real; t is the template index within the call (out.T columns, out.t_offset).
-template <int LOGN, int MODE, class Release>
+// Spectrum element types: float (the fp32-grade path) or __half (the <= 2e-3 fast path: the contraction
+// stored its fp32 accumulators times FAST_SPEC_SCALE as fp16, so the result is scaled back by 1/that).
+constexpr float FAST_SPEC_SCALE = 1.0f / 1048576.0f;            // 2^-20: keeps |D| (< 2^35) inside fp16 range
+template <class Tin> __device__ __forceinline__ float spec_f(Tin x);
+template <> __device__ __forceinline__ float spec_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ float spec_f<__half>(__half x) { return __half2float(x); }
+template <class Tin> constexpr float spec_unscale() { return sizeof(Tin) == 2 ? 1048576.0f : 1.0f; }
+
+template <int LOGN, int MODE, class Release, class Tin = float>
 __device__ __forceinline__ void fft2_item(float *U, int gt, int warp, int lane, int gbar_id, const float2 *Wn,
                                           const float2 *Wq, int64_t m_first, int n_valid, int64_t t, float st,
                                           const uint32_t (&stale)[Fft2Cfg<LOGN>::P2_PER],
@@ -70,13 +80,14 @@ __device__ __forceinline__ void fft2_item(float *U, int gt, int warp, int lane, 
     constexpr int N = C::N, Q = C::Q, N1 = C::N1, N2 = C::N2, TB = C::TB, SZ = C::SZ, GT = C::GT;
     float2 *ZY = reinterpret_cast<float2 *>(U);                           // [TB][SZ], in place after pass-1 reads
     auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(gbar_id), "n"(GT) : "memory"); };
-    const float PI = 3.14159265358979323846f;
+    const float PI = 3.14159265358979323846f * spec_unscale<Tin>();
     const int ca = warp == 0 ? 0 : warp;
     const int cb = warp == 0 ? N1 / 2 : N1 - warp;
 
     // ---- pass 1: Z from the ring, two DFTs of length N2
     float2 za[N2], zb[N2];
-    auto ld = [&](int n) { return make_float2(U[n * TB + lane], U[(N + n) * TB + lane]); };
+    const Tin *Ui = reinterpret_cast<const Tin *>(U);
+    auto ld = [&](int n) { return make_float2(spec_f<Tin>(Ui[n * TB + lane]), spec_f<Tin>(Ui[(N + n) * TB + lane])); };
     if (warp == 0) {
         // column 0: rows N1*n2; pairs (n2, N2 - n2); n2 = 0 -> Z_0, n2 = N2/2 -> Z_{N/2}
         {
@@ -236,13 +247,13 @@ __device__ __forceinline__ void fft2_tables(float2 *Wn, float2 *Wq, int tid, int
     }
 }
 
-template <int LOGN, int MODE>
+template <int LOGN, int MODE, class Tin = float>
 __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                                int64_t m0, int64_t t0, int64_t mcv,
                                                                                int64_t tcv, FftOut out,
                                                                                float *__restrict__ Upk, int64_t Mc,
                                                                                int64_t Tc) {
-    using C = Fft2Cfg<LOGN>;
+    using C = Fft2Cfg<LOGN, (int)sizeof(Tin)>;
     constexpr int N = C::N, TB = C::TB, G = C::G, GT = C::GT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // pointer arithmetic on the __shared__ array (not an integer round trip) keeps LDS/STS addressing
@@ -274,7 +285,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
                      : "memory");
 #pragma unroll
         for (int bx = 0; bx < C::NBOX; ++bx) {
-            const uint32_t dst = fr_smem(base + (size_t)sl * C::SLOT + (size_t)bx * C::BOXR * TB * 4);
+            const uint32_t dst = fr_smem(base + (size_t)sl * C::SLOT + (size_t)bx * C::BOXR * TB * sizeof(Tin));
             asm volatile(
                 "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                 ::"r"(dst), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(mb0), "r"(tl), "r"(bx * C::BOXR), "r"(bar)
@@ -304,7 +315,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
     const int step = G * grid, dtl = step / nmb, dmb = step - dtl * nmb;
     int tl = item_of(g) / nmb, mbi = item_of(g) - tl * nmb;
     // this thread's discard rows r = gt, gt + GT, ... (row stride Tc * Mc floats)
-    float *const dbase = Upk ? Upk + (int64_t)gt * Tc * Mc : nullptr;
+    float *const dbase = (Upk && sizeof(Tin) == 4) ? Upk + (int64_t)gt * Tc * Mc : nullptr;
     const int64_t dstride = (int64_t)GT * Tc * Mc;
     for (int i = g; item_of(i) < nitems; i += G, tl += dtl, mbi += dmb) {
         if (mbi >= nmb) { mbi -= nmb; ++tl; }
@@ -339,33 +350,35 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
                 issue(i + C::NSLOT);
             }
         };
-        fft2_item<LOGN, MODE>(U, gt, warp, lane, 1 + g, Wn, Wq, m0 + mb0, n_valid, t, st, stale, smv, out, release);
+        fft2_item<LOGN, MODE, decltype(release), Tin>(U, gt, warp, lane, 1 + g, Wn, Wq, m0 + mb0, n_valid, t, st, stale,
+                                                       smv, out, release);
     }
 }
 
 // 3-D view of the planar workspace with 32-image boxes (the fft2 work item).
+// eb = bytes per element: 4 (fp32 spectrum) or 2 (fp16 spectrum of the fast path).
 template <int LOGN>
-static cudaError_t make_spectrum_tmap2(CUtensorMap *tm, const float *Upk, int64_t Mc, int64_t Tc) {
+static cudaError_t make_spectrum_tmap2(CUtensorMap *tm, const float *Upk, int64_t Mc, int64_t Tc, int eb = 4) {
     using C = Fft2Cfg<LOGN>;
     PFN_encodeTiled_fr enc = encode_tiled_fn();
     if (!enc) return cudaErrorNotSupported;
     const cuuint64_t dims[3] = {(cuuint64_t)Mc, (cuuint64_t)Tc, (cuuint64_t)C::ROWS};
-    const cuuint64_t strides[2] = {(cuuint64_t)Mc * 4, (cuuint64_t)Mc * Tc * 4};
+    const cuuint64_t strides[2] = {(cuuint64_t)Mc * eb, (cuuint64_t)Mc * Tc * eb};
     const cuuint32_t box[3] = {(cuuint32_t)C::TB, 1u, (cuuint32_t)C::BOXR};
     const cuuint32_t estr[3] = {1u, 1u, 1u};
-    const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(Upk), dims, strides, box, estr,
+    const CUresult r = enc(tm, eb == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(Upk), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int LOGN, int MODE>
+template <int LOGN, int MODE, class Tin = float>
 static cudaError_t launch_fft2_mode(cudaStream_t s, const CUtensorMap &tm, int64_t m0, int64_t t0, int64_t mcv,
                                     int64_t tcv, const FftOut &out, float *Upk, int64_t Mc, int64_t Tc) {
-    using C = Fft2Cfg<LOGN>;
+    using C = Fft2Cfg<LOGN, (int)sizeof(Tin)>;
     const size_t smem = C::smem_bytes();
     static std::atomic<uint64_t> attr{0};
-    const cudaError_t e = smem_attr_once((const void *)fft2_reduce_kernel<LOGN, MODE>, (int)smem, attr);
+    const cudaError_t e = smem_attr_once((const void *)fft2_reduce_kernel<LOGN, MODE, Tin>, (int)smem, attr);
     if (e != cudaSuccess) return e;
     const int64_t nitems = tcv * ((mcv + C::TB - 1) / C::TB);
     const int64_t grid = std::min<int64_t>((nitems + C::G - 1) / C::G, (int64_t)num_sms());
@@ -379,15 +392,21 @@ static cudaError_t launch_fft2_mode(cudaStream_t s, const CUtensorMap &tm, int64
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, fft2_reduce_kernel<LOGN, MODE>, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
+    return cudaLaunchKernelEx(&cfg, fft2_reduce_kernel<LOGN, MODE, Tin>, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
 }
 
+template <int LOGN, class Tin = float>
+static cudaError_t launch_fft2_t(int mode, cudaStream_t s, const CUtensorMap &tm, int64_t m0, int64_t t0, int64_t mcv,
+                                 int64_t tcv, const FftOut &out, float *Upk, int64_t Mc, int64_t Tc) {
+    if (mode == MODE_PAIR) return launch_fft2_mode<LOGN, MODE_PAIR, Tin>(s, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
+    if (mode == MODE_IMAGE) return launch_fft2_mode<LOGN, MODE_IMAGE, Tin>(s, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
+    return launch_fft2_mode<LOGN, MODE_LANDSCAPE, Tin>(s, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
+}
 template <int LOGN>
 static cudaError_t launch_fft2(int mode, cudaStream_t s, const CUtensorMap &tm, int64_t m0, int64_t t0, int64_t mcv,
-                               int64_t tcv, const FftOut &out, float *Upk, int64_t Mc, int64_t Tc) {
-    if (mode == MODE_PAIR) return launch_fft2_mode<LOGN, MODE_PAIR>(s, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
-    if (mode == MODE_IMAGE) return launch_fft2_mode<LOGN, MODE_IMAGE>(s, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
-    return launch_fft2_mode<LOGN, MODE_LANDSCAPE>(s, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
+                               int64_t tcv, const FftOut &out, float *Upk, int64_t Mc, int64_t Tc, bool half = false) {
+    return half ? launch_fft2_t<LOGN, __half>(mode, s, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc)
+                : launch_fft2_t<LOGN, float>(mode, s, tm, m0, t0, mcv, tcv, out, Upk, Mc, Tc);
 }
 
 }  // namespace rsvd

@@ -87,7 +87,7 @@ __device__ __forceinline__ void st_spectrum(float *p, float v, uint64_t pol) {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int steps, int KB, int N,
     int mtl, int ntl, int mt0, int nt0, int qg, int nqg, int nitems, int64_t Mc, int64_t Tc,
-    float *__restrict__ Upk, int Nout, int operands_fresh) {
+    float *__restrict__ Upk, int Nout, int operands_fresh, int fast) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint64_t *bars = reinterpret_cast<uint64_t *>(base + TC_STAGES * TC_STAGE_BYTES);
@@ -180,8 +180,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
                         for (int k = 0; k < nst; ++k) {
                             const uint64_t o = (uint64_t)(2 * k);          // +32 B per K=16 fp16 step
                             tc_mma_f16_pair(dt, a_hi + o, b_hi + o, idesc, (kb | k) ? 1u : 0u);
-                            tc_mma_f16_pair(dt, a_hi + o, b_lo + o, idesc, 1u);
-                            tc_mma_f16_pair(dt, a_lo + o, b_hi + o, idesc, 1u);
+                            if (!fast) {                                   // fast path (<= 2e-3): hi x hi only
+                                tc_mma_f16_pair(dt, a_hi + o, b_lo + o, idesc, 1u);
+                                tc_mma_f16_pair(dt, a_lo + o, b_hi + o, idesc, 1u);
+                            }
                         }
                         tc_commit_pair(empty + s);       // both CTAs' stage s free once these complete
                     }
@@ -239,12 +241,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
                         tmem_ld32(tbase + (uint32_t)(64 * b + 64), v[cur ^ 1][0]);
                         tmem_ld32(tbase + (uint32_t)(64 * b + 96), v[cur ^ 1][1]);
                     }
-                    if (store) {
+                    if (store && !fast) {
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
 #pragma unroll
                             for (int i = 0; i < 32; ++i)
                                 st_spectrum(dst + (int64_t)(64 * b + 32 * h + i) * Mc, qs * __uint_as_float(v[cur][h][i]), pol_ws);
+                    } else if (store) {
+                        // fast path: fp16 spectrum (same [n][t][m] planes, 2 B per value), accumulators
+                        // scaled by FAST_SPEC_SCALE = 2^-20 into fp16 range; the transform scales back
+                        __half *hdst = reinterpret_cast<__half *>(Upk) + (dst - Upk);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                hdst[(int64_t)(64 * b + 32 * h + i) * Mc] =
+                                    __float2half_rn(qs * (1.0f / 1048576.0f) * __uint_as_float(v[cur][h][i]));
                     }
                     tmem_wait_ld();
                 }
@@ -594,6 +606,17 @@ int resolve_path(int Q, int H) {
 }
 void set_path(int p) { g_path = (p == PATH_SIMT || p == PATH_TC) ? p : PATH_AUTO; }
 
+static std::atomic<int> g_precision{-1};
+int resolve_precision() {
+    int p = g_precision.load(std::memory_order_relaxed);
+    if (p < 0) {
+        const char *e = getenv("RSVD_PRECISION");
+        p = (e && !strcmp(e, "fast")) ? PREC_FAST : PREC_FP32;
+        g_precision.store(p, std::memory_order_relaxed);
+    }
+    return p;
+}
+
 template <int LOGQ, int HC, bool SPLIT>
 static cudaError_t launch_compress_tc_qh(const float2 *rings, int64_t n, int R, const double *w, const double *U, int H,
                                          int side, void *blocks, const double *kr, const double *shifts, int S,
@@ -707,7 +730,7 @@ cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t ro
 // One chunk: images [m0, m0 + mc) (multiples of 128), templates [t0, t0 + tc) (multiples of 256).
 cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int Nout, int64_t m0,
                                int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms,
-                               bool operands_fresh, cudaStream_t s) {
+                               bool operands_fresh, bool fast, cudaStream_t s) {
     static std::atomic<uint64_t> attr{0};
     {
         const cudaError_t e = smem_attr_once((const void *)contract_tc_kernel, (int)TC_SMEM, attr);
@@ -736,7 +759,7 @@ cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, i
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, contract_tc_kernel, tmA, tmB, tc_steps(H), tc_kb(H), N, mtl, ntl,
                                        (int)(m0 / TC_PIMG), (int)(t0 / TC_TT), qg, nqg, nitems, Mc, Tc, Upk, Nout,
-                                       operands_fresh ? 1 : 0);
+                                       operands_fresh ? 1 : 0, fast ? 1 : 0);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -744,4 +767,8 @@ cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, i
 }  // namespace rsvd
 
 extern "C" void rsvd_set_path(int32_t path) { rsvd::set_path(path); }
+extern "C" void rsvd_set_precision(int32_t precision) {
+    rsvd::g_precision.store(precision == rsvd::PREC_FAST ? rsvd::PREC_FAST : rsvd::PREC_FP32);
+}
+extern "C" int32_t rsvd_precision(void) { return rsvd::resolve_precision(); }
 extern "C" int32_t rsvd_path_for(int32_t Q, int32_t H) { return rsvd::resolve_path(Q, H); }
