@@ -10,3 +10,5 @@ for h in 64 32 16 8; do run medium_h$h --config medium --H $h --steps 10 --warmu
 run translations --config translations --steps 10 --warmup 3 --no-cpu-baseline
 run translations_landscape --config translations --mode landscape --steps 5 --warmup 3 --no-cpu-baseline --traffic off
 run large_per_pair --config large --mode per_pair --steps 5 --warmup 3 --no-cpu-baseline --traffic off
+run large_fast --config large --precision fast --steps 10 --warmup 3 --no-cpu-baseline --no-e2e
+run large_ctf4 --config large --ctf-groups 4 --steps 10 --warmup 3 --no-cpu-baseline --traffic off
