@@ -20,6 +20,7 @@
 #include "rsvd_common.cuh"
 #include "rsvd_fft.cuh"
 #include "rsvd_fft2.cuh"
+#include "rsvd_fftc.cuh"
 
 namespace rsvd {
 
@@ -222,6 +223,12 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     // bytes per pair); TC layout, fft2 transform, plain Q_out == Q grid only
     const bool fast = tc && resolve_precision() == PREC_FAST && a.Qout == a.Q && fft_version(ilog2(a.Q / 2)) == 2;
     const int eb = fast ? 2 : 4;
+    // Steps 3-4 with pass 1 on the tensor cores (rsvd_fftc.cuh): TC layout, Q in {256, 512}, argmax
+    // modes, plain grid; the contraction then writes the split hi/lo fp16 spectrum (fmt 2, same bytes)
+    const char *fftc_e = getenv("RSVD_FFTC");
+    const int fftc_env = fftc_e ? atoi(fftc_e) : 0;
+    const int lognq = ilog2(a.Q / 2);
+    const bool fftc = tc && !fast && fftc_env && a.Qout == a.Q && (lognq == 7 || lognq == 8) && a.mode != MODE_LANDSCAPE;
     // pair tiles: SIMT 64 x 64; TC 128 images x 256 templates (one tcgen05 CTA-pair tile)
     const int64_t TM = tc ? 128 : 64, TT = tc ? 256 : CT_TILE;
     const int64_t Mpad = tc ? tc_rows_pad_side(a.M, RSVD_SIDE_IMAGE) : rows_pad_of(a.M);
@@ -248,7 +255,7 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const FftOut o{a.best_val, a.best_k, a.best_key, a.X, a.ld_m, a.ld_t, a.T, a.t_offset,
                    tc ? tc_scales(a.alpha, a.M, a.Q, a.H, RSVD_SIDE_IMAGE) : nullptr,
                    tc ? tc_scales(a.beta, a.T, a.Q, a.H, RSVD_SIDE_TEMPLATE) : nullptr, a.best_gamma};
-    if (tc && Nout == N && !fast) {
+    if (tc && Nout == N && !fast && !fftc) {
         // one persistent launch: contraction and transform roles over an L2-sized spectrum ring
         // (rsvd_fused.cu); falls through to the two-kernel chunk loop where it does not apply
         cudaEvent_t ev0 = timing_enabled() ? timing_event(s) : nullptr;
@@ -270,7 +277,8 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     }
     const int LOGN = ilog2(Nout);
     CUtensorMap tmap;
-    if ((e = fast ? make_spectrum_tmap2_any(LOGN, &tmap, Upk, Mc, Tc, 2) : make_tmap_any(LOGN, &tmap, Upk, Mc, Tc)) !=
+    if ((e = fftc ? make_fftc_tmap_any(LOGN, &tmap, Upk, Mc, Tc)
+              : (fast ? make_spectrum_tmap2_any(LOGN, &tmap, Upk, Mc, Tc, 2) : make_tmap_any(LOGN, &tmap, Upk, Mc, Tc))) !=
         cudaSuccess)
         return cuda_check(e, "spectrum tensor map");
     const bool timed = timing_enabled();
@@ -283,7 +291,8 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
             const int64_t mcv = std::min(mc, a.M - m0);
             cudaEvent_t ev0 = timed ? timing_event(s) : nullptr;
             if (tc) {
-                e = launch_contract_tc(tmA, tmB, a.H, N, Nout, m0, t0, mc, tc_, Mc, Tc, Upk, num_sms(), first, fast, s);
+                e = launch_contract_tc(tmA, tmB, a.H, N, Nout, m0, t0, mc, tc_, Mc, Tc, Upk, num_sms(), first,
+                                       fast ? 1 : (fftc ? 2 : 0), s);
                 first = false;
                 if (e != cudaSuccess) return cuda_check(e, "contract (tcgen05) launch");
             } else {
@@ -292,7 +301,8 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
                 if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "contract launch");
             }
             cudaEvent_t ev1 = timed ? timing_event(s) : nullptr;
-            e = launch_fft_any(LOGN, a.mode, s, tmap, Mc, Tc, m0, t0, mcv, tcv, o, Nout > N ? nullptr : Upk, fast);
+            e = fftc ? launch_fftc(LOGN, a.mode, s, tmap, m0, t0, mcv, tcv, o, Mc)
+                     : launch_fft_any(LOGN, a.mode, s, tmap, Mc, Tc, m0, t0, mcv, tcv, o, Nout > N ? nullptr : Upk, fast);
             if (e != cudaSuccess) return cuda_check(e, "fft_reduce launch");
             count_launches(2);
             if (timed) {

@@ -52,10 +52,13 @@ cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t ro
 const float *tc_scales(const void *blocks, int64_t rows, int Q, int H, int side);
 cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int Nout, int64_t m0,
                                int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms,
-                               bool operands_fresh, bool fast, cudaStream_t s);
+                               bool operands_fresh, int fmt, cudaStream_t s);
 // numeric precision of the TC align path: PREC_FP32 (error-compensated fp16 hi/lo, fp32 spectrum; the
 // 1e-5 gate) or PREC_FAST (one fp16 MMA per product, fp16 spectrum; the <= 2e-3 gate of north_star)
 enum { PREC_FP32 = 0, PREC_FAST = 1 };
+#ifndef RSVD_SPLIT_SCALE
+#define RSVD_SPLIT_SCALE (1.0f / 1048576.0f)     // split hi/lo spectrum: value x 2^-20 (fp16 range)
+#endif
 int resolve_precision();
 
 // Per-device one-time kernel attribute (max dynamic shared memory): bit d of `done` is set once the

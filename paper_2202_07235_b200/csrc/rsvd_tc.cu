@@ -87,7 +87,11 @@ __device__ __forceinline__ void st_spectrum(float *p, float v, uint64_t pol) {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int steps, int KB, int N,
     int mtl, int ntl, int mt0, int nt0, int qg, int nqg, int nitems, int64_t Mc, int64_t Tc,
-    float *__restrict__ Upk, int Nout, int operands_fresh, int fast) {
+    float *__restrict__ Upk, int Nout, int operands_fresh, int fmt) {
+    // fmt: spectrum format -- 0 fp32 planes; 1 fp16 planes (single-MMA fast path); 2 split fp16 hi/lo
+    // planes for the tensor-core transform (rsvd_fftc.cuh): [n][part][t][m], part = re_hi, im_hi, re_lo,
+    // im_lo, value = (hi + lo 2^-10) 2^20
+    const bool fast = fmt == 1;
     extern __shared__ unsigned char smem_raw[];
     unsigned char *base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint64_t *bars = reinterpret_cast<uint64_t *>(base + TC_STAGES * TC_STAGE_BYTES);
@@ -241,12 +245,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
                         tmem_ld32(tbase + (uint32_t)(64 * b + 64), v[cur ^ 1][0]);
                         tmem_ld32(tbase + (uint32_t)(64 * b + 96), v[cur ^ 1][1]);
                     }
-                    if (store && !fast) {
+                    if (store && fmt == 0) {
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
 #pragma unroll
                             for (int i = 0; i < 32; ++i)
                                 st_spectrum(dst + (int64_t)(64 * b + 32 * h + i) * Mc, qs * __uint_as_float(v[cur][h][i]), pol_ws);
+                    } else if (store && fmt == 2) {
+                        // split hi/lo fp16 (same 4 B per value): hi = fp16(x), lo = fp16(x - hi), x = v 2^-20
+                        const bool imv = (nyq_packed || (q != 0 && q != N && !re_rows));
+                        __half *sp = reinterpret_cast<__half *>(Upk) +
+                                     (((int64_t)n * 4 + (imv ? 1 : 0)) * Tc + (int64_t)nt_l * TC_TT + 64 * b) * Mc + ml;
+                        const int64_t lo_off = (int64_t)2 * Tc * Mc;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) {
+                                const float x = RSVD_SPLIT_SCALE * __uint_as_float(v[cur][h][i]);
+                                const __half hi = __float2half_rn(x);
+                                const __half lo = __float2half_rn((x - __half2float(hi)) * 1024.0f);
+                                __half *e = sp + (int64_t)(32 * h + i) * Mc;
+                                e[0] = hi;
+                                e[lo_off] = lo;
+                            }
                     } else if (store) {
                         // fast path: fp16 spectrum (same [n][t][m] planes, 2 B per value), accumulators
                         // scaled by FAST_SPEC_SCALE = 2^-20 into fp16 range; the transform scales back
@@ -730,7 +751,7 @@ cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t ro
 // One chunk: images [m0, m0 + mc) (multiples of 128), templates [t0, t0 + tc) (multiples of 256).
 cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int Nout, int64_t m0,
                                int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms,
-                               bool operands_fresh, bool fast, cudaStream_t s) {
+                               bool operands_fresh, int fmt, cudaStream_t s) {
     static std::atomic<uint64_t> attr{0};
     {
         const cudaError_t e = smem_attr_once((const void *)contract_tc_kernel, (int)TC_SMEM, attr);
@@ -759,7 +780,7 @@ cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, i
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, contract_tc_kernel, tmA, tmB, tc_steps(H), tc_kb(H), N, mtl, ntl,
                                        (int)(m0 / TC_PIMG), (int)(t0 / TC_TT), qg, nqg, nitems, Mc, Tc, Upk, Nout,
-                                       operands_fresh ? 1 : 0, fast ? 1 : 0);
+                                       operands_fresh ? 1 : 0, fmt);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
