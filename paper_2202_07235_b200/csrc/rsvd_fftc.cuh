@@ -43,10 +43,11 @@ struct FftcCfg {
     static constexpr int N2 = N / N1;                 // rows (16 for LOGN = 7, 8)
     static constexpr int NCP = N1 / 2;                // mirror column pairs
     static constexpr int BM = 128;                    // images per batch (MMA M)
-    static constexpr int STAGES = 4;
     static constexpr uint32_t A_BYTES = 32768;        // [hl][mh][col][32 rows x 128 B]
     static constexpr uint32_t B_BYTES = 16384;        // B_hi, B_lo: 64 rows x 128 B each
-    static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+    static constexpr uint32_t STAGE = A_BYTES;        // A ring; every B_cp stays resident
+    static constexpr uint32_t BRES = (uint32_t)NCP * B_BYTES;
+    static constexpr int STAGES = NCP == 8 ? 2 : 4;
     static constexpr int SUBS = 4;                    // stage-B warps per TMEM lane quadrant
     static constexpr int KPS = N2 / SUBS;             // k1 values per stage-B warp
     static constexpr int TCOLS = NCP * 64;            // TMEM columns per batch
@@ -54,7 +55,7 @@ struct FftcCfg {
     static constexpr int THREADS = 18 * 32;
     static_assert(N2 == 16, "fftc: N in {128, 256}");
     static constexpr size_t smem_bytes() {
-        return 1024 + (size_t)STAGES * STAGE + 2 * SUBS * 128 * 8 + (2 * STAGES + 2 * NACC) * 8 + 16;
+        return 1024 + (size_t)BRES + (size_t)STAGES * STAGE + 2 * SUBS * 128 * 8 + (2 * STAGES + 2 * NACC + 1) * 8 + 16;
     }
 };
 
@@ -110,8 +111,10 @@ __global__ void __launch_bounds__(FftcCfg<LOGN>::THREADS, 1)
     constexpr int N1 = C::N1, N2 = C::N2, NCP = C::NCP, Q = C::Q;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    float2 *red = reinterpret_cast<float2 *>(base + C::STAGES * C::STAGE);          // [2][SUBS][128] (value, index)
-    uint64_t *full = reinterpret_cast<uint64_t *>(red + 2 * C::SUBS * 128);
+    unsigned char *bres = base + C::STAGES * C::STAGE;                              // [NCP][B_BYTES]
+    float2 *red = reinterpret_cast<float2 *>(bres + C::BRES);                       // [2][SUBS][128] (value, index)
+    uint64_t *bfull = reinterpret_cast<uint64_t *>(red + 2 * C::SUBS * 128);
+    uint64_t *full = bfull + 1;
     uint64_t *empty = full + C::STAGES;
     uint64_t *tfull = empty + C::STAGES;
     uint64_t *tempty = tfull + C::NACC;
@@ -125,6 +128,7 @@ __global__ void __launch_bounds__(FftcCfg<LOGN>::THREADS, 1)
     if (warp == 16 && lane == 0) {
         for (int s = 0; s < C::STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
         for (int a = 0; a < C::NACC; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 16); }
+        mbar_init(bfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 17) {
@@ -144,6 +148,13 @@ __global__ void __launch_bounds__(FftcCfg<LOGN>::THREADS, 1)
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmS)) : "memory");
             int it = 0;
+            // the pass-1 matrices once per CTA (resident for the whole kernel)
+            mbar_expect_tx(bfull, C::BRES);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(bres)),
+                "l"(Bg), "r"(C::BRES), "r"(smem_u32(bfull))
+                : "memory");
             for (int item = blockIdx.x; item < nitems; item += grid) {
                 const int tl = item / nbm, mb = item - tl * nbm;
 #pragma unroll 1
@@ -153,11 +164,6 @@ __global__ void __launch_bounds__(FftcCfg<LOGN>::THREADS, 1)
                     const uint32_t fb = smem_u32(full + s);
                     mbar_expect_tx(full + s, C::STAGE);
                     const uint32_t st = smem_u32(base + (size_t)s * C::STAGE);
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                            st + C::A_BYTES),
-                        "l"(Bg + (size_t)cp * C::B_BYTES), "r"(C::B_BYTES), "r"(fb)
-                        : "memory");
                     const int cols[2] = {fftc_ca(cp, N1), fftc_cb(cp, N1)};
 #pragma unroll
                     for (int hl = 0; hl < 2; ++hl)
@@ -185,6 +191,7 @@ __global__ void __launch_bounds__(FftcCfg<LOGN>::THREADS, 1)
         if (lane == 0) {
             const uint32_t idesc = (1u << 4) | (1u << 15) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             int it = 0, bi = 0;
+            mbar_wait(bfull, 0);
             for (int item = blockIdx.x; item < nitems; item += grid, ++bi) {
                 const int acc = bi % C::NACC;
                 mbar_wait(tempty + acc, (((uint32_t)(bi / C::NACC)) & 1u) ^ 1u);
@@ -196,7 +203,8 @@ __global__ void __launch_bounds__(FftcCfg<LOGN>::THREADS, 1)
                     tc_fence_after();
                     const uint32_t st = smem_u32(base + (size_t)s * C::STAGE);
                     const uint64_t a_hi = mn_sw128_desc(st, 8192), a_lo = mn_sw128_desc(st + 16384, 8192);
-                    const uint64_t b_hi = sw128_desc(st + C::A_BYTES), b_lo = sw128_desc(st + C::A_BYTES + 8192);
+                    const uint32_t sb = smem_u32(bres + (size_t)cp * C::B_BYTES);
+                    const uint64_t b_hi = sw128_desc(sb), b_lo = sw128_desc(sb + 8192);
                     const uint32_t dt = tmem + (uint32_t)(acc * C::TCOLS + cp * 64);
                     // corrections first, each operand's lo part stored x 2^10 (keeps it out of the fp16
                     // subnormals, which the tensor core flushes): D = 2^10 (A_lo B_hi + A_hi B_lo); then

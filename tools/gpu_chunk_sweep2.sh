@@ -1,0 +1,10 @@
+#!/bin/bash
+# larger chunks (round 2): does fewer launches beat more DRAM spill?
+out=gpurun_out/chunk_sweep2.txt; : > $out
+for cfg in "2 128" "2 192" "2 256" "2 384" "0 256"; do
+  set -- $cfg; pol=$1; mb=$2
+  lib=""; [ $pol != 2 ] && lib="RSVD_LIB=build_var/librsvd_ws$pol.so"
+  env $lib timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --traffic off --work-mb $mb > gpurun_out/cs.log 2>&1
+  tail -1 gpurun_out/cs.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['step_roofline']['kernel_ms_per_step']; print('pol=$pol mb=$mb', d['ms_per_step'], d['phases_ms_last_step']['align'], r['contract'], r['fft_reduce'], d['clocks']['sm_mhz'])" >> $out 2>&1 || tail -3 gpurun_out/cs.log >> $out
+done
+cat $out
