@@ -42,6 +42,21 @@
 
 namespace rsvd {
 
+typedef CUresult (*PFN_encodeTiled_tc)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                       const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled_tc encode_fn() {
+    static PFN_encodeTiled_tc fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled_tc>(p);
+    }
+    return fn;
+}
+
 constexpr int TC_THREADS = 6 * 32;
 constexpr int TC_STAGES = 7;
 constexpr int TC_PIMG = 128;                        // images per CTA pair (64 per CTA)
@@ -325,9 +340,13 @@ __device__ __forceinline__ float scale_for(float m) {
     return ldexpf(1.f, 13 - ilogbf(m));
 }
 
-__device__ __forceinline__ void split_h(float x, __half &hi, __half &lo) {
-    hi = __float2half_rn(x);
-    lo = __float2half_rn(x - __half2float(hi));
+// the same split for a pair, packed: (hi.x, hi.y) and (lo.x, lo.y) as half2 bit patterns
+__device__ __forceinline__ void split_h2(float2 v, uint32_t &hi, uint32_t &lo) {
+    const __half2 h = __float22half2_rn(v);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __float22half2_rn(make_float2(v.x - hf.x, v.y - hf.y));
+    hi = *reinterpret_cast<const uint32_t *>(&h);
+    lo = *reinterpret_cast<const uint32_t *>(&l);
 }
 
 // Operand rows of this CTA's quarters (4 complex k-slots = 16 B of hi and 16 B of lo): global quarter
@@ -335,12 +354,14 @@ __device__ __forceinline__ void split_h(float x, __half &hi, __half &lo) {
 // H <= j < 2H: mirror h = j - H, j >= 2H: zero padding).  at holds principal rings h0 .. h0 + hg - 1.
 struct QuarterSet { int a0, a1, b0, b1, c0, c1; };        // up to three ranges [x0, x1) of global quarters
 __device__ void emit_tc_rows(const float2 *at, int h0, int H, int Q, int KB, int side, int64_t row,
-                             int64_t op_rows, float s, QuarterSet qs, __half *__restrict__ ops) {
+                             int64_t op_rows, float s, QuarterSet qs, __half *__restrict__ ops,
+                             int t0 = -1, int nt = 0) {
     const int N = Q / 2;
     const int E = Q / 32;
     const int na = qs.a1 - qs.a0, nb = qs.b1 - qs.b0, nc = qs.c1 - qs.c0, nq = na + nb + nc;
     const int total = (N + 1) * nq;                       // (q, owned quarter)
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    if (t0 < 0) { t0 = threadIdx.x; nt = blockDim.x; }
+    for (int idx = t0; idx < total; idx += nt) {
         const int lq = idx % nq;
         const int q = idx / nq;
         const int gq = lq < na ? qs.a0 + lq : (lq < na + nb ? qs.b0 + lq - na : qs.c0 + lq - na - nb);
@@ -361,25 +382,21 @@ __device__ void emit_tc_rows(const float2 *at, int h0, int H, int Q, int KB, int
         }
         const int64_t sub = (int64_t)q * KB + kb;         // (q, kb): rows of 64 fp16 (hi | lo)
         if (side == RSVD_SIDE_TEMPLATE) {
-            __align__(16) __half hi[8], lo[8];
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) { split_h(c[jj].x, hi[2 * jj], lo[2 * jj]); split_h(c[jj].y, hi[2 * jj + 1], lo[2 * jj + 1]); }
-            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + row) * 64 + qu * 8) = *reinterpret_cast<uint4 *>(hi);
-            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + row) * 64 + 32 + qu * 8) = *reinterpret_cast<uint4 *>(lo);
+            uint4 hi, lo;
+            split_h2(c[0], hi.x, lo.x); split_h2(c[1], hi.y, lo.y); split_h2(c[2], hi.z, lo.z); split_h2(c[3], hi.w, lo.w);
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + row) * 64 + qu * 8) = hi;
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + row) * 64 + 32 + qu * 8) = lo;
         } else {
             const int64_t rre = (row / 64) * 128 + row % 64, rim = rre + 64;
-            __align__(16) __half rh[8], rl[8], ih[8], il[8];
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                split_h(c[jj].x, rh[2 * jj], rl[2 * jj]);            // A_re = (Re a, -Im a)
-                split_h(-c[jj].y, rh[2 * jj + 1], rl[2 * jj + 1]);
-                split_h(c[jj].y, ih[2 * jj], il[2 * jj]);            // A_im = (Im a, Re a)
-                split_h(c[jj].x, ih[2 * jj + 1], il[2 * jj + 1]);
-            }
-            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rre) * 64 + qu * 8) = *reinterpret_cast<uint4 *>(rh);
-            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rre) * 64 + 32 + qu * 8) = *reinterpret_cast<uint4 *>(rl);
-            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rim) * 64 + qu * 8) = *reinterpret_cast<uint4 *>(ih);
-            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rim) * 64 + 32 + qu * 8) = *reinterpret_cast<uint4 *>(il);
+            uint4 rh, rl, ih, il;                         // A_re = (Re a, -Im a), A_im = (Im a, Re a)
+            split_h2(make_float2(c[0].x, -c[0].y), rh.x, rl.x); split_h2(make_float2(c[0].y, c[0].x), ih.x, il.x);
+            split_h2(make_float2(c[1].x, -c[1].y), rh.y, rl.y); split_h2(make_float2(c[1].y, c[1].x), ih.y, il.y);
+            split_h2(make_float2(c[2].x, -c[2].y), rh.z, rl.z); split_h2(make_float2(c[2].y, c[2].x), ih.z, il.z);
+            split_h2(make_float2(c[3].x, -c[3].y), rh.w, rl.w); split_h2(make_float2(c[3].y, c[3].x), ih.w, il.w);
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rre) * 64 + qu * 8) = rh;
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rre) * 64 + 32 + qu * 8) = rl;
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rim) * 64 + qu * 8) = ih;
+            *reinterpret_cast<uint4 *>(ops + (sub * op_rows + rim) * 64 + 32 + qu * 8) = il;
         }
     }
 }
@@ -670,8 +687,15 @@ static cudaError_t launch_compress_tc_q(const float2 *rings, int64_t n, int R, c
     }
 }
 
+#include "rsvd_compress_mma.cuh"
+
 cudaError_t launch_compress_tc(const float2 *rings, int64_t n, int R, int Q, const double *w, const double *U, int H,
                                int side, float *blocks, const double *kr, const double *shifts, int S, cudaStream_t s) {
+    if (!shifts) {
+        bool launched = false;
+        const cudaError_t e = launch_compress_mma(rings, n, R, Q, w, U, H, side, blocks, s, &launched);
+        if (e != cudaSuccess || launched) return e;
+    }
     switch (ilog2(Q)) {
         case 5: return launch_compress_tc_q<5>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
         case 6: return launch_compress_tc_q<6>(rings, n, R, w, U, H, side, blocks, kr, shifts, S, s);
@@ -716,21 +740,6 @@ cudaError_t launch_unpack_tc(const float *blocks, int64_t n, int Q, int H, int s
 }
 
 // ------------------------------------------------------------------ tensor maps + launch
-typedef CUresult (*PFN_encodeTiled_tc)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                       const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static PFN_encodeTiled_tc encode_fn() {
-    static PFN_encodeTiled_tc fn = nullptr;
-    if (!fn) {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_encodeTiled_tc>(p);
-    }
-    return fn;
-}
-
 // 4-D map of one side's operand rows: (64 fp16 = hi | lo, row, kb, q), box (64, box_rows, 1, 1), SWIZZLE_128B.
 cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t rows, int Q, int H, int side,
                                  int box_rows) {
