@@ -7,12 +7,13 @@
 //   U'[r][h] = U[r][h] sqrt(w_r) / Q      (the same fp32-rounded basis as compress_tc_kernel),
 // M = 2Q floats of each ring, K = R rings, N = H principal rings (padded to NPAD = 16 or 32).
 // tcgen05.mma kind::tf32 (cta_group::1, M = 128 per tile, N = NPAD, K = 8 rings per instruction) with a
-// three-term split for ~fp32 accuracy: a = a_hi + a_lo (a_hi = a rounded to tf32, exact remainder),
-// U' = U'_hi + U'_lo, D = a_hi U'_hi + a_hi U'_lo + a_lo U'_hi (dropped a_lo U'_lo ~ 2^-22 relative).
+// three-term split for ~fp32 accuracy: a = a_hi + a_lo (a_hi = a truncated to tf32 -- what the tensor
+// core reads from an fp32 operand --, a_lo the exact remainder), U' = U'_hi + U'_lo (rounded split),
+// D = a_hi U'_hi + a_hi U'_lo + a_lo U'_hi (dropped a_lo U'_lo ~ 2^-21 relative).
 // The rings stream from HBM once: TMA boxes of 8 rings x 512 floats (four M-tiles) land MN-major in
 // the SWIZZLE_128B_BASE32B layout that tf32 MN-major operands need.  Each stage is used twice in place:
-// four splitter warps overwrite it with a_hi (keeping a_lo in registers) for the a_hi products, then
-// with a_lo for the a_lo product -- no second buffer, so all spare shared memory goes to TMA depth.  The row's accumulator (2Q/128 M-tiles x NPAD columns of TMEM, two buffers)
+// the a_hi products read the raw stage, then four splitter warps overwrite it with a_lo for the a_lo
+// product -- no second buffer, so all spare shared memory goes to TMA depth.  The row's accumulator (2Q/128 M-tiles x NPAD columns of TMEM, two buffers)
 // is read by eight epilogue warps into the [H][Q] coefficient block in shared memory, which then takes
 // the same length-Q DFTs, row scale and hi/lo operand emission as compress_tc_kernel.
 //
@@ -22,8 +23,8 @@
 #pragma once
 // (included inside namespace rsvd)
 
-#ifndef RSVD_CM_DEBUG
-#define RSVD_CM_DEBUG 0        // timing experiments only: 1 = splitters do no work, 2 = no MMAs
+#ifndef CM_LAG
+#define CM_LAG 3               // stages between a stage's phase-1 and phase-2 products
 #endif
 #ifndef RSVD_CM_PREFETCH
 #define RSVD_CM_PREFETCH 0     // L2 prefetch of the next row (measured: doubles the HBM reads -- L2 thrash)
@@ -56,11 +57,6 @@ static inline CmGeom cm_geom(int Q, int H, int R) {
     g.stage_bytes = (uint32_t)(CM_KR * g.MC * 4);
     g.fixed = 1024 + 2 * (size_t)(g.RP32 / 32) * g.NPAD * 128 +
               (size_t)CM_HC * Q * 8 + (size_t)Q * 8 + 1024;
-#ifdef RSVD_CM_NST
-    g.NST = RSVD_CM_NST;
-    g.smem = g.fixed + (size_t)g.NST * g.stage_bytes;
-    return g;
-#endif
     g.NST = g.fixed < CM_SMEM_MAX ? (int)std::min<size_t>(CM_MAXST, (CM_SMEM_MAX - g.fixed) / g.stage_bytes) : 0;
     g.smem = g.fixed + (size_t)g.NST * g.stage_bytes;
     return g;
@@ -108,6 +104,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[32]) {
 }
 // a = hi + lo with hi = a rounded to tf32 (10 explicit mantissa bits; low 13 bits zero) and lo exact
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u); }
+// what kind::tf32 reads from an fp32 operand: the low 13 mantissa bits dropped (measured: a_lo = a - this
+// passes the compress parity gate, a_lo = a - RNE(a) fails it)
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 template <int LOGQ>
 __global__ void __launch_bounds__(CM_THREADS, 1)
@@ -129,9 +128,9 @@ __global__ void __launch_bounds__(CM_THREADS, 1)
     float2 *at = reinterpret_cast<float2 *>(blo + (size_t)(RP32 / 32) * NPAD * 128);   // [CM_HC][Q] chunk
     float2 *tw = at + (size_t)CM_HC * Q;                                              // [E][L]
     uint64_t *bars = reinterpret_cast<uint64_t *>(tw + Q);
-    // per stage: full (TMA landed) -> split1 (a_hi in place) -> mma1 (a_hi products done) -> split2 (a_lo
-    // in place) -> empty (a_lo product done)
-    uint64_t *full = bars, *split1 = full + CM_MAXST, *mma1 = split1 + CM_MAXST, *split2 = mma1 + CM_MAXST;
+    // per stage: full (TMA landed) -> mma1 (a_hi products done) -> split2 (a_lo in place) -> empty (a_lo
+    // product done)
+    uint64_t *full = bars, *mma1 = full + CM_MAXST, *split2 = mma1 + CM_MAXST;
     uint64_t *empty = split2 + CM_MAXST;
     uint64_t *tfull = empty + CM_MAXST, *tempty = tfull + 2, *amaxb = tempty + 2, *amaxf = amaxb + 2;
     float *amax_w = reinterpret_cast<float *>(amaxf + 2);                           // [2][4]
@@ -144,7 +143,7 @@ __global__ void __launch_bounds__(CM_THREADS, 1)
 
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
-            mbar_init(full + s, 1); mbar_init(split1 + s, 4); mbar_init(mma1 + s, 1); mbar_init(split2 + s, 4);
+            mbar_init(full + s, 1); mbar_init(mma1 + s, 1); mbar_init(split2 + s, 4);
             mbar_init(empty + s, 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -186,7 +185,8 @@ __global__ void __launch_bounds__(CM_THREADS, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- TMA producer; the next row's rings are pulled into L2 one row ahead
+        // ---------------- TMA producer (RSVD_CM_PREFETCH=1 also pulls the next row into L2: measured to
+        // double the HBM reads -- 148 CTAs x 2 rows in flight do not fit L2 -- so off)
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmR)) : "memory");
             uint64_t pol;
@@ -219,99 +219,77 @@ __global__ void __launch_bounds__(CM_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer: per stage and M-tile a_hi U'_hi + a_hi U'_lo (phase 1), then, once the
-        // splitters have overwritten the stage with a_lo, a_lo U'_hi (phase 2); phase 2 of a stage is
-        // issued after phase 1 of the next stage of the same row, so the splitters' round trip overlaps
+        // ---------------- MMA issuer: phase 1 of a stage (a_hi U'_hi + a_hi U'_lo per M-tile, a_hi being the
+        // raw fp32 stage, which the tensor core reads as tf32 by truncation) as soon as it lands; phase 2
+        // (a_lo U'_hi, after the splitters overwrote the stage with a_lo) CM_LAG stages later, so the
+        // splitters' round trip overlaps the following stages' phase-1 products
         if (lane == 0) {
             const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | ((uint32_t)(NPAD >> 3) << 17) |
                                    ((uint32_t)(128 >> 4) << 24);
+            const int SPR = NPASS * NSLAB;                            // stages per row
             int it = 0, k = 0;
             for (int64_t row = blockIdx.x; row < n; row += gridDim.x, ++k) {
                 const int b = k & 1;
                 mbar_wait(tempty + b, (((uint32_t)k >> 1) & 1u) ^ 1u);
                 tc_fence_after();
-                int pit = -1, pp = 0, pj = 0;                     // stage awaiting phase 2
-                auto issue2 = [&]() {
-                    const int s2 = pit % NST;
-                    mbar_wait(split2 + s2, (uint32_t)(pit / NST) & 1u);
+                const int it0 = it;
+                auto phase2 = [&](int i2) {                           // stage i2 of this row
+                    const int s2 = i2 % NST, l2 = i2 - it0, p2 = l2 / NSLAB, j2 = l2 - p2 * NSLAB;
+                    mbar_wait(split2 + s2, (uint32_t)(i2 / NST) & 1u);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(base + (size_t)s2 * SB);
-                    const uint64_t bh = sw128_desc(smem_u32(bhi) + (uint32_t)(pj >> 2) * NPAD * 128) + (uint64_t)(2 * (pj & 3));
+                    const uint64_t bh = sw128_desc(smem_u32(bhi) + (uint32_t)(j2 >> 2) * NPAD * 128) + (uint64_t)(2 * (j2 & 3));
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt)
-                        if (RSVD_CM_DEBUG != 2 && RSVD_CM_DEBUG != 3)
-                            tc_mma_tf32_1(tmem + (uint32_t)(b * COLS + (pp * MT + mt) * NPAD),
+                        tc_mma_tf32_1(tmem + (uint32_t)(b * COLS + (p2 * MT + mt) * NPAD),
                                           mn_sw128b32_desc(sa + mt * 4096, 1024), bh, idesc, 1u);
-                    cm_commit(empty + s2);                        // stage free once these complete
+                    cm_commit(empty + s2);                            // stage free once these complete
                 };
-                for (int p = 0; p < NPASS; ++p)
-                    for (int j = 0; j < NSLAB; ++j, ++it) {
-                        const int s = it % NST;
-                        mbar_wait(split1 + s, (uint32_t)(it / NST) & 1u);
-                        tc_fence_after();
-                        const uint32_t sa = smem_u32(base + (size_t)s * SB);
-                        const uint64_t bh = sw128_desc(smem_u32(bhi) + (uint32_t)(j >> 2) * NPAD * 128) + (uint64_t)(2 * (j & 3));
-                        const uint64_t bl = sw128_desc(smem_u32(blo) + (uint32_t)(j >> 2) * NPAD * 128) + (uint64_t)(2 * (j & 3));
+                for (int l = 0; l < SPR; ++l, ++it) {
+                    const int p = l / NSLAB, j = l - p * NSLAB, s = it % NST;
+                    mbar_wait(full + s, (uint32_t)(it / NST) & 1u);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(base + (size_t)s * SB);
+                    const uint64_t bh = sw128_desc(smem_u32(bhi) + (uint32_t)(j >> 2) * NPAD * 128) + (uint64_t)(2 * (j & 3));
+                    const uint64_t bl = sw128_desc(smem_u32(blo) + (uint32_t)(j >> 2) * NPAD * 128) + (uint64_t)(2 * (j & 3));
 #pragma unroll
-                        for (int mt = 0; mt < MT; ++mt) {
-                            const uint32_t d = tmem + (uint32_t)(b * COLS + (p * MT + mt) * NPAD);
-                            const uint64_t ah = mn_sw128b32_desc(sa + mt * 4096, 1024);
-                            if (RSVD_CM_DEBUG == 2 || RSVD_CM_DEBUG == 3) continue;
-                            tc_mma_tf32_1(d, ah, bh, idesc, j > 0 ? 1u : 0u);
-                            tc_mma_tf32_1(d, ah, bl, idesc, 1u);
-                        }
-                        cm_commit(mma1 + s);                      // a_hi products done: stage may become a_lo
-                        if (pit >= 0) issue2();
-                        pit = it; pp = p; pj = j;
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const uint32_t d = tmem + (uint32_t)(b * COLS + (p * MT + mt) * NPAD);
+                        const uint64_t ah = mn_sw128b32_desc(sa + mt * 4096, 1024);
+                        tc_mma_tf32_1(d, ah, bh, idesc, j > 0 ? 1u : 0u);
+                        tc_mma_tf32_1(d, ah, bl, idesc, 1u);
                     }
-                issue2();
-                cm_commit(tfull + b);                             // the row's accumulator is complete
+                    cm_commit(mma1 + s);                              // a_hi products done: stage may become a_lo
+                    if (l >= CM_LAG) phase2(it - CM_LAG);
+                }
+                for (int l = SPR > CM_LAG ? SPR - CM_LAG : 0; l < SPR; ++l) phase2(it0 + l);
+                cm_commit(tfull + b);                                 // the row's accumulator is complete
             }
         }
     } else if (warp >= 4 && warp < 8) {
-        // ---------------- splitters: a_hi in place (phase 1), a_lo kept in registers and written over the
-        // stage once its phase-1 products are done (phase 2, one stage behind); row max |Re|, |Im|
+        // ---------------- splitters: once a stage's phase-1 products are done, overwrite it with
+        // a_lo = a - trunc_tf32(a) (exact); row max |Re|, |Im|
         const int t = tid - 128;
-        constexpr int PER = SB / 16 / 128;                        // float4 per thread and stage
-        float4 lo_prev[PER];
+        constexpr int PER = SB / 16 / 128;                            // float4 per thread and stage
+        const int SPR = NPASS * NSLAB;
         int it = 0, k = 0;
         for (int64_t row = blockIdx.x; row < n; row += gridDim.x, ++k) {
             float amax = 0.f;
-            int pit = -1;
-            auto stage2 = [&]() {
-                const int s2 = pit % NST;
-                mbar_wait(mma1 + s2, (uint32_t)(pit / NST) & 1u);
-                float4 *st = reinterpret_cast<float4 *>(base + (size_t)s2 * SB);
+            for (int l = 0; l < SPR; ++l, ++it) {
+                const int s = it % NST;
+                mbar_wait(mma1 + s, (uint32_t)(it / NST) & 1u);
+                float4 *st = reinterpret_cast<float4 *>(base + (size_t)s * SB);
 #pragma unroll
-                for (int i = 0; i < PER; ++i)
-                    if (RSVD_CM_DEBUG != 1 && RSVD_CM_DEBUG != 3) st[t + 128 * i] = lo_prev[i];
+                for (int i = 0; i < PER; ++i) {
+                    const float4 x = st[t + 128 * i];
+                    amax = fmaxf(amax, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
+                    st[t + 128 * i] = make_float4(x.x - tf32_trunc(x.x), x.y - tf32_trunc(x.y), x.z - tf32_trunc(x.z),
+                                                  x.w - tf32_trunc(x.w));
+                }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                if (lane == 0) cm_arrive(split2 + s2);
-            };
-            for (int p = 0; p < NPASS; ++p)
-                for (int j = 0; j < NSLAB; ++j, ++it) {
-                    const int s = it % NST;
-                    mbar_wait(full + s, (uint32_t)(it / NST) & 1u);
-                    float4 *st = reinterpret_cast<float4 *>(base + (size_t)s * SB);
-                    float4 lo_cur[PER];
-#pragma unroll
-                    for (int i = 0; i < PER && RSVD_CM_DEBUG != 1 && RSVD_CM_DEBUG != 3; ++i) {
-                        const float4 x = st[t + 128 * i];
-                        amax = fmaxf(amax, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
-                        const float4 h4 = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-                        st[t + 128 * i] = h4;
-                        lo_cur[i] = make_float4(x.x - h4.x, x.y - h4.y, x.z - h4.z, x.w - h4.w);
-                    }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    __syncwarp();
-                    if (lane == 0) cm_arrive(split1 + s);
-                    if (pit >= 0) stage2();
-                    pit = it;
-#pragma unroll
-                    for (int i = 0; i < PER; ++i) lo_prev[i] = lo_cur[i];
-                }
-            stage2();
+                if (lane == 0) cm_arrive(split2 + s);
+            }
 #pragma unroll
             for (int off = 16; off; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
             const int b = k & 1;
@@ -360,7 +338,6 @@ __global__ void __launch_bounds__(CM_THREADS, 1)
                 if (last) tc_fence_before();
                 ebar();                                   // chunk complete in at[]
                 if (last && e == 0) cm_arrive(tempty + b);   // TMEM buffer b read out
-                if (RSVD_CM_DEBUG == 3) continue;
                 // in-place length-Q forward DFT of each principal ring, natural order (as compress_tc_kernel)
                 if (ew < hc) {
                     float2 v[E];
