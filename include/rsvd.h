@@ -196,6 +196,16 @@ rsvd_status rsvd_compress_translated(const void *rings, int64_t n_base, int32_t 
 void rsvd_set_precision(int32_t precision);
 int32_t rsvd_precision(void);
 
+/* Step 1 kernel choice on the TC layout (row a1).  mode 1 (default, also
+ * RSVD_COMPRESS_MMA unset): the tensor-core projection (compress_mma_kernel: tcgen05 kind::tf32 with a
+ * three-term split, ~fp32 accuracy) where the shape fits (2Q >= 256, H <= 32, 4 | H when H > 8,
+ * R <= 256, un-translated rows) and measurement says it is faster (H > 16, or H = 16 at Q <= 256);
+ * mode 2: that kernel wherever the shape fits; mode 0: always the FFMA2 projection (compress_tc_kernel).
+ * Both write the same operand layout to the same accuracy gate.  Process-global; no error return.
+ * rsvd_compress_mma_mode: the current mode. */
+void rsvd_set_compress_mma(int32_t mode);
+int32_t rsvd_compress_mma_mode(void);
+
 /* ------------------------------------------------------------------ rows a2-a4: align
  * Step 2: S_q[m,t] = sum_h conj(A_q[m,h]) B_q[t,h] for all q;
  * Step 3: X_k = 2 pi sum_q e^{-2 pi i q k/Q} S_q, k = 0..Q-1 (forward sign, G3);

@@ -26,6 +26,8 @@ SIGNATURES = [
     ("rsvd_set_path", None, [_I32]),
     ("rsvd_set_precision", None, [_I32]),
     ("rsvd_precision", _I32, []),
+    ("rsvd_set_compress_mma", None, [_I32]),
+    ("rsvd_compress_mma_mode", _I32, []),
     ("rsvd_kernel_chunk", _I64, []),
     ("rsvd_kernel_partials_bytes", _I64, [_I64, _I32]),
     ("rsvd_align_workspace_bytes", _I64, [_I64, _I64, _I32, _I32]),

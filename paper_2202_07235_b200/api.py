@@ -50,6 +50,15 @@ def precision() -> int:
     return int(_lib.lib().rsvd_precision())
 
 
+def set_compress_mma(mode: int):
+    """rsvd_set_compress_mma: 1 auto (default), 2 force the tensor-core projection, 0 force the FFMA2 one."""
+    _lib.lib().rsvd_set_compress_mma(int(mode))
+
+
+def compress_mma_mode() -> int:
+    return int(_lib.lib().rsvd_compress_mma_mode())
+
+
 def set_path(path: int):
     _lib.lib().rsvd_set_path(int(path))
 

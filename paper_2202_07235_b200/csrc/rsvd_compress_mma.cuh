@@ -397,12 +397,27 @@ static cudaError_t launch_compress_mma_q(const CUtensorMap &tm, const float2 *ri
     return cudaGetLastError();
 }
 
-// Projection on the tensor cores where the shape fits (RSVD_COMPRESS_MMA=0 forces compress_tc_kernel).
+static std::atomic<int> g_compress_mma{-1};
+static int compress_mma_mode() {
+    int m = g_compress_mma.load(std::memory_order_relaxed);
+    if (m < 0) {
+        const char *e = getenv("RSVD_COMPRESS_MMA");
+        m = e ? atoi(e) : 1;
+        g_compress_mma.store(m, std::memory_order_relaxed);
+    }
+    return m;
+}
+// Projection on the tensor cores where the shape fits and it is faster (RSVD_COMPRESS_MMA=0 forces
+// compress_tc_kernel, =2 forces this kernel wherever the shape fits -- the tests use it).
 static cudaError_t launch_compress_mma(const float2 *rings, int64_t n, int R, int Q, const double *w, const double *U,
                                        int H, int side, float *blocks, cudaStream_t s, bool *launched) {
     *launched = false;
-    static const int env = [] { const char *e = getenv("RSVD_COMPRESS_MMA"); return e ? atoi(e) : 1; }();
-    if (!env || !cm_supported(Q, H, R)) return cudaSuccess;
+    const int env = compress_mma_mode();
+    // measured crossover (tools/gpu_compress_ab.sh): the FFMA2 projection of compress_tc_kernel is cheaper
+    // at small H (H = 8: 2.26 vs 3.02 ms on Large-shape rows), the tensor cores win from H = 16 at
+    // Q = 256 and above H = 16 at Q = 512 (H = 24: 3.27 vs 4.21 ms; H = 32, Q = 256: 0.41 vs 0.64 ms)
+    const bool wins = H > 16 || (H == 16 && Q <= 256);
+    if (!env || !cm_supported(Q, H, R) || (env == 1 && !wins)) return cudaSuccess;    // 2: force
     CUtensorMap tm;
     if (make_rings_tmap(&tm, rings, n, R, Q) != cudaSuccess) return cudaSuccess;    // shape the TMA cannot map
     cudaError_t e;

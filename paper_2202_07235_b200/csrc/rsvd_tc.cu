@@ -801,4 +801,8 @@ extern "C" void rsvd_set_precision(int32_t precision) {
     rsvd::g_precision.store(precision == rsvd::PREC_FAST ? rsvd::PREC_FAST : rsvd::PREC_FP32);
 }
 extern "C" int32_t rsvd_precision(void) { return rsvd::resolve_precision(); }
+extern "C" void rsvd_set_compress_mma(int32_t mode) {
+    rsvd::g_compress_mma.store(mode < 0 || mode > 2 ? 1 : mode, std::memory_order_relaxed);
+}
+extern "C" int32_t rsvd_compress_mma_mode(void) { return rsvd::compress_mma_mode(); }
 extern "C" int32_t rsvd_path_for(int32_t Q, int32_t H) { return rsvd::resolve_path(Q, H); }

@@ -106,7 +106,15 @@ def test_basis_parity_and_determinism():
             assert np.linalg.norm(P - Pr, 2) <= 1e-10 / relgap, (name, h, relgap)
 
 
-def test_compress_parity():
+@pytest.fixture(params=[1, 2, 0], ids=["auto", "mma", "ffma"])
+def compress_mode(request):
+    """Step 1 kernel choice (rsvd_set_compress_mma): auto, tensor-core projection forced, FFMA2 forced."""
+    api.set_compress_mma(request.param)
+    yield request.param
+    api.set_compress_mma(1)
+
+
+def test_compress_parity(compress_mode):
     d = make_dataset("small", M=40, T=24)
     A, B, w = to_np(d.images), to_np(d.templates), to_np(d.w)
     for H, rings, side in [(8, A, api.SIDE_IMAGE), (8, B, api.SIDE_TEMPLATE), (12, A, api.SIDE_IMAGE),
@@ -118,6 +126,27 @@ def test_compress_parity():
         want = np.einsum("rh,nrq->nqh", U * np.sqrt(w)[:, None], coef)
         err = np.abs(got - want).max() / np.abs(want).max()
         assert err <= 2e-6, err
+
+
+@pytest.mark.parametrize("Q,R,H,n", [(256, 40, 6, 9), (512, 100, 16, 5), (1024, 24, 12, 3), (512, 128, 32, 4),
+                                     (128, 16, 3, 7), (512, 128, 24, 150)])
+def test_compress_shapes(Q, R, H, n, compress_mode):
+    """Compress (both sides) against the oracle's coefficients on shapes that exercise the tensor-core
+    projection's edges: R not a multiple of the 8-ring stage (TMA zero fill), H not a multiple of 4 in
+    one epilogue chunk, several chunks, Q = 1024 (four passes), N padded to 16 / 32, more rows than SMs."""
+    rng = np.random.default_rng(1000 + Q + R + H)
+    rings = (rng.standard_normal((n, R, Q)) + 1j * rng.standard_normal((n, R, Q))).astype(np.complex64)
+    rings *= np.exp(rng.uniform(-3, 3, (n, 1, 1))).astype(np.float32)        # rows of very different scale
+    U = np.linalg.qr(rng.standard_normal((R, H)))[0]
+    w = radial_grid(R)[1]
+    coef = ref.fb_coefficients(rings)
+    want = np.einsum("rh,nrq->nqh", U * np.sqrt(w)[:, None], coef)
+    for side in (api.SIDE_IMAGE, api.SIDE_TEMPLATE):
+        blocks = api.compress(cuda(rings), cuda(w, torch.float64), cuda(U, torch.float64), side)
+        got = to_np(api.blocks_unpack(blocks, n, Q, H, side))
+        for i in range(n):                                   # gate per row (each row has its own scale)
+            err = np.abs(got[i] - want[i]).max() / np.abs(want[i]).max()
+            assert err <= 2e-6, (side, i, err)
 
 
 def test_small_full_argmax_sampled_pairs():
