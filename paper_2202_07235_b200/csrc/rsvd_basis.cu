@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "rsvd_common.cuh"
@@ -119,19 +120,27 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
             si[tid][0] += sr; si[tid][1] += sim;
             sj[tid][0] += tr; sj[tid][1] += tim;
         }
-        // Gram: Re(x_r conj(x_r')) = xr xr' + xi xi'
+        // Gram: Re(x_r conj(x_r')) = xr xr' + xi xi'.  On a diagonal tile only r >= r' is ever read
+        // (kernel_reduce_kernel takes the lower triangle), so register entries (a, b) whose rows all lie
+        // above their columns for every thread (ty + 8a < 16b, i.e. a < 2b) are skipped: 12 of 32.
+        auto gram = [&](auto diag_c) {
+            constexpr bool DIAG = decltype(diag_c)::value;
 #pragma unroll 4
-        for (int jj = 0; jj < JB; ++jj) {
-            double2 av[KA], bv[KBB];
+            for (int jj = 0; jj < JB; ++jj) {
+                double2 av[KA], bv[KBB];
 #pragma unroll
-            for (int a = 0; a < KA; ++a) av[a] = xi[ty + 8 * a][jj];
+                for (int a = 0; a < KA; ++a) av[a] = xi[ty + 8 * a][jj];
 #pragma unroll
-            for (int b = 0; b < KBB; ++b) bv[b] = xj[tx + 16 * b][jj];
+                for (int b = 0; b < KBB; ++b) bv[b] = xj[tx + 16 * b][jj];
 #pragma unroll
-            for (int a = 0; a < KA; ++a)
+                for (int a = 0; a < KA; ++a)
 #pragma unroll
-                for (int b = 0; b < KBB; ++b) acc[a][b] = fma(av[a].x, bv[b].x, fma(av[a].y, bv[b].y, acc[a][b]));
-        }
+                    for (int b = 0; b < KBB; ++b)
+                        if (!DIAG || a >= 2 * b) acc[a][b] = fma(av[a].x, bv[b].x, fma(av[a].y, bv[b].y, acc[a][b]));
+            }
+        };
+        if (ti == tj) gram(std::true_type{});
+        else gram(std::false_type{});
         if (sl == nslab_t - 1) {
             __syncthreads();                               // every row sum of this template is complete
             // remove the angular mean: - (1/Q) Re(S_r conj(S_r'))
