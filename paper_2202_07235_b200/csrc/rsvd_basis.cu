@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
 #pragma unroll
         for (int b = 0; b < KBB; ++b) {
             const int r1 = ti * BT + ty + 8 * a, r2 = tj * BT + tx + 16 * b;
-            if (r1 < R && r2 < R) out[(int64_t)r1 * R + r2] = acc[a][b];
+            if (r1 < R && r2 < R && r1 >= r2) out[(int64_t)r1 * R + r2] = acc[a][b];   // lower triangle only
         }
 }
 constexpr size_t KP_SMEM = 2 * (size_t)BT * (JB + 1) * sizeof(double2) + 2 * (size_t)BT * JB * sizeof(float2);
