@@ -25,15 +25,23 @@
 
 namespace rsvd {
 
-template <int LOGN, int EB = 4>          // EB: bytes per spectrum element (4 = fp32, 2 = fp16 fast path)
+#ifndef RSVD_FFT2_ONECOL
+#define RSVD_FFT2_ONECOL 0      // 1: pass 1 with one column per warp (1024 threads, <= 64 registers); measured slower
+#endif
+
+// EB: bytes per spectrum element (4 = fp32, 2 = fp16 fast path).  ONE: pass 1 with one column per warp
+// (N1 warps per group, 1024 threads per CTA) instead of one mirror column pair per warp (N1/2 warps,
+// 512 threads): half the registers per thread, so twice the warps hide the FP and shared-memory latency,
+// at the cost of forming each Z value pair twice (once per mirror column).
+template <int LOGN, int EB = 4, bool ONE = false>
 struct Fft2Cfg {
     static constexpr int N = 1 << LOGN;
     static constexpr int Q = 2 * N;
     static constexpr int N1 = 1 << (LOGN / 2);        // columns (pass-2 length)
     static constexpr int N2 = N / N1;                 // rows (pass-1 length), N2 in {N1, 2 N1}
-    static constexpr int TASKS = N1 / 2;              // warps per group
+    static constexpr int TASKS = ONE ? N1 : N1 / 2;   // warps per group
     static constexpr int GT = 32 * TASKS;             // threads per group
-    static constexpr int G = 16 / TASKS;              // groups per CTA (512 threads)
+    static constexpr int G = (ONE ? 32 : 16) / TASKS; // groups per CTA (1024 / 512 threads)
     static constexpr int THREADS = G * GT;
     static constexpr int TB = 32;                     // images per item (lane = image)
     static constexpr int ROWS = 2 * N;                // re plane rows, then im plane rows
@@ -70,24 +78,67 @@ template <> __device__ __forceinline__ float spec_f<float>(float x) { return x; 
 template <> __device__ __forceinline__ float spec_f<__half>(__half x) { return __half2float(x); }
 template <class Tin> constexpr float spec_unscale() { return sizeof(Tin) == 2 ? 1048576.0f : 1.0f; }
 
-template <int LOGN, int MODE, class Release, class Tin = float>
+template <int LOGN, int MODE, class Release, class Tin = float, bool ONE = false>
 __device__ __forceinline__ void fft2_item(float *U, int gt, int warp, int lane, int gbar_id, const float2 *Wn,
                                           const float2 *Wq, int64_t m_first, int n_valid, int64_t t, float st,
-                                          const uint32_t (&stale)[Fft2Cfg<LOGN>::P2_PER],
-                                          const float (&smv)[Fft2Cfg<LOGN>::P2_PER], const FftOut &out,
+                                          const uint32_t (&stale)[Fft2Cfg<LOGN, 4, ONE>::P2_PER],
+                                          const float (&smv)[Fft2Cfg<LOGN, 4, ONE>::P2_PER], const FftOut &out,
                                           Release release) {
-    using C = Fft2Cfg<LOGN>;
+    using C = Fft2Cfg<LOGN, 4, ONE>;
     constexpr int N = C::N, Q = C::Q, N1 = C::N1, N2 = C::N2, TB = C::TB, SZ = C::SZ, GT = C::GT;
     float2 *ZY = reinterpret_cast<float2 *>(U);                           // [TB][SZ], in place after pass-1 reads
     auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(gbar_id), "n"(GT) : "memory"); };
     const float PI = 3.14159265358979323846f * spec_unscale<Tin>();
-    const int ca = warp == 0 ? 0 : warp;
-    const int cb = warp == 0 ? N1 / 2 : N1 - warp;
 
-    // ---- pass 1: Z from the ring, two DFTs of length N2
-    float2 za[N2], zb[N2];
+    // ---- pass 1: Z from the ring, DFTs of length N2 (one column per warp, or a mirror column pair)
     const Tin *Ui = reinterpret_cast<const Tin *>(U);
     auto ld = [&](int n) { return make_float2(spec_f<Tin>(Ui[n * TB + lane]), spec_f<Tin>(Ui[(N + n) * TB + lane])); };
+    if constexpr (ONE) {
+        float2 za[N2];
+        const int c = warp;                                // column c: rows c + N1 n2
+        if (c == 0) {
+            const float2 u0 = ld(0);                       // (U_0, U_N) packed
+            za[0] = make_float2(u0.x + u0.y, u0.x - u0.y);
+            const float2 uh = ld(N / 2);
+            za[N2 / 2] = make_float2(2.f * uh.x, 2.f * uh.y);
+#pragma unroll
+            for (int n2 = 1; n2 < N2 / 2; ++n2) z_pair(ld(N1 * n2), ld(N1 * (N2 - n2)), Wq[N1 * n2], za[n2], za[N2 - n2]);
+        } else if (c == N1 / 2) {
+#pragma unroll
+            for (int n2 = 0; n2 < N2 / 2; ++n2) {
+                const int r = N1 / 2 + N1 * n2;
+                z_pair(ld(r), ld(N - r), Wq[r], za[n2], za[N2 - 1 - n2]);
+            }
+        } else {
+            // Z_r for r = c + N1 n2: from (U_r, U_{N-r}) with W_Q^r when r < N/2 (n2 < N2/2), else as the
+            // mirror output of the pair at r' = N - r < N/2 (the mirror column's warp forms the same pair)
+#pragma unroll
+            for (int n2 = 0; n2 < N2; ++n2) {
+                const int r = c + N1 * n2;
+                float2 zr, zm;
+                if (n2 < N2 / 2) {
+                    z_pair(ld(r), ld(N - r), Wq[r], zr, zm);
+                    za[n2] = zr;
+                } else {
+                    z_pair(ld(N - r), ld(r), Wq[N - r], zr, zm);
+                    za[n2] = zm;
+                }
+            }
+        }
+        gbar();                                            // (A) every U read: slot becomes ZY
+        dif4<N2>(za);
+        float2 *yw = ZY + lane * SZ + c;
+        const float2 *tw = Wn + c * N2;
+#pragma unroll
+        for (int k1 = 0; k1 < N2; ++k1) {
+            float2 x = za[dpos4<N2>(k1)];
+            if (k1) x = c_mul(x, tw[k1]);
+            yw[k1 * C::SK] = x;
+        }
+    } else {
+    float2 za[N2], zb[N2];
+    const int ca = warp == 0 ? 0 : warp;
+    const int cb = warp == 0 ? N1 / 2 : N1 - warp;
     if (warp == 0) {
         // column 0: rows N1*n2; pairs (n2, N2 - n2); n2 = 0 -> Z_0, n2 = N2/2 -> Z_{N/2}
         {
@@ -129,6 +180,7 @@ __device__ __forceinline__ void fft2_item(float *U, int gt, int warp, int lane, 
             ywa[k1 * C::SK] = xa;
             ywb[k1 * C::SK] = xb;
         }
+    }
     }
     gbar();                                                // (B) ZY complete
 
@@ -221,10 +273,11 @@ __device__ __forceinline__ void fft2_item(float *U, int gt, int warp, int lane, 
 
 // per-image side data of an item's pass-2 tasks (image scale; MODE_IMAGE: the image's current key),
 // fetched before the item's data wait so its latency hides behind it
-template <int LOGN, int MODE>
+template <int LOGN, int MODE, bool ONE = false>
 __device__ __forceinline__ void fft2_side(int gt, int64_t m_first, int n_valid, const FftOut &out,
-                                          uint32_t (&stale)[Fft2Cfg<LOGN>::P2_PER], float (&smv)[Fft2Cfg<LOGN>::P2_PER]) {
-    using C = Fft2Cfg<LOGN>;
+                                          uint32_t (&stale)[Fft2Cfg<LOGN, 4, ONE>::P2_PER],
+                                          float (&smv)[Fft2Cfg<LOGN, 4, ONE>::P2_PER]) {
+    using C = Fft2Cfg<LOGN, 4, ONE>;
 #pragma unroll
     for (int j = 0; j < C::P2_PER; ++j) {
         const int p = (gt + C::GT * j) / C::N2;
@@ -248,12 +301,12 @@ __device__ __forceinline__ void fft2_tables(float2 *Wn, float2 *Wq, int tid, int
 }
 
 template <int LOGN, int MODE, class Tin = float>
-__global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(Fft2Cfg<LOGN, 4, RSVD_FFT2_ONECOL>::THREADS, 1) fft2_reduce_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                                int64_t m0, int64_t t0, int64_t mcv,
                                                                                int64_t tcv, FftOut out,
                                                                                float *__restrict__ Upk, int64_t Mc,
                                                                                int64_t Tc) {
-    using C = Fft2Cfg<LOGN, (int)sizeof(Tin)>;
+    using C = Fft2Cfg<LOGN, (int)sizeof(Tin), RSVD_FFT2_ONECOL>;
     constexpr int N = C::N, TB = C::TB, G = C::G, GT = C::GT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // pointer arithmetic on the __shared__ array (not an integer round trip) keeps LDS/STS addressing
@@ -327,7 +380,7 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
         const int n_valid = (int)(mcv - mb0 < TB ? mcv - mb0 : TB);
         uint32_t stale[C::P2_PER];
         float smv[C::P2_PER];
-        fft2_side<LOGN, MODE>(gt, m0 + mb0, n_valid, out, stale, smv);
+        fft2_side<LOGN, MODE, RSVD_FFT2_ONECOL>(gt, m0 + mb0, n_valid, out, stale, smv);
         while (tag[sl] != i) {}
         fr_mbar_wait(full + sl, (uint32_t)(i / C::NSLOT) & 1u);
         // the item's 2N spectrum rows (one 128-B line each: 32 images x fp32) are now in shared memory
@@ -350,8 +403,8 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN>::THREADS, 1) fft2_reduce_kernel(
                 issue(i + C::NSLOT);
             }
         };
-        fft2_item<LOGN, MODE, decltype(release), Tin>(U, gt, warp, lane, 1 + g, Wn, Wq, m0 + mb0, n_valid, t, st, stale,
-                                                       smv, out, release);
+        fft2_item<LOGN, MODE, decltype(release), Tin, RSVD_FFT2_ONECOL>(U, gt, warp, lane, 1 + g, Wn, Wq, m0 + mb0,
+                                                                         n_valid, t, st, stale, smv, out, release);
     }
 }
 
@@ -375,7 +428,7 @@ static cudaError_t make_spectrum_tmap2(CUtensorMap *tm, const float *Upk, int64_
 template <int LOGN, int MODE, class Tin = float>
 static cudaError_t launch_fft2_mode(cudaStream_t s, const CUtensorMap &tm, int64_t m0, int64_t t0, int64_t mcv,
                                     int64_t tcv, const FftOut &out, float *Upk, int64_t Mc, int64_t Tc) {
-    using C = Fft2Cfg<LOGN, (int)sizeof(Tin)>;
+    using C = Fft2Cfg<LOGN, (int)sizeof(Tin), RSVD_FFT2_ONECOL>;
     const size_t smem = C::smem_bytes();
     static std::atomic<uint64_t> attr{0};
     const cudaError_t e = smem_attr_once((const void *)fft2_reduce_kernel<LOGN, MODE, Tin>, (int)smem, attr);
