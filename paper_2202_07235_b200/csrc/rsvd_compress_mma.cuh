@@ -62,11 +62,12 @@ static inline CmGeom cm_geom(int Q, int H, int R) {
     return g;
 }
 // shapes: 2Q >= 256, H <= 32 with 4 | H once it takes more than one epilogue chunk (operand quarters
-// of 4 coefficients must not straddle chunks), at least 3 hi stages, both TMEM buffers in 512 columns
+// of 4 coefficients must not straddle chunks), more stages than the phase-2 lag, both TMEM buffers in
+// 512 columns
 static inline bool cm_supported(int Q, int H, int R) {
     if (2 * Q < 256 || 2 * Q > 2048 || H > 32 || (H > CM_HC && H % 4 != 0) || R > 256) return false;
     const CmGeom g = cm_geom(Q, H, R);
-    return g.ALLOC <= 512 && g.NST >= 3;
+    return g.ALLOC <= 512 && g.NST > CM_LAG;      // phase 2 of stage i is issued after phase 1 of i + CM_LAG
 }
 
 // UMMA descriptor, MN-major SWIZZLE_128B_BASE32B (tf32): 128-B MN rows (32 elements), 4-row K groups
