@@ -349,8 +349,18 @@ def run_ours(args):
         tbs_g = [torch.empty(max(api.block_bytes(T_loc, Q, H, api.SIDE_TEMPLATE), 16) // 4, dtype=torch.float32,
                              device=dev) for g in range(G_ctf)]
 
+    # NVTX ranges per SURVEY.md section 8 row (visible in nsys / ncu --nvtx timelines): one range per phase
+    nvtx_next = {"start": "a0 basis", "basis": "a1 compress", "compress": "a2-a4 align", "align": "combine"}
+
+    def nvtx_mark(name):
+        if name != "start":
+            torch.cuda.nvtx.range_pop()
+        if name in nvtx_next:
+            torch.cuda.nvtx.range_push(nvtx_next[name])
+
     def step_grouped(imgs, tmps, marks=None):
         def mark(name):
+            nvtx_mark(name)
             if marks is not None:
                 e = torch.cuda.Event(enable_timing=True)
                 e.record(stream)
@@ -379,6 +389,7 @@ def run_ours(args):
             return step_grouped(imgs, tmps, marks)
 
         def mark(name):
+            nvtx_mark(name)
             if marks is not None:
                 e = torch.cuda.Event(enable_timing=True)
                 e.record(stream)
