@@ -148,3 +148,19 @@ def test_grouped_align_validates_before_any_launch(lib):
     assert b"group 0" in lib.rsvd_last_error()
     assert lib.rsvd_align_argmax_grouped(ctypes.addressof(arr), 1, 48, 4, 0, None, 0, None) == 2   # Q not a power of 2
     assert lib.rsvd_align_argmax_grouped(ctypes.addressof(arr), 0, 64, 4, 0, None, 0, None) == 0
+
+
+def test_process_settings_roundtrip(lib):
+    """Host-only setters of include/rsvd.h: precision (0 / 1) and the Step-1 kernel choice (0 / 1 / 2,
+    out-of-range values fall back to the default 1); both are process-global and need no GPU."""
+    p0, c0 = lib.rsvd_precision(), lib.rsvd_compress_mma_mode()
+    try:
+        for v in (1, 0):
+            lib.rsvd_set_precision(v)
+            assert lib.rsvd_precision() == v
+        for v, want in ((2, 2), (0, 0), (7, 1), (-3, 1), (1, 1)):
+            lib.rsvd_set_compress_mma(v)
+            assert lib.rsvd_compress_mma_mode() == want
+    finally:
+        lib.rsvd_set_precision(p0)
+        lib.rsvd_set_compress_mma(c0)
