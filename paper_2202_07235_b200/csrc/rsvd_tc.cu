@@ -99,14 +99,15 @@ __device__ __forceinline__ void st_spectrum(float *p, float v, uint64_t pol) {
 // Items (tile, q-group) of one chunk, tile = (128-image tile mt_l < mtl, 256-template tile nt_l < ntl);
 // cluster c processes items c, c + nclusters, ...  Upk planar: re plane [(n*Tc + tl)*Mc + ml], im
 // plane at + N*Mc*Tc (floats); slot n = 0 packs (U_0, U_N).
+template <int fmt>      // compile-time spectrum format: one lean epilogue per format
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int steps, int KB, int N,
     int mtl, int ntl, int mt0, int nt0, int qg, int nqg, int nitems, int64_t Mc, int64_t Tc,
-    float *__restrict__ Upk, int Nout, int operands_fresh, int fmt) {
+    float *__restrict__ Upk, int Nout, int operands_fresh) {
     // fmt: spectrum format -- 0 fp32 planes; 1 fp16 planes (single-MMA fast path); 2 split fp16 hi/lo
     // planes for the tensor-core transform (rsvd_fftc.cuh): [n][part][t][m], part = re_hi, im_hi, re_lo,
     // im_lo, value = (hi + lo 2^-10) 2^20
-    const bool fast = fmt == 1;
+    constexpr bool fast = fmt == 1;
     extern __shared__ unsigned char smem_raw[];
     unsigned char *base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint64_t *bars = reinterpret_cast<uint64_t *>(base + TC_STAGES * TC_STAGE_BYTES);
@@ -260,13 +261,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
                         tmem_ld32(tbase + (uint32_t)(64 * b + 64), v[cur ^ 1][0]);
                         tmem_ld32(tbase + (uint32_t)(64 * b + 96), v[cur ^ 1][1]);
                     }
-                    if (store && fmt == 0) {
+                    if constexpr (fmt == 0) {
+                        if (store) {
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
 #pragma unroll
                             for (int i = 0; i < 32; ++i)
                                 st_spectrum(dst + (int64_t)(64 * b + 32 * h + i) * Mc, qs * __uint_as_float(v[cur][h][i]), pol_ws);
-                    } else if (store && fmt == 2) {
+                        }
+                    } else if (fmt == 2 && store) {
                         // split hi/lo fp16 (same 4 B per value): hi = fp16(x), lo = fp16(x - hi), x = v 2^-20
                         const bool imv = (nyq_packed || (q != 0 && q != N && !re_rows));
                         __half *sp = reinterpret_cast<__half *>(Upk) +
@@ -761,9 +764,10 @@ cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t ro
 cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, int H, int N, int Nout, int64_t m0,
                                int64_t t0, int64_t mc, int64_t tc, int64_t Mc, int64_t Tc, float *Upk, int nsms,
                                bool operands_fresh, int fmt, cudaStream_t s) {
-    static std::atomic<uint64_t> attr{0};
+    static std::atomic<uint64_t> attr0{0}, attr1{0}, attr2{0};
+    auto kern = fmt == 1 ? contract_tc_kernel<1> : (fmt == 2 ? contract_tc_kernel<2> : contract_tc_kernel<0>);
     {
-        const cudaError_t e = smem_attr_once((const void *)contract_tc_kernel, (int)TC_SMEM, attr);
+        const cudaError_t e = smem_attr_once((const void *)kern, (int)TC_SMEM, fmt == 1 ? attr1 : (fmt == 2 ? attr2 : attr0));
         if (e != cudaSuccess) return e;
     }
     const int mtl = (int)(mc / TC_PIMG), ntl = (int)(tc / TC_TT);
@@ -787,9 +791,9 @@ cudaError_t launch_contract_tc(const CUtensorMap &tmA, const CUtensorMap &tmB, i
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, contract_tc_kernel, tmA, tmB, tc_steps(H), tc_kb(H), N, mtl, ntl,
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tc_steps(H), tc_kb(H), N, mtl, ntl,
                                        (int)(m0 / TC_PIMG), (int)(t0 / TC_TT), qg, nqg, nitems, Mc, Tc, Upk, Nout,
-                                       operands_fresh ? 1 : 0, fmt);
+                                       operands_fresh ? 1 : 0);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
