@@ -239,7 +239,11 @@ static rsvd_status run_align(const AlignArgs &a, cudaStream_t s) {
     const int64_t ntiles = a.work_bytes / tile_bytes;
     if (ntiles < 1) return fail(RSVD_ERR_ARG, "workspace smaller than rsvd_align_min_workspace_bytes(Q)");
     const int64_t tmax = Tpad / TT, mmax = Mpad / TM;
-    int64_t tct = std::min<int64_t>(tmax, tc ? 1 : std::max<int64_t>(1, (int64_t)std::sqrt((double)ntiles)));
+    // TC: template tiles per chunk (RSVD_TCT, experiment override; default 1 -- the chunk's image tiles
+    // share one template tile whose operands stay in L2 while image operands stream)
+    const char *tct_e = getenv("RSVD_TCT");
+    const int64_t tct_tc = tct_e ? std::max(1, atoi(tct_e)) : 1;
+    int64_t tct = std::min<int64_t>(tmax, tc ? std::min(tct_tc, ntiles) : std::max<int64_t>(1, (int64_t)std::sqrt((double)ntiles)));
     int64_t mct = std::min(mmax, std::max<int64_t>(1, ntiles / tct));
     tct = std::min(tmax, std::max(tct, ntiles / mct));      // widen t when rows run out
     const int64_t Mc = mct * TM, Tc = tct * TT;

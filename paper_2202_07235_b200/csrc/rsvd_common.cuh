@@ -88,6 +88,40 @@ inline int num_sms() {
     return n;
 }
 
+// ------------------------------------------------------------------ optional CTA timeline (-DRSVD_TRACE)
+// Diagnostic build only (tools/trace_align.py): every CTA of the two align kernels appends one record
+// of %globaltimer stamps (entry, dependency wait passed, first work item ready, exit) to a per-TU
+// device buffer, dumped by rsvd_trace_dump_<tu>.  Compiled out of the product library.
+struct TraceRec { unsigned long long t0, t1, t2, t3; unsigned int kind_blk, key; };
+#ifdef RSVD_TRACE
+constexpr int TRACE_MAX = 1 << 20;
+__device__ __forceinline__ unsigned long long trace_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define RSVD_TRACE_DEFINE(tu)                                                                          \
+    static __device__ TraceRec g_trace[TRACE_MAX];                                                     \
+    static __device__ unsigned int g_trace_n;                                                          \
+    __device__ __forceinline__ void trace_put(const TraceRec &r) {                                     \
+        const unsigned i = atomicAdd(&g_trace_n, 1u);                                                  \
+        if (i < TRACE_MAX) g_trace[i] = r;                                                             \
+    }                                                                                                  \
+    extern "C" int rsvd_trace_dump_##tu(TraceRec *host, int max, int reset) {                          \
+        unsigned n = 0;                                                                                \
+        if (cudaDeviceSynchronize() != cudaSuccess) return -1;                                         \
+        if (cudaMemcpyFromSymbol(&n, g_trace_n, sizeof(n)) != cudaSuccess) return -1;                  \
+        n = n < (unsigned)TRACE_MAX ? n : (unsigned)TRACE_MAX;                                         \
+        n = n < (unsigned)max ? n : (unsigned)max;                                                     \
+        if (n && host && cudaMemcpyFromSymbol(host, g_trace, n * sizeof(TraceRec)) != cudaSuccess) return -1; \
+        if (reset) {                                                                                   \
+            const unsigned z = 0;                                                                      \
+            if (cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z)) != cudaSuccess) return -1;                \
+        }                                                                                              \
+        return (int)n;                                                                                 \
+    }
+#endif
+
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 inline int ilog2(int64_t x) {

@@ -25,6 +25,14 @@
 
 namespace rsvd {
 
+#ifdef RSVD_TRACE
+#ifdef RSVD_TRACE_TU_FUSED
+RSVD_TRACE_DEFINE(fused)
+#else
+RSVD_TRACE_DEFINE(fft)
+#endif
+#endif
+
 #ifndef RSVD_FFT2_ONECOL
 #define RSVD_FFT2_ONECOL 0      // 1: pass 1 with one column per warp (1024 threads, <= 64 registers); measured slower
 #endif
@@ -323,6 +331,11 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN, 4, RSVD_FFT2_ONECOL>::THREADS, 1
     const int tid = threadIdx.x;
     const int g = tid / GT, gt = tid - g * GT;
     const int warp = gt >> 5, lane = tid & 31;
+#ifdef RSVD_TRACE
+    __shared__ unsigned long long trs[4];
+    if (tid == 0) trs[0] = trace_now();
+    bool tr_first = true;
+#endif
     const int nmb = (int)((mcv + TB - 1) / TB);
     const int nitems = (int)tcv * nmb;
     const int grid = (int)gridDim.x;
@@ -359,6 +372,9 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN, 4, RSVD_FFT2_ONECOL>::THREADS, 1
     }
     fft2_tables<LOGN>(Wn, Wq, tid, C::THREADS);
     asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef RSVD_TRACE
+    if (tid == 0) trs[1] = trace_now();
+#endif
     if (tid == 0)
         for (int i = 0; i < C::NSLOT; ++i)
             if (item_of(i) < nitems) issue(i);
@@ -383,6 +399,10 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN, 4, RSVD_FFT2_ONECOL>::THREADS, 1
         fft2_side<LOGN, MODE, RSVD_FFT2_ONECOL>(gt, m0 + mb0, n_valid, out, stale, smv);
         while (tag[sl] != i) {}
         fr_mbar_wait(full + sl, (uint32_t)(i / C::NSLOT) & 1u);
+#ifdef RSVD_TRACE
+        if (tr_first && tid == 0) trs[2] = trace_now();
+        tr_first = false;
+#endif
         // the item's 2N spectrum rows (one 128-B line each: 32 images x fp32) are now in shared memory
         // and dead in HBM terms: drop them from L2 without write-back (the next chunk's contraction
         // rewrites every line before it is read again)
@@ -406,6 +426,16 @@ __global__ void __launch_bounds__(Fft2Cfg<LOGN, 4, RSVD_FFT2_ONECOL>::THREADS, 1
         fft2_item<LOGN, MODE, decltype(release), Tin, RSVD_FFT2_ONECOL>(U, gt, warp, lane, 1 + g, Wn, Wq, m0 + mb0,
                                                                          n_valid, t, st, stale, smv, out, release);
     }
+#ifdef RSVD_TRACE
+    __syncthreads();
+    if (tid == 0) {
+        TraceRec r;
+        r.t0 = trs[0]; r.t1 = trs[1]; r.t2 = trs[2]; r.t3 = trace_now();
+        r.kind_blk = (1u << 24) | blockIdx.x;
+        r.key = ((unsigned)(m0 / 128) << 16) | (unsigned)(t0 / 256);
+        trace_put(r);
+    }
+#endif
 }
 
 // 3-D view of the planar workspace with 32-image boxes (the fft2 work item).

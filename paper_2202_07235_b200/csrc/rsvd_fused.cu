@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#define RSVD_TRACE_TU_FUSED
 #include "rsvd_common.cuh"
 #include "rsvd_fft2.cuh"
 #include "rsvd_tcgen05.cuh"

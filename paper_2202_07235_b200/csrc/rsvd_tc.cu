@@ -57,6 +57,9 @@ static PFN_encodeTiled_tc encode_fn() {
     return fn;
 }
 
+#ifdef RSVD_TRACE
+RSVD_TRACE_DEFINE(contract)
+#endif
 constexpr int TC_THREADS = 6 * 32;
 constexpr int TC_STAGES = 7;
 constexpr int TC_PIMG = 128;                        // images per CTA pair (64 per CTA)
@@ -117,6 +120,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = cluster_rank();
     const int cl = (int)(blockIdx.x >> 1), ncl = (int)(gridDim.x >> 1);
+#ifdef RSVD_TRACE
+    __shared__ unsigned long long trs[4];
+    if (tid == 0) trs[0] = trace_now();
+#endif
     // PDL: the next kernel (Step 3 on this chunk) may be scheduled as SMs free up; it waits for us.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
@@ -224,6 +231,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
         // PDL: operands are read-only, so TMA + MMA above may overlap the previous kernel's tail; the
         // workspace is only written after that kernel (Step 3 of the previous chunk) has finished.
         asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef RSVD_TRACE
+        if (warp == 2 && lane == 0) trs[1] = trace_now();
+        bool tr_first = true;
+#endif
         uint64_t pol_ws = 0;
 #if RSVD_WS_POLICY == 1
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_ws));
@@ -240,6 +251,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
                 const int acc = qi & 1;
                 mbar_wait(tfull + acc, ((uint32_t)qi >> 1) & 1u);
                 tc_fence_after();
+#ifdef RSVD_TRACE
+                if (tr_first && warp == 2 && lane == 0) trs[2] = trace_now();
+                tr_first = false;
+#endif
                 // q = 0: Re U_0 -> re plane slot 0; q = N: Re U_N -> im plane slot 0; Im rows of both dropped
                 const bool store = (q != 0 && q != N) || re_rows;
                 const bool nyq_packed = q == N && !padded;
@@ -307,6 +322,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) contr
     }
     tc_fence_before();
     cluster_sync_relaxed();
+#ifdef RSVD_TRACE
+    if (tid == 0) {
+        TraceRec r;
+        r.t0 = trs[0]; r.t1 = trs[1]; r.t2 = trs[2]; r.t3 = trace_now();
+        r.kind_blk = (0u << 24) | blockIdx.x;
+        r.key = ((unsigned)mt0 << 16) | (unsigned)nt0;
+        trace_put(r);
+    }
+#endif
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
