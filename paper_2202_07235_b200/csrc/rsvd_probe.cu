@@ -7,6 +7,7 @@
 //   kind 0  FFMA  (scalar, 3-register form)        2 flops per lane per instruction
 //   kind 1  FFMA2 (sm_100 packed fp32x2)           4 flops per lane per instruction
 //   kind 2  FADD2 (sm_100 packed fp32x2 add)        2 flops per lane per instruction
+//   kind 3  DFMA  (fp64)                            2 flops per lane per instruction (kernel-partials peak)
 #include <cuda_runtime.h>
 
 #include "rsvd_common.cuh"
@@ -44,6 +45,23 @@ __global__ void __launch_bounds__(PR_THREADS) fp32_probe_kernel(int iters, float
     if (s == 1234.5678f) sink[threadIdx.x] = s;      // never true in practice; keeps the chains live
 }
 
+__global__ void __launch_bounds__(PR_THREADS) fp64_probe_kernel(int iters, double seed, double *__restrict__ sink) {
+    double acc[2 * PR_NCH];
+    const double a = seed * 1e-3 + 0.999, b = seed * 1e-7;
+#pragma unroll
+    for (int c = 0; c < 2 * PR_NCH; ++c) acc[c] = (double)(threadIdx.x + c);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int c = 0; c < 2 * PR_NCH; ++c) acc[c] = fma(acc[c], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < 2 * PR_NCH; ++c) s += acc[c];
+    if (s == 1234.5678) sink[threadIdx.x] = s;
+}
+
 template <int KIND>
 static cudaError_t run_probe(int iters, cudaStream_t st, float *sink, float *ms) {
     const int grid = num_sms() * 4;
@@ -51,9 +69,15 @@ static cudaError_t run_probe(int iters, cudaStream_t st, float *sink, float *ms)
     cudaError_t e = cudaEventCreate(&e0);
     if (e != cudaSuccess) return e;
     if ((e = cudaEventCreate(&e1)) != cudaSuccess) { cudaEventDestroy(e0); return e; }
-    fp32_probe_kernel<KIND><<<grid, PR_THREADS, 0, st>>>(iters / 16, 0.5f, sink);      // warm-up
-    cudaEventRecord(e0, st);
-    fp32_probe_kernel<KIND><<<grid, PR_THREADS, 0, st>>>(iters, 0.5f, sink);
+    if constexpr (KIND == 3) {
+        fp64_probe_kernel<<<grid, PR_THREADS, 0, st>>>(iters / 16, 0.5, reinterpret_cast<double *>(sink));
+        cudaEventRecord(e0, st);
+        fp64_probe_kernel<<<grid, PR_THREADS, 0, st>>>(iters, 0.5, reinterpret_cast<double *>(sink));
+    } else {
+        fp32_probe_kernel<KIND><<<grid, PR_THREADS, 0, st>>>(iters / 16, 0.5f, sink);      // warm-up
+        cudaEventRecord(e0, st);
+        fp32_probe_kernel<KIND><<<grid, PR_THREADS, 0, st>>>(iters, 0.5f, sink);
+    }
     cudaEventRecord(e1, st);
     e = cudaEventSynchronize(e1);
     if (e == cudaSuccess) e = cudaEventElapsedTime(ms, e0, e1);
@@ -67,18 +91,19 @@ static cudaError_t run_probe(int iters, cudaStream_t st, float *sink, float *ms)
 
 extern "C" rsvd_status rsvd_probe_fp32(int32_t kind, int32_t iters, double *tflops, rsvd_stream_t stream) {
     using namespace rsvd;
-    if (kind < 0 || kind > 2 || iters < 16 || !tflops) return fail(RSVD_ERR_ARG, "bad probe arguments");
+    if (kind < 0 || kind > 3 || iters < 16 || !tflops) return fail(RSVD_ERR_ARG, "bad probe arguments");
     float *sink = nullptr;
-    cudaError_t e = cudaMalloc(&sink, PR_THREADS * sizeof(float));
+    cudaError_t e = cudaMalloc(&sink, PR_THREADS * sizeof(double));
     if (e != cudaSuccess) return cuda_check(e, "probe sink");
     float ms = 0.f;
     cudaStream_t s = (cudaStream_t)stream;
-    e = kind == 0 ? run_probe<0>(iters, s, sink, &ms) : kind == 1 ? run_probe<1>(iters, s, sink, &ms)
-                                                                  : run_probe<2>(iters, s, sink, &ms);
+    e = kind == 0 ? run_probe<0>(iters, s, sink, &ms)
+      : kind == 1 ? run_probe<1>(iters, s, sink, &ms)
+      : kind == 2 ? run_probe<2>(iters, s, sink, &ms) : run_probe<3>(iters, s, sink, &ms);
     cudaFree(sink);
     if (e != cudaSuccess) return cuda_check(e, "fp32 probe");
     const double lanes = (double)num_sms() * 4 * PR_THREADS;
-    const double per_iter = 4.0 * PR_NCH * (kind == 0 ? 4.0 : (kind == 1 ? 4.0 : 2.0));   // flops per thread per iter
+    const double per_iter = 4.0 * PR_NCH * (kind == 2 ? 2.0 : 4.0);   // flops per thread per iter
     *tflops = lanes * (double)iters * per_iter / (ms * 1e-3) / 1e12;
     count_launches(2);
     return RSVD_OK;
