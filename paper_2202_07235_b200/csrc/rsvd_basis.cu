@@ -27,7 +27,8 @@ constexpr int BT = 64;         // output tile (rows) of C per CTA
 #define RSVD_KP_JB 16
 #endif
 #ifndef RSVD_KP_MINB
-#define RSVD_KP_MINB 3      // 3 CTAs (12 warps) per SM: 16-sample slabs, <= 170 registers; measured 11.4 -> 10.8 ms
+#define RSVD_KP_MINB 4      // 4 CTAs (16 warps) per SM: 16-sample slabs, 128 registers without spills; measured
+                            // 11.4 -> 10.8 ms (3 CTAs), 9.39 -> 9.20 ms (4 CTAs, latency-bound: profiles/r02b_partials_fp64.txt)
 #endif
 constexpr int JB = RSVD_KP_JB;   // angular samples per smem slab
 constexpr int NTHR = 128;
