@@ -108,6 +108,10 @@ def test_validation_before_launch(lib):
     assert lib.rsvd_align_argmax(None, 3, None, 3, 0, 96, 2, 0, None, 0, None, None, None, None) == 2
     assert lib.rsvd_kernel_reduce(None, 0, 8, 1, 64, None, None, None) == 1
     assert b"Q" in lib.rsvd_last_error() or len(lib.rsvd_last_error()) > 0
+    out = ctypes.c_double(0.0)
+    assert lib.rsvd_probe_fp32(4, 1000, ctypes.byref(out), None) == 1                 # kinds 0..3 (3 = DFMA)
+    assert lib.rsvd_probe_fp32(3, 8, ctypes.byref(out), None) == 1                    # iters < 16
+    assert lib.rsvd_probe_fp32(3, 1000, None, None) == 1                              # NULL result
 
 
 def test_eigen_solver_top_h_path(lib):
