@@ -435,6 +435,7 @@ def run_ours(args):
     barrier(world)
     # measured FP32 peak of this GPU (Pi_fp32 of SURVEY.md 8(d)), outside the timed region
     fp32_meas = {k: api.probe_fp32(k) for k in ("ffma2", "ffma")}
+    fp64_meas = api.probe_fp32("dfma", 100000)                     # the kernel partials' peak (row a0)
 
     clocks = Clocks(local)
     clocks.start()
@@ -564,6 +565,17 @@ def run_ours(args):
                                                                  if path == api.PATH_TC else "Pi_fp32")
                                 + ", Pi_fp32 = measured FFMA2 peak (SURVEY.md 8(d))"),
                  "kernel_ms_per_step": {k: round(v[0] / ts, 3) for k, v in ktime.items()}}
+    # row a0 against the measured DFMA peak: the kernel partials execute 2 DFMA per (template, sample)
+    # for every entry of the lower-triangle 64 x 64 tiles (diagonal tiles skip 12 of every 32)
+    kp_ms = ktime["kernel_partials"][0] / ts
+    if kp_ms > 0 and R % 64 == 0:
+        nt = R // 64
+        entries = (nt * (nt - 1) // 2) * 4096 + nt * 4096 * 20 // 32
+        kp_tf = 2.0 * 2 * entries * (b1 - b0) * Q / (kp_ms / 1e3) / 1e12       # the rank's basis sub-shard
+        step_roof["kernel_partials_fp64"] = {
+            "bound": "fp64", "achieved": round(kp_tf, 2), "peak": round(fp64_meas, 2), "unit": "TFLOP/s",
+            "frac": round(kp_tf / fp64_meas, 4),
+            "peak_note": "measured sustained DFMA rate (rsvd_probe_fp32 kind 3); executed DFMAs of the tile schedule"}
 
     # e2e: host (pinned) rings -> device -> step -> winners back, through the public API (per-image mode)
     e2e = None
@@ -644,6 +656,7 @@ def run_ours(args):
                        "seed": 220207235},
             "roofline": roof, "contraction_l2": contr_l2, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk, "fp32_peak_measured_tflops": {k: round(v, 2) for k, v in fp32_meas.items()},
+            "fp64_peak_measured_tflops": round(fp64_meas, 2),
             "gpu_launches": launches_all, "phases_ms_last_step": {k: round(v, 3) for k, v in phase.items()},
             "gen_seconds": round(gen_s, 1),
         }
