@@ -435,7 +435,8 @@ def run_ours(args):
     barrier(world)
     # measured FP32 peak of this GPU (Pi_fp32 of SURVEY.md 8(d)), outside the timed region
     fp32_meas = {k: api.probe_fp32(k) for k in ("ffma2", "ffma")}
-    fp64_meas = api.probe_fp32("dfma", 100000)                     # the kernel partials' peak (row a0)
+    fp64_meas = {"dfma": api.probe_fp32("dfma", 100000),          # fp64 peaks for row a0 (kernel partials)
+                 "dmma8": api.probe_fp32("dmma8", 20000)}
 
     clocks = Clocks(local)
     clocks.start()
@@ -565,17 +566,26 @@ def run_ours(args):
                                                                  if path == api.PATH_TC else "Pi_fp32")
                                 + ", Pi_fp32 = measured FFMA2 peak (SURVEY.md 8(d))"),
                  "kernel_ms_per_step": {k: round(v[0] / ts, 3) for k, v in ktime.items()}}
-    # row a0 against the measured DFMA peak: the kernel partials execute 2 DFMA per (template, sample)
-    # for every entry of the lower-triangle 64 x 64 tiles (diagonal tiles skip 12 of every 32)
+    # row a0 against the measured fp64 tensor-core peak: the kernel partials run the Gram of each 64 x 64
+    # tile of the lower triangle as mma.sync m8n8k4 .f64 (2 real K per sample, 4 flops per entry and
+    # sample); diagonal tiles skip the warp block above the diagonal and the m8n8 blocks a < b of the two
+    # diagonal warp blocks (36 of 64 blocks executed).  RSVD_KP_SIMT=1 selects the DFMA tile (20 of 32).
     kp_ms = ktime["kernel_partials"][0] / ts
     if kp_ms > 0 and R % 64 == 0:
         nt = R // 64
-        entries = (nt * (nt - 1) // 2) * 4096 + nt * 4096 * 20 // 32
+        simt = os.environ.get("RSVD_KP_SIMT", "0") == "1"
+        entries = (nt * (nt - 1) // 2) * 4096 + nt * 4096 * (20 if simt else 36) // (32 if simt else 64)
         kp_tf = 2.0 * 2 * entries * (b1 - b0) * Q / (kp_ms / 1e3) / 1e12       # the rank's basis sub-shard
+        kp_alg = 2.0 * 2 * (R * (R + 1) // 2) * (b1 - b0) * Q / (kp_ms / 1e3) / 1e12
+        kp_peak = fp64_meas["dfma"] if simt else fp64_meas["dmma8"]
         step_roof["kernel_partials_fp64"] = {
-            "bound": "fp64", "achieved": round(kp_tf, 2), "peak": round(fp64_meas, 2), "unit": "TFLOP/s",
-            "frac": round(kp_tf / fp64_meas, 4),
-            "peak_note": "measured sustained DFMA rate (rsvd_probe_fp32 kind 3); executed DFMAs of the tile schedule"}
+            "bound": "fp64", "achieved": round(kp_tf, 2), "peak": round(kp_peak, 2), "unit": "TFLOP/s",
+            "frac": round(kp_tf / kp_peak, 4), "achieved_algorithmic": round(kp_alg, 2),
+            "frac_algorithmic": round(kp_alg / kp_peak, 4),
+            "peak_note": ("measured sustained " + ("DFMA rate (rsvd_probe_fp32 kind 3)" if simt else
+                          "fp64 tensor-core rate (rsvd_probe_fp32 kind 4, mma.sync m8n8k4 .f64)")
+                          + "; achieved = executed flops of the tile schedule, achieved_algorithmic = the "
+                          "lower triangle R(R+1)/2 only")}
 
     # e2e: host (pinned) rings -> device -> step -> winners back, through the public API (per-image mode)
     e2e = None
@@ -656,7 +666,7 @@ def run_ours(args):
                        "seed": 220207235},
             "roofline": roof, "contraction_l2": contr_l2, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk, "fp32_peak_measured_tflops": {k: round(v, 2) for k, v in fp32_meas.items()},
-            "fp64_peak_measured_tflops": round(fp64_meas, 2),
+            "fp64_peak_measured_tflops": {k: round(v, 2) for k, v in fp64_meas.items()},
             "gpu_launches": launches_all, "phases_ms_last_step": {k: round(v, 3) for k, v in phase.items()},
             "gen_seconds": round(gen_s, 1),
         }

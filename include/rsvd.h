@@ -299,8 +299,9 @@ rsvd_status rsvd_combine_winners(const uint64_t *keys, int32_t G, int64_t M, int
  *   SURVEY.md 8(d)): one launch of register-only dependency chains on every SM (4 x 256 threads per
  *   SM, 8 chains per thread, `iters` x 32 instructions per chain), timed with CUDA events on `stream`
  *   after a short warm-up launch; synchronises.  kind 0 = FFMA, 1 = FFMA2 (packed fp32x2, sm_100),
- *   2 = FADD2, 3 = DFMA (fp64: the kernel-partials peak, 16 chains per thread).  *tflops = flops /
- *   elapsed (FFMA 2, FFMA2 4, FADD2 2, DFMA 2 flops per lane and instruction).
+ *   2 = FADD2, 3 = DFMA (fp64: the kernel-partials peak, 16 chains per thread), 4 / 5 = fp64 tensor-core
+ *   mma.sync m8n8k4 / m16n8k4 (8 accumulator fragments per warp).  *tflops = flops / elapsed (FFMA 2,
+ *   FFMA2 4, FADD2 2, DFMA 2 flops per lane and instruction; DMMA 2 M N K per warp instruction).
  *   Not part of the method; allocates a 1 KB scratch buffer. */
 int64_t rsvd_launch_count(void);
 void rsvd_timing_enable(int32_t on);

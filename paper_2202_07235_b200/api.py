@@ -361,7 +361,7 @@ def timing_read():
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(TIMING_KINDS)}
 
 
-PROBE_KINDS = {"ffma": 0, "ffma2": 1, "fadd2": 2, "dfma": 3}
+PROBE_KINDS = {"ffma": 0, "ffma2": 1, "fadd2": 2, "dfma": 3, "dmma8": 4, "dmma16": 5}
 
 
 def probe_fp32(kind: str = "ffma2", iters: int = 200000, stream=None) -> float:

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -46,6 +47,14 @@ __device__ __forceinline__ void kp_cp_async16(void *smem, const void *gmem, bool
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
 }
+// MMA = true: the Gram on the fp64 tensor cores (mma.sync m8n8k4 .f64; measured 37.1 TF/s on B200 vs
+// 34.1 for DFMA, tools/gpu_dmma_probe.sh) -- the product X X^T of the slab's fp64 rows with K = 2 JB reals
+// (re, im interleaved, so sum_k X[r][k] X[r'][k] = Re(x_r conj x_r')).  Warp w owns the 32 x 32 block
+// (rows 32 (w / 2), columns 32 (w % 2)) of the 64 x 64 tile as 4 x 4 m8n8 accumulators; per k-step of 4
+// it loads 4 A and 4 B fragments (8 LDS.64, conflict-free with the 2 JB + 4 double row stride) for 16
+// MMAs (4096 FMAs), where the SIMT tile issues 12 loads per 32 DFMAs per thread.
+template <bool MMA> struct KpLayout { static constexpr int SJ = MMA ? JB + 2 : JB + 1; };   // double2 per staged row
+template <bool MMA>
 __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(const float2 *__restrict__ tmpl,
                                                                int64_t T, int R, int Q,
                                                                double *__restrict__ partials,
@@ -54,16 +63,25 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
     if (ti < tj) return;
     const int64_t c = blockIdx.z;
     const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;     // ty < 8, tx < 16
+    constexpr int SJ = KpLayout<MMA>::SJ;
     extern __shared__ __align__(16) double2 kp_smem[];
-    double2 (*xi)[JB + 1] = reinterpret_cast<double2 (*)[JB + 1]>(kp_smem);
-    double2 (*xj)[JB + 1] = reinterpret_cast<double2 (*)[JB + 1]>(kp_smem + BT * (JB + 1));
+    double2 (*xi)[SJ] = reinterpret_cast<double2 (*)[SJ]>(kp_smem);
+    double2 (*xj)[SJ] = reinterpret_cast<double2 (*)[SJ]>(kp_smem + BT * SJ);
     __shared__ double si[BT][2], sj[BT][2];       // per-template row sums (re, im)
 
-    double acc[KA][KBB];
+    // SIMT: acc[a][b] = entry (ty + 8a, tx + 16b).  MMA: acc[a][b][e] = entry
+    // (wr + 8a + lane / 4, wc + 8b + 2 (lane % 4) + e) of the m8n8 accumulator fragments.
+    constexpr int NA = MMA ? 4 : KA, NB = MMA ? 4 : KBB, NE = MMA ? 2 : 1;
+    const int lane = tid & 31, wr = (tid >> 6) * 32, wc = ((tid >> 5) & 1) * 32;
+    double acc[NA][NB][NE];
 #pragma unroll
-    for (int a = 0; a < KA; ++a)
+    for (int a = 0; a < NA; ++a)
 #pragma unroll
-        for (int b = 0; b < KBB; ++b) acc[a][b] = 0.0;
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int e = 0; e < NE; ++e) acc[a][b][e] = 0.0;
+    auto row_of = [&](int a) { return MMA ? wr + 8 * a + (lane >> 2) : ty + 8 * a; };
+    auto col_of = [&](int b, int e) { return MMA ? wc + 8 * b + 2 * (lane & 3) + e : tx + 16 * b; };
 
     const int64_t t_begin = c * KCHUNK;
     const int64_t t_end = min(T, t_begin + KCHUNK);
@@ -72,7 +90,7 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
     // multiplied, so the global-load latency hides behind the DFMA loop
     const int nslab_t = (Q + JB - 1) / JB;
     const int64_t ts0 = t_begin * S, nslab = (t_end * S - ts0) * nslab_t;
-    float2 *rawi = reinterpret_cast<float2 *>(kp_smem + 2 * BT * (JB + 1));      // [BT][JB]
+    float2 *rawi = reinterpret_cast<float2 *>(kp_smem + 2 * BT * SJ);      // [BT][JB]
     float2 *rawj = rawi + BT * JB;
     auto issue = [&](int64_t k) {
         const int64_t t = (ts0 + k / nslab_t) / S;
@@ -126,6 +144,29 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
         // above their columns for every thread (ty + 8a < 16b, i.e. a < 2b) are skipped: 12 of 32.
         auto gram = [&](auto diag_c) {
             constexpr bool DIAG = decltype(diag_c)::value;
+            if constexpr (MMA) {
+                // diagonal tile: the warp block above the diagonal (wr < wc) and the m8n8 blocks a < b of
+                // the two diagonal warp blocks are never read
+                if (DIAG && wr < wc) return;
+                const double *xa = reinterpret_cast<const double *>(&xi[wr + (lane >> 2)][0]) + (lane & 3);
+                const double *xb = reinterpret_cast<const double *>(&xj[wc + (lane >> 2)][0]) + (lane & 3);
+#pragma unroll
+                for (int k0 = 0; k0 < 2 * JB; k0 += 4) {
+                    double af[4], bf[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) af[a] = xa[a * 8 * 2 * SJ + k0];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) bf[b] = xb[b * 8 * 2 * SJ + k0];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+                            if (!DIAG || wr != wc || a >= b)
+                                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                             : "+d"(acc[a][b][0]), "+d"(acc[a][b][NE - 1])
+                                             : "d"(af[a]), "d"(bf[b]));
+                }
+            } else {
 #pragma unroll 4
             for (int jj = 0; jj < JB; ++jj) {
                 double2 av[KA], bv[KBB];
@@ -137,7 +178,9 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
                 for (int a = 0; a < KA; ++a)
 #pragma unroll
                     for (int b = 0; b < KBB; ++b)
-                        if (!DIAG || a >= 2 * b) acc[a][b] = fma(av[a].x, bv[b].x, fma(av[a].y, bv[b].y, acc[a][b]));
+                        if (!DIAG || a >= 2 * b)
+                            acc[a][b][0] = fma(av[a].x, bv[b].x, fma(av[a].y, bv[b].y, acc[a][b][0]));
+            }
             }
         };
         if (ti == tj) gram(std::true_type{});
@@ -147,26 +190,52 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
             // remove the angular mean: - (1/Q) Re(S_r conj(S_r'))
             const double invQ = 1.0 / (double)Q;
 #pragma unroll
-            for (int a = 0; a < KA; ++a)
+            for (int a = 0; a < NA; ++a)
 #pragma unroll
-                for (int b = 0; b < KBB; ++b) {
-                    const double re = si[ty + 8 * a][0] * sj[tx + 16 * b][0] + si[ty + 8 * a][1] * sj[tx + 16 * b][1];
-                    acc[a][b] -= re * invQ;
-                }
+                for (int b = 0; b < NB; ++b)
+#pragma unroll
+                    for (int e = 0; e < NE; ++e) {
+                        const int ra = row_of(a), cb = col_of(b, e);
+                        const double re = si[ra][0] * sj[cb][0] + si[ra][1] * sj[cb][1];
+                        acc[a][b][e] -= re * invQ;
+                    }
             __syncthreads();       // every thread has read si/sj before the next template zeroes them
         }
     }
     double *out = partials + c * (int64_t)R * R;
 #pragma unroll
-    for (int a = 0; a < KA; ++a)
+    for (int a = 0; a < NA; ++a)
 #pragma unroll
-        for (int b = 0; b < KBB; ++b) {
-            const int r1 = ti * BT + ty + 8 * a, r2 = tj * BT + tx + 16 * b;
-            if (r1 < R && r2 < R && r1 >= r2) out[(int64_t)r1 * R + r2] = acc[a][b];   // lower triangle only
-        }
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                const int r1 = ti * BT + row_of(a), r2 = tj * BT + col_of(b, e);
+                if (r1 < R && r2 < R && r1 >= r2) out[(int64_t)r1 * R + r2] = acc[a][b][e];   // lower triangle only
+            }
 }
-constexpr size_t KP_SMEM = 2 * (size_t)BT * (JB + 1) * sizeof(double2) + 2 * (size_t)BT * JB * sizeof(float2);
-static std::atomic<uint64_t> g_partials_attr{0};   // per-device max-smem attribute of kernel_partials_kernel
+template <bool MMA>
+constexpr size_t kp_smem_bytes() {
+    return 2 * (size_t)BT * KpLayout<MMA>::SJ * sizeof(double2) + 2 * (size_t)BT * JB * sizeof(float2);
+}
+static std::atomic<uint64_t> g_partials_attr[2];   // per-device max-smem attribute of kernel_partials_kernel<MMA>
+
+// Gram kernel choice: the fp64 tensor-core form (default) or the DFMA tile (RSVD_KP_SIMT=1, A/B only)
+static bool kp_use_mma() {
+    static const bool simt = [] { const char *e = std::getenv("RSVD_KP_SIMT"); return e && e[0] == '1'; }();
+    return !simt;
+}
+static rsvd_status launch_partials(dim3 grid, cudaStream_t s, const float2 *tmpl, int64_t T, int R, int Q,
+                                   double *partials, const double2 *ramp, int S) {
+    const bool mma = kp_use_mma();
+    const void *fn = mma ? (const void *)kernel_partials_kernel<true> : (const void *)kernel_partials_kernel<false>;
+    const size_t smem = mma ? kp_smem_bytes<true>() : kp_smem_bytes<false>();
+    const cudaError_t e = smem_attr_once(fn, (int)smem, g_partials_attr[mma ? 1 : 0]);
+    if (e != cudaSuccess) return cuda_check(e, "kernel_partials attribute");
+    if (mma) kernel_partials_kernel<true><<<grid, NTHR, smem, s>>>(tmpl, T, R, Q, partials, ramp, S);
+    else kernel_partials_kernel<false><<<grid, NTHR, smem, s>>>(tmpl, T, R, Q, partials, ramp, S);
+    count_launches(1);
+    return cuda_check(cudaGetLastError(), "kernel_partials launch");
+}
 
 // C[r][r'] = sqrt(w_r w_r') / (T Q) * sum_c P_c[max(r,r')][min(r,r')] (lower triangle is the
 // computed one; reading it for both halves makes C exactly symmetric).  The chunk sum is a fixed
@@ -277,15 +346,11 @@ extern "C" rsvd_status rsvd_kernel_partials(const void *templates, int64_t T, in
     dim3 grid(nt, nt, (unsigned)nchunks);
     const bool timed = timing_enabled();
     cudaEvent_t ev0 = timed ? timing_event((cudaStream_t)stream) : nullptr;
-    {
-        const cudaError_t e = smem_attr_once((const void *)kernel_partials_kernel, (int)KP_SMEM, g_partials_attr);
-        if (e != cudaSuccess) return cuda_check(e, "kernel_partials attribute");
-    }
-    kernel_partials_kernel<<<grid, NTHR, KP_SMEM, (cudaStream_t)stream>>>(
-        reinterpret_cast<const float2 *>(templates), T, R, Q, partials, nullptr, 1);
-    count_launches(1);
+    const rsvd_status st2 = launch_partials(grid, (cudaStream_t)stream, reinterpret_cast<const float2 *>(templates), T, R,
+                                            Q, partials, nullptr, 1);
+    if (st2 != RSVD_OK) return st2;
     if (timed) timing_span(ev0, timing_event((cudaStream_t)stream), TK_BASIS);
-    return cuda_check(cudaGetLastError(), "kernel_partials launch");
+    return RSVD_OK;
 }
 
 extern "C" rsvd_status rsvd_kernel_reduce(const double *partials, int64_t nchunks, int32_t R,
@@ -364,16 +429,9 @@ extern "C" rsvd_status rsvd_build_basis_translated(const void *templates, int64_
         st = cuda_check(cudaGetLastError(), "ramp launch");
     }
     if (st == RSVD_OK) {
-        e = smem_attr_once((const void *)kernel_partials_kernel, (int)KP_SMEM, g_partials_attr);
-        if (e != cudaSuccess) st = cuda_check(e, "kernel_partials attribute");
-    }
-    if (st == RSVD_OK) {
         const int nt = (R + BT - 1) / BT;
         dim3 grid(nt, nt, (unsigned)nchunks);
-        kernel_partials_kernel<<<grid, NTHR, KP_SMEM, s>>>(reinterpret_cast<const float2 *>(templates), T, R, Q,
-                                                          partials, ramp, S);
-        count_launches(1);
-        st = cuda_check(cudaGetLastError(), "kernel_partials (translated) launch");
+        st = launch_partials(grid, s, reinterpret_cast<const float2 *>(templates), T, R, Q, partials, ramp, S);
     }
     if (st == RSVD_OK) st = rsvd_kernel_reduce(partials, nchunks, R, T * (int64_t)S, Q, w_dev, C_dev, stream);
     if (st == RSVD_OK && (e = cudaMemcpyAsync(C.data(), C_dev, cbytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)

@@ -8,6 +8,8 @@
 //   kind 1  FFMA2 (sm_100 packed fp32x2)           4 flops per lane per instruction
 //   kind 2  FADD2 (sm_100 packed fp32x2 add)        2 flops per lane per instruction
 //   kind 3  DFMA  (fp64)                            2 flops per lane per instruction (kernel-partials peak)
+//   kind 4  DMMA  mma.sync m8n8k4 f64 (tensor core)  512 flops per warp per instruction
+//   kind 5  DMMA  mma.sync m16n8k4 f64 (tensor core) 1024 flops per warp per instruction
 #include <cuda_runtime.h>
 
 #include "rsvd_common.cuh"
@@ -62,6 +64,39 @@ __global__ void __launch_bounds__(PR_THREADS) fp64_probe_kernel(int iters, doubl
     if (s == 1234.5678) sink[threadIdx.x] = s;
 }
 
+// fp64 tensor-core probe: NCH independent accumulator fragments per warp, A/B fragments in registers
+template <int SHAPE>   // 0: m8n8k4, 1: m16n8k4
+__global__ void __launch_bounds__(PR_THREADS) dmma_probe_kernel(int iters, double seed, double *__restrict__ sink) {
+    constexpr int NC = SHAPE == 0 ? 2 : 4;           // accumulator doubles per lane
+    double acc[PR_NCH][NC];
+    const double a0 = seed * 1e-3 + 0.999 + 1e-9 * threadIdx.x, a1 = 1.0001 - seed * 1e-3, b0 = seed * 1e-7;
+#pragma unroll
+    for (int c = 0; c < PR_NCH; ++c)
+#pragma unroll
+        for (int i = 0; i < NC; ++i) acc[c][i] = (double)(threadIdx.x + c + i);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int c = 0; c < PR_NCH; ++c) {
+                if constexpr (SHAPE == 0) {
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                 : "+d"(acc[c][0]), "+d"(acc[c][1]) : "d"(a0), "d"(b0));
+                } else {
+                    asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0, %1, %2, %3}, {%4, %5}, {%6}, {%0, %1, %2, %3};"
+                                 : "+d"(acc[c][0]), "+d"(acc[c][1]), "+d"(acc[c][2]), "+d"(acc[c][3])
+                                 : "d"(a0), "d"(a1), "d"(b0));
+                }
+            }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < PR_NCH; ++c)
+#pragma unroll
+        for (int i = 0; i < NC; ++i) s += acc[c][i];
+    if (s == 1234.5678) sink[threadIdx.x] = s;
+}
+
 template <int KIND>
 static cudaError_t run_probe(int iters, cudaStream_t st, float *sink, float *ms) {
     const int grid = num_sms() * 4;
@@ -69,7 +104,11 @@ static cudaError_t run_probe(int iters, cudaStream_t st, float *sink, float *ms)
     cudaError_t e = cudaEventCreate(&e0);
     if (e != cudaSuccess) return e;
     if ((e = cudaEventCreate(&e1)) != cudaSuccess) { cudaEventDestroy(e0); return e; }
-    if constexpr (KIND == 3) {
+    if constexpr (KIND == 4 || KIND == 5) {
+        dmma_probe_kernel<KIND - 4><<<grid, PR_THREADS, 0, st>>>(iters / 16, 0.5, reinterpret_cast<double *>(sink));
+        cudaEventRecord(e0, st);
+        dmma_probe_kernel<KIND - 4><<<grid, PR_THREADS, 0, st>>>(iters, 0.5, reinterpret_cast<double *>(sink));
+    } else if constexpr (KIND == 3) {
         fp64_probe_kernel<<<grid, PR_THREADS, 0, st>>>(iters / 16, 0.5, reinterpret_cast<double *>(sink));
         cudaEventRecord(e0, st);
         fp64_probe_kernel<<<grid, PR_THREADS, 0, st>>>(iters, 0.5, reinterpret_cast<double *>(sink));
@@ -91,7 +130,7 @@ static cudaError_t run_probe(int iters, cudaStream_t st, float *sink, float *ms)
 
 extern "C" rsvd_status rsvd_probe_fp32(int32_t kind, int32_t iters, double *tflops, rsvd_stream_t stream) {
     using namespace rsvd;
-    if (kind < 0 || kind > 3 || iters < 16 || !tflops) return fail(RSVD_ERR_ARG, "bad probe arguments");
+    if (kind < 0 || kind > 5 || iters < 16 || !tflops) return fail(RSVD_ERR_ARG, "bad probe arguments");
     float *sink = nullptr;
     cudaError_t e = cudaMalloc(&sink, PR_THREADS * sizeof(double));
     if (e != cudaSuccess) return cuda_check(e, "probe sink");
@@ -99,11 +138,13 @@ extern "C" rsvd_status rsvd_probe_fp32(int32_t kind, int32_t iters, double *tflo
     cudaStream_t s = (cudaStream_t)stream;
     e = kind == 0 ? run_probe<0>(iters, s, sink, &ms)
       : kind == 1 ? run_probe<1>(iters, s, sink, &ms)
-      : kind == 2 ? run_probe<2>(iters, s, sink, &ms) : run_probe<3>(iters, s, sink, &ms);
+      : kind == 2 ? run_probe<2>(iters, s, sink, &ms) : kind == 3 ? run_probe<3>(iters, s, sink, &ms)
+      : kind == 4 ? run_probe<4>(iters, s, sink, &ms) : run_probe<5>(iters, s, sink, &ms);
     cudaFree(sink);
     if (e != cudaSuccess) return cuda_check(e, "fp32 probe");
     const double lanes = (double)num_sms() * 4 * PR_THREADS;
-    const double per_iter = 4.0 * PR_NCH * (kind == 2 ? 2.0 : 4.0);   // flops per thread per iter
+    // flops per thread per iter (DMMA: a warp instruction's 2 M N K flops spread over its 32 lanes)
+    const double per_iter = 4.0 * PR_NCH * (kind == 2 ? 2.0 : kind == 4 ? 512.0 / 32 : kind == 5 ? 1024.0 / 32 : 4.0);
     *tflops = lanes * (double)iters * per_iter / (ms * 1e-3) / 1e12;
     count_launches(2);
     return RSVD_OK;

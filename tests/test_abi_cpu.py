@@ -109,7 +109,7 @@ def test_validation_before_launch(lib):
     assert lib.rsvd_kernel_reduce(None, 0, 8, 1, 64, None, None, None) == 1
     assert b"Q" in lib.rsvd_last_error() or len(lib.rsvd_last_error()) > 0
     out = ctypes.c_double(0.0)
-    assert lib.rsvd_probe_fp32(4, 1000, ctypes.byref(out), None) == 1                 # kinds 0..3 (3 = DFMA)
+    assert lib.rsvd_probe_fp32(6, 1000, ctypes.byref(out), None) == 1                 # kinds 0..5 (3 = DFMA, 4/5 = DMMA)
     assert lib.rsvd_probe_fp32(3, 8, ctypes.byref(out), None) == 1                    # iters < 16
     assert lib.rsvd_probe_fp32(3, 1000, None, None) == 1                              # NULL result
 

@@ -106,6 +106,28 @@ def test_basis_parity_and_determinism():
             assert np.linalg.norm(P - Pr, 2) <= 1e-10 / relgap, (name, h, relgap)
 
 
+def test_basis_parity_multi_tile():
+    """R = 128 (2 x 2 tiles of the partials grid: off-diagonal and diagonal tiles, every warp block of the
+    fp64 tensor-core Gram) and R = 96 (a ragged second tile), T not a multiple of the 8-template chunk:
+    the same SURVEY.md 8(c) O3 gates against the oracle's C and eigenbasis."""
+    for name, T, R_use in [("large", 45, 128), ("medium", 37, 64)]:
+        d = make_dataset(name, T=T, M=8)
+        B, w = to_np(d.templates), to_np(d.w)
+        for R in sorted({R_use, 96 if R_use == 128 else R_use}):
+            Bs, ws = np.ascontiguousarray(B[:, :R]), np.ascontiguousarray(w[:R])
+            U, lam = api.build_basis(cuda(Bs), ws, 24)
+            C_ref = ref.kernel_C(Bs, ws)
+            Ur, lr = ref.basis(C_ref, 24)
+            assert np.abs(lam - lr).max() <= 1e-12 * lr[0], (name, R)
+            assert np.linalg.norm(C_ref @ U - U * lam[None, :24]) <= 1e-12 * lr[0], (name, R)
+            for h in range(1, 24):
+                relgap = (lr[h - 1] - lr[h]) / lr[0]
+                if relgap < 1e-6:
+                    continue
+                P, Pr = U[:, :h] @ U[:, :h].T, Ur[:, :h] @ Ur[:, :h].T
+                assert np.linalg.norm(P - Pr, 2) <= 1e-10 / relgap, (name, R, h, relgap)
+
+
 @pytest.fixture(params=[1, 2, 0], ids=["auto", "mma", "ffma"])
 def compress_mode(request):
     """Step 1 kernel choice (rsvd_set_compress_mma): auto, tensor-core projection forced, FFMA2 forced."""
