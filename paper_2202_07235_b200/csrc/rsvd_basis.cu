@@ -92,52 +92,73 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
     const int64_t ts0 = t_begin * S, nslab = (t_end * S - ts0) * nslab_t;
     float2 *rawi = reinterpret_cast<float2 *>(kp_smem + 2 * BT * SJ);      // [BT][JB]
     float2 *rawj = rawi + BT * JB;
-    auto issue = [&](int64_t k) {
-        const int64_t t = (ts0 + k / nslab_t) / S;
-        const int j0 = (int)(k % nslab_t) * JB;
+    // cp.async mapping: thread -> 16-B chunk jc of rows rr0 + RSTEP i (no divisions in the slab loop)
+    constexpr int CPR = JB / 2, RSTEP = NTHR / CPR, NPASS = BT / RSTEP;
+    static_assert(NTHR % CPR == 0 && BT % RSTEP == 0, "cp.async mapping");
+    const int jc = tid % CPR, rr0 = tid / CPR;
+    auto issue = [&](int64_t t, int j0) {
         const float2 *bt = tmpl + t * (int64_t)R * Q;
-        for (int idx = tid; idx < BT * JB / 2; idx += NTHR) {    // 16-B chunks of 2 samples
-            const int rr = idx / (JB / 2), j = j0 + 2 * (idx % (JB / 2));
+        const int j = j0 + 2 * jc;
+#pragma unroll
+        for (int i = 0; i < NPASS; ++i) {                 // 16-B chunks of 2 samples
+            const int rr = rr0 + RSTEP * i;
             const int r1 = ti * BT + rr, r2 = tj * BT + rr;
-            kp_cp_async16(rawi + rr * JB + (j - j0), (r1 < R && j < Q) ? bt + (int64_t)r1 * Q + j : bt, (r1 < R && j < Q));
-            kp_cp_async16(rawj + rr * JB + (j - j0), (r2 < R && j < Q) ? bt + (int64_t)r2 * Q + j : bt, (r2 < R && j < Q));
+            const bool v1 = r1 < R && j < Q, v2 = r2 < R && j < Q;
+            kp_cp_async16(rawi + rr * JB + 2 * jc, v1 ? bt + r1 * Q + j : bt, v1);
+            kp_cp_async16(rawj + rr * JB + 2 * jc, v2 ? bt + r2 * Q + j : bt, v2);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    if (nslab > 0) issue(0);
+    // widening mapping: thread -> sample jw of rows rw0 + WSTEP i
+    constexpr int WSTEP = NTHR / JB;
+    static_assert(NTHR % JB == 0 && BT % WSTEP == 0, "widening mapping");
+    const int jw = tid % JB, rw0 = tid / JB;
+    // slab coordinates carried without divisions: template t_c, translated copy s_c, slab sl
+    int64_t t_c = t_begin;
+    int s_c = 0, sl = 0;
+    if (nslab > 0) issue(t_c, 0);
     for (int64_t k = 0; k < nslab; ++k) {
-        const int64_t ts = ts0 + k / nslab_t;
-        const int sl = (int)(k % nslab_t), j0 = sl * JB;
-        const double2 *rp = ramp ? ramp + (ts % S) * (int64_t)R * Q : nullptr;
+        int64_t t_n = t_c;
+        int s_n = s_c, sl_n = sl + 1;
+        if (sl_n == nslab_t) { sl_n = 0; if (++s_n == S) { s_n = 0; ++t_n; } }
+        const int j0 = sl * JB;
+        const double2 *rp = ramp ? ramp + (int64_t)s_c * R * Q : nullptr;
         if (sl == 0 && tid < BT) { si[tid][0] = si[tid][1] = 0.0; sj[tid][0] = sj[tid][1] = 0.0; }
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();                                   // slab k landed; slab k - 1 fully consumed
         // widen to fp64 (products of fp32 values are then exact)
-        for (int idx = tid; idx < BT * JB; idx += NTHR) {
-            const int rr = idx / JB, jj = idx % JB;
-            const float2 u = rawi[idx], v = rawj[idx];
+#pragma unroll
+        for (int i = 0; i < BT / WSTEP; ++i) {
+            const int rr = rw0 + WSTEP * i;
+            const float2 u = rawi[rr * JB + jw], v = rawj[rr * JB + jw];
             double2 du = make_double2((double)u.x, (double)u.y), dv = make_double2((double)v.x, (double)v.y);
             if (rp) {                                  // translated copy: exact fp64 complex product
-                const int r1 = ti * BT + rr, r2 = tj * BT + rr, j = j0 + jj;
+                const int r1 = ti * BT + rr, r2 = tj * BT + rr, j = j0 + jw;
                 const double2 a = (r1 < R && j < Q) ? rp[(int64_t)r1 * Q + j] : make_double2(1.0, 0.0);
                 const double2 b = (r2 < R && j < Q) ? rp[(int64_t)r2 * Q + j] : make_double2(1.0, 0.0);
                 du = make_double2(du.x * a.x - du.y * a.y, du.x * a.y + du.y * a.x);
                 dv = make_double2(dv.x * b.x - dv.y * b.y, dv.x * b.y + dv.y * b.x);
             }
-            xi[rr][jj] = du;
-            xj[rr][jj] = dv;
+            xi[rr][jw] = du;
+            xj[rr][jw] = dv;
         }
         __syncthreads();                                   // fp64 slab ready, raw buffer free
-        if (k + 1 < nslab) issue(k + 1);
-        // row sums (fp64, fixed order)
-        if (tid < BT) {
-            double sr = 0, sim = 0, tr = 0, tim = 0;
-            for (int jj = 0; jj < JB; ++jj) {
-                sr += xi[tid][jj].x; sim += xi[tid][jj].y;
-                tr += xj[tid][jj].x; tim += xj[tid][jj].y;
+        if (k + 1 < nslab) issue(t_n, sl_n * JB);
+        // row sums (fp64, fixed order): threads 0-63 the rows of xi, 64-127 those of xj; row rr starts
+        // at sample rr mod JB, so the 8 threads of a 128-bit wavefront hit distinct banks
+        {
+            static_assert((JB & (JB - 1)) == 0 && NTHR == 2 * BT, "row-sum mapping");
+            const int rr = tid & (BT - 1);
+            const double2 *xr = tid < BT ? &xi[rr][0] : &xj[rr][0];
+            double sr[4] = {0, 0, 0, 0}, sim[4] = {0, 0, 0, 0};      // 4 independent chains, fixed order
+#pragma unroll
+            for (int s2 = 0; s2 < JB; ++s2) {
+                const double2 v = xr[(rr + s2) & (JB - 1)];
+                sr[s2 & 3] += v.x; sim[s2 & 3] += v.y;
             }
-            si[tid][0] += sr; si[tid][1] += sim;
-            sj[tid][0] += tr; sj[tid][1] += tim;
+            double (*sd)[2] = tid < BT ? si : sj;
+            sd[rr][0] += (sr[0] + sr[1]) + (sr[2] + sr[3]);
+            sd[rr][1] += (sim[0] + sim[1]) + (sim[2] + sim[3]);
         }
         // Gram: Re(x_r conj(x_r')) = xr xr' + xi xi'.  On a diagonal tile only r >= r' is ever read
         // (kernel_reduce_kernel takes the lower triangle), so register entries (a, b) whose rows all lie
@@ -201,6 +222,9 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
                     }
             __syncthreads();       // every thread has read si/sj before the next template zeroes them
         }
+        t_c = t_n;
+        s_c = s_n;
+        sl = sl_n;
     }
     double *out = partials + c * (int64_t)R * R;
 #pragma unroll
