@@ -56,13 +56,22 @@ void householder_tridiag(int n, std::vector<double> &A, std::vector<double> &d, 
         for (int i = 0; i < m; ++i) p[i] = 0.0;
         for (int i = 0; i < m; ++i) {
             const double *row = &A[(size_t)(k + 1 + i) * n + (k + 1)];
-            double s = row[i] * v[i];
             const double vi = v[i];
-            for (int j = 0; j < i; ++j) {
-                s += row[j] * v[j];
+            // the dot over the row prefix in four interleaved partial sums (fixed order; four
+            // independent add chains instead of one), the axpy into p alongside
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};
+            int j = 0;
+            for (; j + 4 <= i; j += 4) {
+                for (int u = 0; u < 4; ++u) {
+                    s4[u] += row[j + u] * v[j + u];
+                    p[j + u] += row[j + u] * vi;
+                }
+            }
+            for (; j < i; ++j) {
+                s4[0] += row[j] * v[j];
                 p[j] += row[j] * vi;
             }
-            p[i] += s;
+            p[i] += row[i] * vi + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
         }
         for (int i = 0; i < m; ++i) p[i] *= beta;
         double vp = 0.0;
@@ -243,9 +252,12 @@ bool top_vectors_inverse_iteration(int n, const std::vector<double> &d, const st
         for (int k = n - 3; k >= 0; --k) {
             if (betas[k] == 0.0) continue;
             const double *vk = &refl[(size_t)k * n];
-            double s = 0.0;
-            for (int j = k + 1; j < n; ++j) s += vk[j] * v[j];
-            s *= betas[k];
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};                // four interleaved partial sums
+            int j = k + 1;
+            for (; j + 4 <= n; j += 4)
+                for (int u = 0; u < 4; ++u) s4[u] += vk[j + u] * v[j + u];
+            for (; j < n; ++j) s4[0] += vk[j] * v[j];
+            const double s = ((s4[0] + s4[1]) + (s4[2] + s4[3])) * betas[k];
             for (int j = k + 1; j < n; ++j) v[j] -= s * vk[j];
         }
     }
