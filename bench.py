@@ -68,6 +68,8 @@ def parse():
     p.add_argument("--path", default=None, choices=["auto", "simt", "tc"], help="contraction path override")
     p.add_argument("--precision", default="fp32", choices=["fp32", "fast"],
                    help="fp32: the 1e-5 path (default); fast: single fp16 MMA + fp16 spectrum, the 2e-3 tensor-core path")
+    p.add_argument("--eigen", default="device", choices=["device", "host"],
+                   help="row a0 eigen-solve: on the device (rsvd_eigen_basis_device, no host round trip; R <= 128) or on the host")
     p.add_argument("--shard", default="templates", choices=["2d", "templates"],
                    help="rank grid: templates only (north_star: templates sharded over the GPUs, default) or "
                         "image x template shards (dist.grid_shape)")
@@ -384,6 +386,9 @@ def run_ours(args):
         mark("combine")
         return out, bases[0][0]
 
+    dev_eigen = args.eigen == "device" and R <= 128 and R * H <= 8192
+    eig_infos = []
+
     def step(imgs, tmps, marks=None):
         if G_ctf:
             return step_grouped(imgs, tmps, marks)
@@ -395,8 +400,13 @@ def run_ours(args):
                 e.record(stream)
                 marks.append((name, e))
         mark("start")
-        U, lam = pdist.basis_from_shards(tmps[b0 - t0:b1 - t0], T, w_dev, H, GI=GI)   # a0 (syncs for the host solve)
-        U_dev.copy_(torch.from_numpy(U), non_blocking=False)
+        if dev_eigen:                                                              # a0, no host round trip
+            U, _, info = pdist.basis_from_shards_device(tmps[b0 - t0:b1 - t0], T, w_dev, H, GI=GI)
+            U_dev.copy_(U)
+            eig_infos.append(info)
+        else:
+            U, lam = pdist.basis_from_shards(tmps[b0 - t0:b1 - t0], T, w_dev, H, GI=GI)   # a0 (syncs for the host solve)
+            U_dev.copy_(torch.from_numpy(U), non_blocking=False)
         mark("basis")
         for (a, e), ib in zip(blocks, ibs):                                        # a1
             if e > a:
@@ -477,6 +487,13 @@ def run_ours(args):
         api.timing_enable(False)
         timing_steps = args.steps
     ktime = api.timing_read()
+    if eig_infos:                                 # device eigen-solves all passed their residual test
+        bad = int(torch.stack(eig_infos).sum().item())
+        if bad:
+            raise RuntimeError(f"device eigen-solver failed its residual test in {bad} steps (rerun with --eigen host)")
+        eig_infos.clear()
+    if torch.is_tensor(last_U):
+        last_U = last_U.cpu().numpy()
     ms_step = max_over_ranks(elapsed_ms / args.steps, world)
     ms_median = max_over_ranks(float(np.median(per_step)), world)
     launches_all = int(sum_over_ranks(launches, world))
@@ -669,6 +686,8 @@ def run_ours(args):
             "fp64_peak_measured_tflops": {k: round(v, 2) for k, v in fp64_meas.items()},
             "gpu_launches": launches_all, "phases_ms_last_step": {k: round(v, 3) for k, v in phase.items()},
             "gen_seconds": round(gen_s, 1),
+            "a0_eigen": ("device (rsvd_eigen_basis_device)" if dev_eigen else "host (rsvd_eigen_basis)")
+                        if not G_ctf else "host (rsvd_eigen_basis_ctf per group)",
         }
         print(json.dumps(line), flush=True)
     if world > 1:

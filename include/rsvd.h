@@ -111,6 +111,19 @@ rsvd_status rsvd_kernel_partials(const void *templates, int64_t T, int32_t R, in
 rsvd_status rsvd_kernel_reduce(const double *partials, int64_t nchunks, int32_t R, int64_t T_total,
                                int32_t Q, const double *w, double *C, rsvd_stream_t stream);
 rsvd_status rsvd_eigen_basis(const double *C, int32_t R, int32_t H, double *U, double *lambda);
+
+/* rsvd_eigen_basis_device: the same eigenbasis computed on the device (one CTA, C in shared memory), so
+ *   a step needs no host round trip between the kernel matrix and Step 1 (DESIGN.md
+ *   reading G7).  C: device fp64 [R][R] (symmetrised as (C + C^T)/2); U: device fp64 [R][H] row-major;
+ *   lambda (may be NULL): device fp64 [R], descending; info: device int32, set to 0 on success or 1 when
+ *   an eigenvector fails the a-posteriori residual test ||T y - lambda y|| <= 64 R eps ||T|| (U is then
+ *   unusable; run rsvd_eigen_basis on the same C).  Householder tridiagonalisation, bisection on the
+ *   Sturm count for every eigenvalue, inverse iteration with Gram-Schmidt for the top H vectors,
+ *   back-transform; fixed reduction orders (bitwise reproducible).  Eigenvalues agree with
+ *   rsvd_eigen_basis to O(eps ||C||), vectors with the same sign rule.  R <= 128, H * R <= 8192, else
+ *   RSVD_ERR_UNSUPPORTED.  Asynchronous on `stream`. */
+rsvd_status rsvd_eigen_basis_device(const double *C, int32_t R, int32_t H, double *U, double *lambda,
+                                    int32_t *info, rsvd_stream_t stream);
 /* Row f3 (per-CTF-group bases; PAPER.md:715-724 builds one kernel and basis per CTF): host only.
  * For targets = templates multiplied ring by ring by a radial CTF ctf[r] = c_g(k_r), the group's
  * kernel is diag(ctf) C diag(ctf) with C the raw templates' kernel (rsvd_kernel_reduce output

@@ -36,6 +36,7 @@ SIGNATURES = [
     ("rsvd_kernel_reduce", _I32, [_P, _I64, _I32, _I64, _I32, _P, _P, _P]),
     ("rsvd_eigen_basis", _I32, [_P, _I32, _I32, _P, _P]),
     ("rsvd_eigen_basis_ctf", _I32, [_P, _I32, _P, _I32, _P, _P, _P]),
+    ("rsvd_eigen_basis_device", _I32, [_P, _I32, _I32, _P, _P, _P, _P]),
     ("rsvd_build_basis", _I32, [_P, _I64, _I32, _I32, _P, _I32, _P, _P, _P]),
     ("rsvd_build_basis_translated", _I32, [_P, _I64, _I32, _I32, _P, _P, _P, _I32, _I32, _P, _P, _P]),
     ("rsvd_kernel_translated_sh", _I32, [_P, _I32, _I32, _P, _P, ctypes.c_double, _P, _P]),

@@ -110,6 +110,20 @@ def eigen_basis(C: np.ndarray, H: int):
     return U, lam
 
 
+def eigen_basis_device(C: torch.Tensor, H: int, stream=None):
+    """rsvd_eigen_basis_device: the eigenbasis on the device (no host round trip).  C: device fp64
+    [R, R].  Returns (U [R, H], lambda [R], info [1] int32) as device tensors, enqueued on the stream;
+    info != 0 (read it after synchronising) means U failed the residual test -- use eigen_basis(C)."""
+    require_cuda(C)
+    C = C.contiguous()
+    R = C.shape[0]
+    U = torch.empty((R, H), dtype=torch.float64, device=C.device)
+    lam = torch.empty(R, dtype=torch.float64, device=C.device)
+    info = torch.zeros(1, dtype=torch.int32, device=C.device)
+    check(_lib.lib().rsvd_eigen_basis_device(ptr(C), R, H, ptr(U), ptr(lam), ptr(info), stream_handle(stream)))
+    return U, lam, info
+
+
 def eigen_basis_ctf(C: np.ndarray, ctf, H: int):
     """rsvd_eigen_basis_ctf (row f3): (U, U_tmpl, lambda) of one CTF group from the raw kernel C."""
     C = np.ascontiguousarray(C, dtype=np.float64)

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "librsvd.so")
-SOURCES = ["rsvd_api.cpp", "rsvd_eigen.cpp", "rsvd_basis.cu", "rsvd_compress.cu", "rsvd_align.cu", "rsvd_tc.cu", "rsvd_vol.cu", "rsvd_probe.cu", "rsvd_fused.cu"]
+SOURCES = ["rsvd_api.cpp", "rsvd_eigen.cpp", "rsvd_basis.cu", "rsvd_compress.cu", "rsvd_align.cu", "rsvd_tc.cu", "rsvd_vol.cu", "rsvd_probe.cu", "rsvd_fused.cu", "rsvd_eigen_dev.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -118,6 +118,15 @@ def basis_from_shards(tmpl_shard: torch.Tensor, T_total: int, w_dev: torch.Tenso
     return api.eigen_basis(C.cpu().numpy(), H)
 
 
+def basis_from_shards_device(tmpl_shard: torch.Tensor, T_total: int, w_dev: torch.Tensor, H: int, group=None,
+                             GI: int = 1):
+    """Rows a0 across ranks without a host round trip: (U [R, H], lambda [R], info) as device tensors from
+    the device eigen-solver (R <= 128), identical on every rank and for any world size."""
+    from . import api
+    C = kernel_from_shards(tmpl_shard, T_total, w_dev, group, GI)
+    return api.eigen_basis_device(C, H)
+
+
 def combine_keys(keys: torch.Tensor, Q: int, group=None):
     """Per-image winners over all ranks: (keys, val, t, k) on every rank."""
     from . import api

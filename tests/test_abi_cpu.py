@@ -108,6 +108,10 @@ def test_validation_before_launch(lib):
     assert lib.rsvd_align_argmax(None, 3, None, 3, 0, 96, 2, 0, None, 0, None, None, None, None) == 2
     assert lib.rsvd_kernel_reduce(None, 0, 8, 1, 64, None, None, None) == 1
     assert b"Q" in lib.rsvd_last_error() or len(lib.rsvd_last_error()) > 0
+    assert lib.rsvd_eigen_basis_device(None, 129, 8, None, None, None, None) == 2     # R > 128
+    assert lib.rsvd_eigen_basis_device(None, 128, 65, None, None, None, None) == 2    # H * R > 8192
+    assert lib.rsvd_eigen_basis_device(None, 64, 0, None, None, None, None) == 2      # H < 1
+    assert lib.rsvd_eigen_basis_device(None, 64, 8, None, None, None, None) == 1      # NULL
     out = ctypes.c_double(0.0)
     assert lib.rsvd_probe_fp32(6, 1000, ctypes.byref(out), None) == 1                 # kinds 0..5 (3 = DFMA, 4/5 = DMMA)
     assert lib.rsvd_probe_fp32(3, 8, ctypes.byref(out), None) == 1                    # iters < 16

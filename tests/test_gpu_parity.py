@@ -128,6 +128,45 @@ def test_basis_parity_multi_tile():
                 assert np.linalg.norm(P - Pr, 2) <= 1e-10 / relgap, (name, R, h, relgap)
 
 
+def test_device_eigen_solver():
+    """rsvd_eigen_basis_device (row a0 without the host round trip) against the oracle's C and eigenbasis at
+    the SURVEY.md 8(c) O3 gates, for every ring count of the BASELINE configs (R = 16, 32, 64, 128) and the
+    H of each, plus H = R / 2 at R = 128 and a 5-template C (fast-decaying spectrum, clustered near-null
+    eigenvalues); the sign rule
+    and eigenvalues agree with the host solver; bitwise reproducible; info = 0."""
+    cases = [("tiny", None, 4), ("small", 256, 8), ("medium", 48, 16), ("medium", 40, 64), ("large", 45, 24),
+             ("large", 45, 64), ("small", 5, 8)]
+    for name, T, H in cases:
+        d = make_dataset(name, T=T, M=8)
+        B, w = to_np(d.templates), to_np(d.w)
+        R = d.R
+        C = api.kernel_reduce(api.kernel_partials(cuda(B)), B.shape[0], d.Q, cuda(w, torch.float64))
+        U, lam, info = api.eigen_basis_device(C, H)
+        U2, lam2, info2 = api.eigen_basis_device(C, H)
+        torch.cuda.synchronize()
+        assert int(info.item()) == 0 and int(info2.item()) == 0, (name, H)
+        U, lam = to_np(U), to_np(lam)
+        assert np.array_equal(U, to_np(U2)) and np.array_equal(lam, to_np(lam2))      # bitwise reproducible
+        Uh, lamh = api.eigen_basis(to_np(C), H)                                         # host solver, same C
+        assert np.abs(lam - lamh).max() <= 1e-13 * lamh[0], (name, H)
+        C_ref = ref.kernel_C(B, w)
+        Ur, lr = ref.basis(C_ref, H)
+        assert np.abs(lam - lr).max() <= 1e-12 * lr[0], (name, H)
+        assert np.linalg.norm(C_ref @ U - U * lam[None, :H]) <= 1e-12 * lr[0], (name, H)
+        assert np.abs(U.T @ U - np.eye(H)).max() <= 1e-12, (name, H)
+        for h in range(1, H + 1):
+            relgap = (lr[h - 1] - lr[h]) / lr[0] if h < R else 1.0
+            if relgap < 1e-6:
+                continue
+            P, Pr = U[:, :h] @ U[:, :h].T, Ur[:, :h] @ Ur[:, :h].T
+            assert np.linalg.norm(P - Pr, 2) <= 1e-10 / relgap, (name, H, h, relgap)
+            # well-separated single vectors: same sign rule as the host solver
+            gap_below = relgap
+            gap_above = (lr[h - 2] - lr[h - 1]) / lr[0] if h >= 2 else 1.0
+            if gap_below >= 1e-6 and gap_above >= 1e-6:
+                assert float(U[:, h - 1] @ Uh[:, h - 1]) > 0.5, (name, H, h)
+
+
 @pytest.fixture(params=[1, 2, 0], ids=["auto", "mma", "ffma"])
 def compress_mode(request):
     """Step 1 kernel choice (rsvd_set_compress_mma): auto, tensor-core projection forced, FFMA2 forced."""
