@@ -32,6 +32,9 @@ constexpr int EV_THREADS = 512;
 constexpr int EV_WARPS = EV_THREADS / 32;
 constexpr int EV_MAXN = 128;
 constexpr int EV_MAXY = 8192;          // H * n doubles of eigenvector workspace (64 KB)
+#ifndef RSVD_EV_STOP
+#define RSVD_EV_STOP 0                 // diagnostic builds only: return after phase 1 / 2 / 3
+#endif
 
 __device__ __forceinline__ double ev_block_sum(double x, double *red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -130,6 +133,7 @@ __global__ void __launch_bounds__(EV_THREADS, 1) eigen_basis_kernel(const double
     if (tid < n - 1) e2[tid] = e[tid] * e[tid];
     __syncthreads();
 
+    if (RSVD_EV_STOP == 1) return;
     // ---- 2. all eigenvalues by bisection (lam[t] = t-th largest)
     double tnorm = 0.0, glo = 0.0, ghi = 0.0;
     for (int i = 0; i < n; ++i) {
@@ -167,6 +171,7 @@ __global__ void __launch_bounds__(EV_THREADS, 1) eigen_basis_kernel(const double
     __syncthreads();
     if (tid < n && lambda) lambda[tid] = lam[tid];
 
+    if (RSVD_EV_STOP == 2) return;
     // ---- 3. top-H eigenvectors of T by inverse iteration + block Gram-Schmidt after every solve
     // thread h keeps its LU factors in registers/local memory; Y[h] holds the iterate
     double la[EV_MAXN], lb[EV_MAXN], lc2[EV_MAXN], lm[EV_MAXN];
@@ -254,6 +259,7 @@ __global__ void __launch_bounds__(EV_THREADS, 1) eigen_basis_kernel(const double
     }
     __syncthreads();
 
+    if (RSVD_EV_STOP == 3) return;
     // ---- 4. back-transform (warp per vector), normalise, sign rule
     for (int h = warp; h < H; h += EV_WARPS) {
         double *y = Y + h * n;
@@ -308,7 +314,9 @@ extern "C" rsvd_status rsvd_eigen_basis_device(const double *C, int32_t R, int32
     if ((reinterpret_cast<uintptr_t>(C) | reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(lambda)) & 7u)
         return fail(RSVD_ERR_ARG, "misaligned pointer");
     const size_t smem = eigen_dev_smem(R, H);
-    const cudaError_t e = smem_attr_once((const void *)eigen_basis_kernel, (int)smem, g_eigen_dev_attr);
+    // the attribute is set once per device, so it must cover the largest supported (R, H)
+    const cudaError_t e = smem_attr_once((const void *)eigen_basis_kernel, (int)eigen_dev_smem(EV_MAXN, EV_MAXY / EV_MAXN),
+                                         g_eigen_dev_attr);
     if (e != cudaSuccess) return cuda_check(e, "eigen_basis attribute");
     eigen_basis_kernel<<<1, EV_THREADS, smem, (cudaStream_t)stream>>>(C, R, H, U, lambda, info);
     count_launches(1);
