@@ -66,7 +66,9 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
     constexpr int SJ = KpLayout<MMA>::SJ;
     extern __shared__ __align__(16) double2 kp_smem[];
     double2 (*xi)[SJ] = reinterpret_cast<double2 (*)[SJ]>(kp_smem);
-    double2 (*xj)[SJ] = reinterpret_cast<double2 (*)[SJ]>(kp_smem + BT * SJ);
+    // diagonal tiles (ti == tj) multiply the slab by itself: stage it once and alias xj to xi
+    const bool diag = ti == tj;
+    double2 (*xj)[SJ] = diag ? xi : reinterpret_cast<double2 (*)[SJ]>(kp_smem + BT * SJ);
     __shared__ double si[BT][2], sj[BT][2];       // per-template row sums (re, im)
 
     // SIMT: acc[a][b] = entry (ty + 8a, tx + 16b).  MMA: acc[a][b][e] = entry
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
             const int r1 = ti * BT + rr, r2 = tj * BT + rr;
             const bool v1 = r1 < R && j < Q, v2 = r2 < R && j < Q;
             kp_cp_async16(rawi + rr * JB + 2 * jc, v1 ? bt + r1 * Q + j : bt, v1);
-            kp_cp_async16(rawj + rr * JB + 2 * jc, v2 ? bt + r2 * Q + j : bt, v2);
+            if (!diag) kp_cp_async16(rawj + rr * JB + 2 * jc, v2 ? bt + r2 * Q + j : bt, v2);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
@@ -130,17 +132,24 @@ __global__ void __launch_bounds__(NTHR, RSVD_KP_MINB) kernel_partials_kernel(con
 #pragma unroll
         for (int i = 0; i < BT / WSTEP; ++i) {
             const int rr = rw0 + WSTEP * i;
-            const float2 u = rawi[rr * JB + jw], v = rawj[rr * JB + jw];
-            double2 du = make_double2((double)u.x, (double)u.y), dv = make_double2((double)v.x, (double)v.y);
+            const float2 u = rawi[rr * JB + jw];
+            double2 du = make_double2((double)u.x, (double)u.y);
             if (rp) {                                  // translated copy: exact fp64 complex product
-                const int r1 = ti * BT + rr, r2 = tj * BT + rr, j = j0 + jw;
+                const int r1 = ti * BT + rr, j = j0 + jw;
                 const double2 a = (r1 < R && j < Q) ? rp[(int64_t)r1 * Q + j] : make_double2(1.0, 0.0);
-                const double2 b = (r2 < R && j < Q) ? rp[(int64_t)r2 * Q + j] : make_double2(1.0, 0.0);
                 du = make_double2(du.x * a.x - du.y * a.y, du.x * a.y + du.y * a.x);
-                dv = make_double2(dv.x * b.x - dv.y * b.y, dv.x * b.y + dv.y * b.x);
             }
             xi[rr][jw] = du;
-            xj[rr][jw] = dv;
+            if (!diag) {
+                const float2 v = rawj[rr * JB + jw];
+                double2 dv = make_double2((double)v.x, (double)v.y);
+                if (rp) {
+                    const int r2 = tj * BT + rr, j = j0 + jw;
+                    const double2 b = (r2 < R && j < Q) ? rp[(int64_t)r2 * Q + j] : make_double2(1.0, 0.0);
+                    dv = make_double2(dv.x * b.x - dv.y * b.y, dv.x * b.y + dv.y * b.x);
+                }
+                xj[rr][jw] = dv;
+            }
         }
         __syncthreads();                                   // fp64 slab ready, raw buffer free
         if (k + 1 < nslab) issue(t_n, sl_n * JB);
