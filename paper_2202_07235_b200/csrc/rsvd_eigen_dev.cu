@@ -49,6 +49,17 @@ __device__ __forceinline__ double ev_block_sum(double x, double *red) {
     return t;
 }
 
+// 1 / q to ~1 ulp: the hardware reciprocal seed (rcp.approx.ftz.f64) and two Newton steps -- half the
+// latency of the IEEE division sequence on the Sturm recurrence's critical path (|q| >= pivmin is normal)
+__device__ __forceinline__ double ev_rcp(double q) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    double e = fma(-q, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-q, r, 1.0);
+    return fma(r, e, r);
+}
+
 // number of eigenvalues of T = (d, e) below sigma (Sturm sequence; e2 = e^2, pivmin guards zero pivots)
 __device__ __forceinline__ int ev_sturm(int n, const double *d, const double *e2, double sigma, double pivmin) {
     int cnt = 0;
@@ -56,7 +67,7 @@ __device__ __forceinline__ int ev_sturm(int n, const double *d, const double *e2
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += q < 0.0;
     for (int i = 1; i < n; ++i) {
-        q = (d[i] - sigma) - e2[i - 1] / q;
+        q = (d[i] - sigma) - e2[i - 1] * ev_rcp(q);
         if (fabs(q) < pivmin) q = -pivmin;
         cnt += q < 0.0;
     }
@@ -198,8 +209,10 @@ __global__ void __launch_bounds__(EV_THREADS, 1) eigen_basis_kernel(const double
                 la[i + 1] -= mm * lb[i];
             }
         }
-        for (int i = 0; i < n; ++i)
+        for (int i = 0; i < n; ++i) {
             if (fabs(la[i]) < eps * tnorm) la[i] = (la[i] < 0 ? -1.0 : 1.0) * eps * tnorm;
+            la[i] = 1.0 / la[i];                 // the back solve multiplies by the reciprocal pivots
+        }
         for (int i = 0; i < n; ++i) Y[h * n + i] = 1.0 + 1e-3 * (double)((i * 7 + h * 3) % 11);
     }
     for (int it = 0; it < 3; ++it) {
@@ -213,7 +226,7 @@ __global__ void __launch_bounds__(EV_THREADS, 1) eigen_basis_kernel(const double
                 double s = x[i];
                 if (i + 1 < n) s -= lb[i] * x[i + 1];
                 if (i + 2 < n) s -= lc2[i] * x[i + 2];
-                x[i] = s / la[i];
+                x[i] = s * la[i];
             }
         }
         __syncthreads();
@@ -263,25 +276,39 @@ __global__ void __launch_bounds__(EV_THREADS, 1) eigen_basis_kernel(const double
     // ---- 4. back-transform (warp per vector), normalise, sign rule
     for (int h = warp; h < H; h += EV_WARPS) {
         double *y = Y + h * n;
+        double yr[EV_MAXN / 32];                 // entries lane + 32 u of the vector, in registers
+#pragma unroll
+        for (int u = 0; u < EV_MAXN / 32; ++u) yr[u] = lane + 32 * u < n ? y[lane + 32 * u] : 0.0;
         for (int k = n - 3; k >= 0; --k) {
             const double bk = beta[k];
             if (bk == 0.0) continue;
             const double *vk = A + k * LDA;      // reflector entries at k + 1 .. n - 1
+            double vr[EV_MAXN / 32];
             double s = 0.0;
-            for (int j = k + 1 + lane; j < n; j += 32) s += vk[j] * y[j];
+#pragma unroll
+            for (int u = 0; u < EV_MAXN / 32; ++u) {
+                const int j = lane + 32 * u;
+                vr[u] = (j > k && j < n) ? vk[j] : 0.0;
+                s = fma(vr[u], yr[u], s);
+            }
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
             s *= bk;
-            for (int j = k + 1 + lane; j < n; j += 32) y[j] -= s * vk[j];
-            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < EV_MAXN / 32; ++u) yr[u] = fma(-s, vr[u], yr[u]);
         }
         double nr = 0.0, amax = -1.0;
         int imax = n;
-        for (int r = lane; r < n; r += 32) {
-            nr += y[r] * y[r];
-            const double a = fabs(y[r]);
-            if (a > amax) { amax = a; imax = r; }
+#pragma unroll
+        for (int u = 0; u < EV_MAXN / 32; ++u) {
+            const int r = lane + 32 * u;
+            if (r < n) {
+                nr = fma(yr[u], yr[u], nr);
+                const double a = fabs(yr[u]);
+                if (a > amax) { amax = a; imax = r; }
+            }
         }
+        double ymax = 0.0;
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) {
             nr += __shfl_xor_sync(0xffffffffu, nr, off);
@@ -289,9 +316,18 @@ __global__ void __launch_bounds__(EV_THREADS, 1) eigen_basis_kernel(const double
             const int oi = __shfl_xor_sync(0xffffffffu, imax, off);
             if (oa > amax || (oa == amax && oi < imax)) { amax = oa; imax = oi; }
         }
-        const double sgn = y[imax] < 0 ? -1.0 : 1.0;
+#pragma unroll
+        for (int u = 0; u < EV_MAXN / 32; ++u)
+            if (lane + 32 * u == imax) ymax = yr[u];
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) ymax += __shfl_xor_sync(0xffffffffu, ymax, off);   // one lane holds it
+        const double sgn = ymax < 0 ? -1.0 : 1.0;
         const double sc = sgn / sqrt(nr);
-        for (int r = lane; r < n; r += 32) U[(size_t)r * H + h] = sc * y[r];
+#pragma unroll
+        for (int u = 0; u < EV_MAXN / 32; ++u) {
+            const int r = lane + 32 * u;
+            if (r < n) U[(size_t)r * H + h] = sc * yr[u];
+        }
     }
     if (tid == 0 && info) *info = bad;
 }
