@@ -36,16 +36,19 @@ constexpr int EV_MAXY = 8192;          // H * n doubles of eigenvector workspace
 #define RSVD_EV_STOP 0                 // diagnostic builds only: return after phase 1 / 2 / 3
 #endif
 
-__device__ __forceinline__ double ev_block_sum(double x, double *red) {
+// block sum with one barrier: consecutive calls alternate between two partial buffers (red[2][EV_WARPS]),
+// so a buffer is rewritten only after every thread has passed the barrier of the call in between
+__device__ __forceinline__ double ev_block_sum(double x, double *red, int &rb) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *buf = red + rb * EV_WARPS;
+    rb ^= 1;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-    if (lane == 0) red[warp] = x;
+    if (lane == 0) buf[warp] = x;
     __syncthreads();
     double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < EV_WARPS; ++w) t += red[w];      // same order in every thread
-    __syncthreads();
+    for (int w = 0; w < EV_WARPS; ++w) t += buf[w];      // same order in every thread
     return t;
 }
 
@@ -86,6 +89,7 @@ __global__ void __launch_bounds__(EV_THREADS, 1) eigen_basis_kernel(const double
     double *Y = red + 2 * EV_WARPS;              // [H][n] eigenvectors of T, then of C
     __shared__ int bad;
     if (tid == 0) bad = 0;
+    int rb = 0;                                  // ev_block_sum buffer toggle (uniform)
     const double eps = 2.220446049250313e-16;
 
     for (int idx = tid; idx < n * n; idx += EV_THREADS) {
@@ -100,7 +104,7 @@ __global__ void __launch_bounds__(EV_THREADS, 1) eigen_basis_kernel(const double
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1, b0 = k + 1;
         const double xi = tid < m ? A[k * LDA + b0 + tid] : 0.0;
-        const double a2 = ev_block_sum(xi * xi, red);
+        const double a2 = ev_block_sum(xi * xi, red, rb);
         const double x0 = A[k * LDA + b0];
         double alpha = sqrt(a2);
         if (alpha == 0.0) {                      // uniform: nothing to annihilate
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(EV_THREADS, 1) eigen_basis_kernel(const double
         pp += __shfl_xor_sync(0xffffffffu, pp, 2);
         if (pr == 0 && pc < m) p[pc] = bk * pp;
         __syncthreads();
-        const double vp = ev_block_sum(tid < m ? v[tid] * p[tid] : 0.0, red);
+        const double vp = ev_block_sum(tid < m ? v[tid] * p[tid] : 0.0, red, rb);
         const double K = 0.5 * bk * vp;
         if (tid < m) p[tid] -= K * v[tid];       // q = p - K v, in place
         __syncthreads();
@@ -251,7 +255,7 @@ __global__ void __launch_bounds__(EV_THREADS, 1) eigen_basis_kernel(const double
                 }
                 __syncthreads();
             }
-            const double nr = ev_block_sum(tid < n ? yh[tid] * yh[tid] : 0.0, red);
+            const double nr = ev_block_sum(tid < n ? yh[tid] * yh[tid] : 0.0, red, rb);
             const double inv = 1.0 / sqrt(nr);
             if (tid < n) yh[tid] *= inv;
             __syncthreads();
