@@ -167,6 +167,48 @@ def test_device_eigen_solver():
                 assert float(U[:, h - 1] @ Uh[:, h - 1]) > 0.5, (name, H, h)
 
 
+def test_device_eigen_solver_edge_shapes():
+    """rsvd_eigen_basis_device on shapes the configs never reach: R = 1, 2, 3, 5 (no or one Householder
+    step), exactly repeated eigenvalues (a 3-fold and a 4-fold cluster: Gram-Schmidt keeps the cluster
+    vectors orthonormal and spanning their eigenspace), a rank-deficient PSD matrix (a null space of
+    dimension R - 4), and R = 128 with H = 64.  Reference: numpy eigh (LAPACK) of the same matrix."""
+    rng = np.random.default_rng(20220723)
+
+    def check(C, H, tag):
+        R = C.shape[0]
+        U, lam, info = api.eigen_basis_device(cuda(C, torch.float64), H)
+        torch.cuda.synchronize()
+        assert int(info.item()) == 0, tag
+        U, lam = to_np(U), to_np(lam)
+        lr, V = np.linalg.eigh(C)
+        lr, V = lr[::-1], V[:, ::-1]
+        scale = max(abs(lr[0]), abs(lr[-1]), 1e-300)
+        assert np.abs(lam - lr).max() <= 1e-12 * scale, tag
+        assert np.linalg.norm(C @ U - U * lam[None, :H]) <= 1e-12 * scale * max(1.0, np.sqrt(R)), tag
+        assert np.abs(U.T @ U - np.eye(H)).max() <= 1e-12, tag
+        # projector onto each complete cluster of (numerically) equal eigenvalues among the top H
+        h = 0
+        while h < H:
+            g = h
+            while g + 1 < R and abs(lr[g + 1] - lr[h]) <= 1e-9 * scale:
+                g += 1
+            if g < H:
+                P, Pr = U[:, h:g + 1] @ U[:, h:g + 1].T, V[:, h:g + 1] @ V[:, h:g + 1].T
+                assert np.linalg.norm(P - Pr, 2) <= 1e-9, (tag, h, g)
+            h = g + 1
+
+    for R in (1, 2, 3, 5):
+        A = rng.standard_normal((R, R + 2))
+        check(A @ A.T, R, f"R={R}")
+    Qm, _ = np.linalg.qr(rng.standard_normal((16, 16)))
+    ev = np.array([5.0, 3.0, 3.0, 3.0, 2.0, 1.0, 1.0, 1.0, 1.0, 0.5, 0.25, 0.2, 0.1, 0.05, 0.02, 0.01])
+    check((Qm * ev) @ Qm.T, 10, "clusters")
+    A = rng.standard_normal((32, 4))
+    check(A @ A.T, 8, "rank 4")
+    A = rng.standard_normal((128, 300))
+    check(A @ A.T / 300.0, 64, "R=128 H=64")
+
+
 @pytest.fixture(params=[1, 2, 0], ids=["auto", "mma", "ffma"])
 def compress_mode(request):
     """Step 1 kernel choice (rsvd_set_compress_mma): auto, tensor-core projection forced, FFMA2 forced."""
