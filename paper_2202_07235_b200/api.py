@@ -115,6 +115,8 @@ def eigen_basis_device(C: torch.Tensor, H: int, stream=None):
     [R, R].  Returns (U [R, H], lambda [R], info [1] int32) as device tensors, enqueued on the stream;
     info != 0 (read it after synchronising) means U failed the residual test -- use eigen_basis(C)."""
     require_cuda(C)
+    if C.dtype != torch.float64 or C.dim() != 2 or C.shape[0] != C.shape[1]:
+        raise ValueError("eigen_basis_device: C must be a square float64 device tensor")
     C = C.contiguous()
     R = C.shape[0]
     U = torch.empty((R, H), dtype=torch.float64, device=C.device)
