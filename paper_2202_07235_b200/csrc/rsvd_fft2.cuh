@@ -33,6 +33,9 @@ RSVD_TRACE_DEFINE(fft)
 #endif
 #endif
 
+#ifndef RSVD_FFT2_L2PROMO
+#define RSVD_FFT2_L2PROMO 3     // spectrum TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B (CUtensorMapL2promotion)
+#endif
 #ifndef RSVD_FFT2_ONECOL
 #define RSVD_FFT2_ONECOL 0      // 1: pass 1 with one column per warp (1024 threads, <= 64 registers); measured slower
 #endif
@@ -450,7 +453,7 @@ static cudaError_t make_spectrum_tmap2(CUtensorMap *tm, const float *Upk, int64_
     const cuuint32_t box[3] = {(cuuint32_t)C::TB, 1u, (cuuint32_t)C::BOXR};
     const cuuint32_t estr[3] = {1u, 1u, 1u};
     const CUresult r = enc(tm, eb == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(Upk), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, (CUtensorMapL2promotion)RSVD_FFT2_L2PROMO,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }

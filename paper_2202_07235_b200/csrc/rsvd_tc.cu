@@ -86,6 +86,9 @@ const float *tc_scales(const void *blocks, int64_t rows, int Q, int H, int side)
 }
 
 // ------------------------------------------------------------------ contraction kernel
+#ifndef RSVD_TC_L2PROMO
+#define RSVD_TC_L2PROMO 3       // operand TMA L2 promotion (CUtensorMapL2promotion; 3 = 256B)
+#endif
 #ifndef RSVD_WS_POLICY
 #define RSVD_WS_POLICY 2      // spectrum-store L2 policy: 0 default, 1 evict_last, 2 evict_first (measured best)
 #endif
@@ -779,7 +782,7 @@ cudaError_t make_tc_operand_tmap(CUtensorMap *tm, const void *blocks, int64_t ro
     const cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void *>(blocks), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, (CUtensorMapL2promotion)RSVD_TC_L2PROMO,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
